@@ -1,0 +1,660 @@
+// C ABI of the VDAMP hot path (include/vdamp_b200.h): plan, workspace,
+// launch sequences.  Host code is plain C++ over the CUDA runtime; the
+// Python package binds it with ctypes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "vdamp_b200.h"
+#include "vdamp_kernels.cuh"
+
+using namespace vdamp;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Err {
+    int code;
+    std::string msg;
+};
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e__ = (x);                                                             \
+        if (e__ != cudaSuccess)                                                            \
+            throw Err{e__ == cudaErrorMemoryAllocation ? VDAMP_ERR_OOM : VDAMP_ERR_CUDA,   \
+                      std::string(#x) + ": " + cudaGetErrorString(e__)};                   \
+    } while (0)
+
+struct Pass {
+    int a, b, k;      // Haar levels a..b handled by one strip kernel
+    int Ha, Wa;       // level a-1 image dims
+    int logWa;
+    int nstrips;
+};
+
+struct Plan {
+    int H, W, s, B, prec, dev;
+    int S;
+    long long N;
+    Geo geo;
+    std::vector<Pass> passes;       // fine -> coarse
+    size_t csz;                     // bytes per complex element
+    int cw, logcw, ntiles, rowlog;  // column tile width, row_pass rows per CTA
+    // device buffers
+    void* r = nullptr;
+    void* T1 = nullptr;
+    void* T2 = nullptr;
+    void* yg = nullptr;
+    void* pinv = nullptr;
+    std::vector<void*> scratch;     // per pass p >= 1: level a_p - 1 approx image
+    double* par = nullptr;          // [B][S][3]
+    double* parf = nullptr;
+    double* taupart = nullptr;      // [B][ntiles][S]
+    double* prow = nullptr;         // [2s][H]
+    double* pcol = nullptr;         // [2s][W]
+    double* nvar = nullptr;         // [B]
+    void* twH = nullptr;
+    void* twW = nullptr;
+    void* kA = nullptr;             // sort scratch (large subbands only)
+    void* kB = nullptr;
+    void* x0 = nullptr;             // ground truth image (owned copy)
+    void* w0 = nullptr;             // dwt(x0)
+    void* xtmp = nullptr;           // per-iteration finalize image (NMSE)
+    double* trtmp = nullptr;        // [B][S][TRACE_F]
+    bool have_meas = false;
+    bool have_gt = false;
+    size_t bytes = 0;
+    long long launches = 0;
+    // timing
+    bool timing = false;
+    cudaError_t pend = cudaSuccess;   // first launch error, raised by dispatch()
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+    double ms[VDAMP_KERNEL_CLASSES] = {0};
+    long long cls_launches[VDAMP_KERNEL_CLASSES] = {0};
+};
+
+void* dalloc(Plan* p, size_t n) {
+    void* ptr = nullptr;
+    if (n == 0) return nullptr;
+    CK(cudaMalloc(&ptr, n));
+    p->bytes += n;
+    return ptr;
+}
+
+int ilog2(long long v) { int l = 0; while ((1LL << l) < v) ++l; return l; }
+bool pow2(long long v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// ---------------------------------------------------------------- launch --
+struct Launch {
+    Plan* p;
+    int cls;
+    cudaStream_t st;
+    cudaEvent_t e0 = nullptr;
+    Launch(Plan* p_, int c, cudaStream_t s) : p(p_), cls(c), st(s) {
+        if (p->timing) {
+            cudaEvent_t e1;
+            CK(cudaEventCreate(&e0));
+            CK(cudaEventCreate(&e1));
+            CK(cudaEventRecord(e0, st));
+            p->ev.push_back({cls, {e0, e1}});
+        }
+    }
+    ~Launch() {
+        p->launches++;
+        p->cls_launches[cls]++;
+        if (p->timing) cudaEventRecord(p->ev.back().second.second, st);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess && p->pend == cudaSuccess) p->pend = e;
+    }
+};
+
+template <typename K>
+void set_smem(K kern, size_t bytes) {
+    static_assert(sizeof(K) > 0, "");
+    if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+// ------------------------------------------------------------ sequences --
+template <typename R>
+struct Seq {
+    typedef typename CT<R>::T C;
+    Plan* p;
+    cudaStream_t st;
+    C* r() { return (C*)p->r; }
+
+    // Haar synthesis of coefficients `coef` with params `par`; FFT -> T1 when
+    // rowfft, else the image goes to `img`.
+    void synth(const C* coef, const double* par, bool rowfft, C* img, int cls) {
+        const int P = (int)p->passes.size();
+        for (int i = P - 1; i >= 0; --i) {
+            const Pass& ps = p->passes[i];
+            SynArgs<R> a;
+            a.coef = coef; a.par = par;
+            a.asrc = (i == P - 1) ? nullptr : (const C*)p->scratch[i + 1];
+            a.asrc_bs = (i == P - 1) ? 0 : (long long)(p->H >> ps.b) * (p->W >> ps.b);
+            a.a = ps.a; a.b = ps.b; a.k = ps.k; a.Wa = ps.Wa; a.logWa = ps.logWa;
+            a.tw = (const C*)p->twW;
+            const bool last = (i == 0);
+            a.dst = last ? (rowfft ? (C*)p->T1 : img) : (C*)p->scratch[i];
+            a.dst_bs = (long long)ps.Ha * ps.Wa;
+            dim3 grid(ps.nstrips, p->B);
+            const size_t sm = (size_t)(ps.Wa << ps.k) * sizeof(C);
+            Launch L(p, cls, st);
+            if (last && rowfft) {
+                auto k = synth_pass<R, SYN_ROWFFT>;
+                const size_t smf = sm + (size_t)p->W * sizeof(C);
+                set_smem(k, smf);
+                k<<<grid, PNT, smf, st>>>(p->geo, a);
+            } else {
+                auto k = synth_pass<R, SYN_PLAIN>;
+                set_smem(k, sm);
+                k<<<grid, PNT, sm, st>>>(p->geo, a);
+            }
+        }
+    }
+
+    // Haar analysis; input T2 (row IFFT first) when rowifft, else image `img`.
+    // vdamp: coef = Onsager(coef; par) + analysis (in place).
+    void analysis(const C* img, bool rowifft, C* coef, const double* par, bool vdamp_mode, int cls) {
+        const int P = (int)p->passes.size();
+        for (int i = 0; i < P; ++i) {
+            const Pass& ps = p->passes[i];
+            AnaArgs<R> a;
+            const bool first = (i == 0);
+            a.src = first ? (rowifft ? (const C*)p->T2 : img) : (const C*)p->scratch[i];
+            a.src_bs = (long long)ps.Ha * ps.Wa;
+            a.coef = coef; a.par = par;
+            a.adst = (i == P - 1) ? nullptr : (C*)p->scratch[i + 1];
+            a.adst_bs = (i == P - 1) ? 0 : (long long)(p->H >> ps.b) * (p->W >> ps.b);
+            a.a = ps.a; a.b = ps.b; a.k = ps.k; a.Wa = ps.Wa; a.logWa = ps.logWa;
+            a.tw = (const C*)p->twW;
+            dim3 grid(ps.nstrips, p->B);
+            size_t sm = (size_t)(ps.Wa << ps.k) * sizeof(C);
+            Launch L(p, cls, st);
+            if (first && rowifft) {
+                sm += (size_t)p->W * sizeof(C);
+                if (vdamp_mode) {
+                    auto k = analysis_pass<R, ANA_IN_ROWIFFT, ANA_OUT_VDAMP>; set_smem(k, sm);
+                    k<<<grid, PNT, sm, st>>>(p->geo, a);
+                } else {
+                    auto k = analysis_pass<R, ANA_IN_ROWIFFT, ANA_OUT_COEF>; set_smem(k, sm);
+                    k<<<grid, PNT, sm, st>>>(p->geo, a);
+                }
+            } else {
+                if (vdamp_mode) {
+                    auto k = analysis_pass<R, ANA_IN_PLAIN, ANA_OUT_VDAMP>; set_smem(k, sm);
+                    k<<<grid, PNT, sm, st>>>(p->geo, a);
+                } else {
+                    auto k = analysis_pass<R, ANA_IN_PLAIN, ANA_OUT_COEF>; set_smem(k, sm);
+                    k<<<grid, PNT, sm, st>>>(p->geo, a);
+                }
+            }
+        }
+    }
+
+    size_t col_smem() const {
+        const int np = 2 * p->s, pairs = np * p->cw;
+        int G = PNT / pairs; if (G < 1) G = 1;
+        const size_t E = (size_t)p->H << p->logcw;
+        return E * sizeof(C) + (size_t)p->H * sizeof(C) + E * sizeof(double) +
+               (size_t)std::max(pairs * G, PNT) * sizeof(double) + (size_t)pairs * sizeof(double);
+    }
+
+    void col(int mode, const C* src, C* dst, int cls) {
+        ColArgs<R> a;
+        a.src = src; a.dst = dst;
+        a.yg = (const C*)p->yg; a.pinv = (const R*)p->pinv; a.noise_var = p->nvar;
+        a.prow = p->prow; a.pcol = p->pcol; a.taupart = p->taupart;
+        a.tw = (const C*)p->twH; a.cw = p->cw; a.logcw = p->logcw; a.ntiles = p->ntiles;
+        dim3 grid(p->ntiles, p->B);
+        const size_t sm = col_smem();
+        Launch L(p, cls, st);
+        switch (mode) {
+            case COL_FWD:   { auto k = col_pass<R, COL_FWD>;   set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
+            case COL_INV:   { auto k = col_pass<R, COL_INV>;   set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
+            case COL_VDAMP: { auto k = col_pass<R, COL_VDAMP>; set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
+            default:        { auto k = col_pass<R, COL_FINAL>; set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
+        }
+    }
+
+    template <bool INV, bool PRE, bool POST>
+    void rows(const C* src, C* dst, int cls) {
+        dim3 grid(p->H >> p->rowlog, p->B);
+        const size_t sm = ((size_t)p->W << p->rowlog) * sizeof(C) + (size_t)p->W * sizeof(C);
+        auto k = row_pass<R, INV, PRE, POST>;
+        set_smem(k, sm);
+        Launch L(p, cls, st);
+        k<<<grid, PNT, sm, st>>>(p->geo, src, dst, (const C*)p->twW, p->rowlog);
+    }
+
+    void select(const C* rr, const double* tau_in, double* trace, bool use_w0) {
+        SelArgs<R> a;
+        a.r = rr; a.taupart = p->taupart; a.tau_in = tau_in; a.ntiles = p->ntiles;
+        a.par = p->par; a.parf = p->parf; a.trace = trace;
+        a.w0 = use_w0 ? (const C*)p->w0 : nullptr;
+        a.kA = (R*)p->kA; a.kB = (R*)p->kB;
+        dim3 grid(p->S, p->B);
+        const int maxlen = *std::max_element(p->geo.len, p->geo.len + p->S);
+        const size_t sm = (size_t)std::min(maxlen, SCAP) * sizeof(R);
+        auto k = sure_select<R>;
+        set_smem(k, sm);
+        Launch L(p, 3, st);
+        k<<<grid, SNT, sm, st>>>(p->geo, a);
+    }
+
+    void apply(const C* in, C* out, const double* par) {
+        const int maxlen = *std::max_element(p->geo.len, p->geo.len + p->S);
+        dim3 grid((unsigned)std::max(1, std::min(maxlen / 256, 64)), p->S, p->B);
+        Launch L(p, 5, st);
+        apply_params<R><<<grid, 256, 0, st>>>(p->geo, in, out, par);
+    }
+
+    void identity_params() {
+        Launch L(p, 5, st);
+        fill_identity_params<R><<<std::max(1, (p->B * p->S + 255) / 256), 256, 0, st>>>(p->par, p->B * p->S);
+    }
+
+    // one VDAMP iteration from (r, par) -> (r, par)   (src/vdamp.py:99-144)
+    void iteration(double* trace, void* snapshot) {
+        synth(r(), p->par, true, nullptr, 0);
+        col(COL_VDAMP, (const C*)p->T1, (C*)p->T2, 1);
+        analysis(nullptr, true, r(), p->par, true, 2);
+        if (snapshot) CK(cudaMemcpyAsync(snapshot, p->r, (size_t)p->B * p->N * sizeof(C), cudaMemcpyDeviceToDevice, st));
+        select(r(), nullptr, trace, p->have_gt);
+    }
+
+    // x_hat = finalize(soft(r; parf))   (src/vdamp.py:147-150)
+    void finalize_from_r(const double* parf, C* out) {
+        synth(r(), parf, true, nullptr, 4);
+        col(COL_FINAL, (const C*)p->T1, (C*)p->T2, 4);
+        rows<true, false, true>((const C*)p->T2, out, 4);
+    }
+
+    void nmse(const C* x, double* out) {
+        Launch L(p, 5, st);
+        nmse_sums<R><<<p->B, SNT, 0, st>>>(p->geo, x, (const C*)p->x0, out);
+    }
+
+    void run(int n_iters, C* xhat, double* trace, double* nmse_out, void* const* snaps) {
+        CK(cudaMemsetAsync(p->r, 0, (size_t)p->B * p->N * sizeof(C), st));   // r~_0 = 0
+        identity_params();
+        const long long tstride = (long long)p->B * p->S * TRACE_F;
+        for (int it = 0; it < n_iters; ++it) {
+            iteration(trace ? trace + it * tstride : nullptr, snaps ? snaps[it] : nullptr);
+            if (nmse_out) {
+                finalize_from_r(p->parf, (C*)p->xtmp);
+                nmse((const C*)p->xtmp, nmse_out + (long long)it * p->B * VDAMP_NMSE_FIELDS);
+            }
+        }
+        finalize_from_r(p->parf, xhat);
+    }
+};
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return VDAMP_OK;
+    } catch (const Err& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return VDAMP_ERR_ARG;
+    }
+}
+
+Plan* P(vdamp_plan_t h) {
+    if (!h) throw Err{VDAMP_ERR_ARG, "null plan"};
+    return reinterpret_cast<Plan*>(h);
+}
+
+template <typename F>
+void dispatch(Plan* p, void* stream, F&& f) {
+    CK(cudaSetDevice(p->dev));
+    if (p->prec == VDAMP_FP32) { Seq<float> s{p, (cudaStream_t)stream}; f(s); }
+    else                       { Seq<double> s{p, (cudaStream_t)stream}; f(s); }
+    if (p->pend != cudaSuccess) {
+        cudaError_t e = p->pend;
+        p->pend = cudaSuccess;
+        throw Err{VDAMP_ERR_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e)};
+    }
+}
+
+void free_plan(Plan* p) {
+    if (!p) return;
+    cudaSetDevice(p->dev);
+    void* bufs[] = {p->r, p->T1, p->T2, p->yg, p->pinv, p->par, p->parf, p->taupart, p->prow, p->pcol,
+                    p->nvar, p->twH, p->twW, p->kA, p->kB, p->x0, p->w0, p->xtmp, p->trtmp};
+    for (void* b : bufs) if (b) cudaFree(b);
+    for (void* b : p->scratch) if (b) cudaFree(b);
+    for (auto& e : p->ev) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
+    delete p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vdamp_last_error(void) { return g_err.c_str(); }
+int vdamp_abi_version(void) { return 1; }
+
+int vdamp_plan_create(int height, int width, int scales, int batch, int precision, int device,
+                      vdamp_plan_t* out) {
+    Plan* p = nullptr;
+    int rc = guard([&] {
+        if (!out) throw Err{VDAMP_ERR_ARG, "null output handle"};
+        *out = nullptr;
+        if (scales < 1) throw Err{VDAMP_ERR_ARG, "scales must be >= 1, got " + std::to_string(scales)};
+        if (height < 1 || width < 1 || batch < 1) throw Err{VDAMP_ERR_ARG, "height, width and batch must be >= 1"};
+        if (height % (1 << std::min(scales, 30)) || width % (1 << std::min(scales, 30)) || scales > 30)
+            throw Err{VDAMP_ERR_SHAPE, "image shape (" + std::to_string(height) + ", " + std::to_string(width) +
+                                           ") not divisible by 2^" + std::to_string(scales)};
+        if (!pow2(height) || !pow2(width) || height < 2 || width < 2 || height > 2048 || width > 2048)
+            throw Err{VDAMP_ERR_UNSUPPORTED, "this build supports power-of-two image sizes in [2, 2048] only"};
+        if (precision != VDAMP_FP32 && precision != VDAMP_FP64) throw Err{VDAMP_ERR_ARG, "precision must be 0 (fp32) or 1 (fp64)"};
+        if (1 + 3 * scales > MAXS) throw Err{VDAMP_ERR_UNSUPPORTED, "too many scales"};
+        p = new Plan();
+        p->H = height; p->W = width; p->s = scales; p->B = batch; p->prec = precision; p->dev = device;
+        p->S = 1 + 3 * scales;
+        p->N = (long long)height * width;
+        CK(cudaSetDevice(device));
+        Geo& g = p->geo;
+        memset(&g, 0, sizeof(g));
+        g.H = height; g.W = width; g.s = scales; g.S = p->S; g.logH = ilog2(height); g.logW = ilog2(width);
+        g.sign_c = (((height / 2) + (width / 2)) & 1) ? -1 : 1;
+        g.N = p->N;
+        {
+            long long off = 0;
+            const int hs = height >> scales, ws = width >> scales;
+            g.off[0] = 0; g.len[0] = hs * ws; off = (long long)hs * ws;
+            int j = 1;
+            for (int l = scales; l >= 1; --l)
+                for (int o = 0; o < 3; ++o) { g.off[j] = off; g.len[j] = (height >> l) * (width >> l); off += g.len[j]; ++j; }
+        }
+        // Haar passes: each strip of 2^k rows x (W >> lvl) must fit PCAP elements
+        int lvl = 0;
+        while (lvl < scales) {
+            const int Wl = width >> lvl, Hl = height >> lvl;
+            int k = 1;
+            while (lvl + k < scales && ((2LL << k) * Wl) <= PCAP && (2 << k) <= Hl) ++k;
+            if ((1LL << k) * Wl > PCAP) throw Err{VDAMP_ERR_UNSUPPORTED, "image row too wide for a strip"};
+            Pass ps;
+            ps.a = lvl + 1; ps.b = lvl + k; ps.k = k; ps.Ha = Hl; ps.Wa = Wl; ps.logWa = ilog2(Wl);
+            ps.nstrips = Hl >> k;
+            p->passes.push_back(ps);
+            lvl += k;
+        }
+        p->cw = std::max(1, std::min(width, PCAP / height));
+        p->logcw = ilog2(p->cw);
+        p->ntiles = width / p->cw;
+        p->rowlog = 0;
+        while ((2LL << p->rowlog) * width <= PCAP && (2 << p->rowlog) <= height) ++p->rowlog;
+        const size_t cs = precision == VDAMP_FP32 ? sizeof(float2) : sizeof(double2);
+        const size_t rs = precision == VDAMP_FP32 ? sizeof(float) : sizeof(double);
+        p->csz = cs;
+        const size_t img = (size_t)batch * p->N;
+        p->r = dalloc(p, img * cs);
+        p->T1 = dalloc(p, img * cs);
+        p->T2 = dalloc(p, img * cs);
+        p->yg = dalloc(p, img * cs);
+        p->pinv = dalloc(p, img * rs);
+        p->scratch.assign(p->passes.size(), nullptr);
+        for (size_t i = 1; i < p->passes.size(); ++i)
+            p->scratch[i] = dalloc(p, (size_t)batch * p->passes[i].Ha * p->passes[i].Wa * cs);
+        p->par = (double*)dalloc(p, (size_t)batch * p->S * 3 * sizeof(double));
+        p->parf = (double*)dalloc(p, (size_t)batch * p->S * 3 * sizeof(double));
+        p->taupart = (double*)dalloc(p, (size_t)batch * p->ntiles * p->S * sizeof(double));
+        p->prow = (double*)dalloc(p, (size_t)2 * scales * height * sizeof(double));
+        p->pcol = (double*)dalloc(p, (size_t)2 * scales * width * sizeof(double));
+        p->nvar = (double*)dalloc(p, (size_t)batch * sizeof(double));
+        p->twH = dalloc(p, (size_t)height * cs);
+        p->twW = dalloc(p, (size_t)width * cs);
+        p->trtmp = (double*)dalloc(p, (size_t)batch * p->S * TRACE_F * sizeof(double));
+        const int maxlen = *std::max_element(g.len, g.len + p->S);
+        if (maxlen > SCAP) {
+            if (maxlen / SCAP > MAXTILES) throw Err{VDAMP_ERR_UNSUPPORTED, "subband too large"};
+            p->kA = dalloc(p, img * rs);
+            p->kB = dalloc(p, img * rs);
+        }
+        CK(cudaMemset(p->yg, 0, img * cs));
+        CK(cudaMemset(p->pinv, 0, img * rs));
+        if (precision == VDAMP_FP32) {
+            make_twiddles<float><<<(height + 255) / 256, 256>>>((float2*)p->twH, height);
+            make_twiddles<float><<<(width + 255) / 256, 256>>>((float2*)p->twW, width);
+        } else {
+            make_twiddles<double><<<(height + 255) / 256, 256>>>((double2*)p->twH, height);
+            make_twiddles<double><<<(width + 255) / 256, 256>>>((double2*)p->twW, width);
+        }
+        make_profiles<<<dim3((height + 127) / 128, 2 * scales), 128>>>(p->prow, height, scales);
+        make_profiles<<<dim3((width + 127) / 128, 2 * scales), 128>>>(p->pcol, width, scales);
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+        *out = reinterpret_cast<vdamp_plan_t>(p);
+    });
+    if (rc != VDAMP_OK && p) free_plan(p);
+    return rc;
+}
+
+int vdamp_plan_destroy(vdamp_plan_t plan) {
+    return guard([&] { free_plan(reinterpret_cast<Plan*>(plan)); });
+}
+
+int vdamp_plan_layout(vdamp_plan_t plan, int64_t* offsets, int64_t* lengths) {
+    return guard([&] {
+        Plan* p = P(plan);
+        for (int j = 0; j < p->S; ++j) {
+            if (offsets) offsets[j] = p->geo.off[j];
+            if (lengths) lengths[j] = p->geo.len[j];
+        }
+    });
+}
+
+int vdamp_plan_workspace_bytes(vdamp_plan_t plan, size_t* bytes) {
+    return guard([&] { *bytes = P(plan)->bytes; });
+}
+
+int vdamp_set_measurements(vdamp_plan_t plan, const void* y, const int64_t* indices, const int64_t* counts,
+                           const double* probs, int64_t probs_batch_stride, const double* noise_var, void* stream) {
+    return guard([&] {
+        Plan* p = P(plan);
+        if (!y || !indices || !counts || !probs || !noise_var) throw Err{VDAMP_ERR_ARG, "null measurement pointer"};
+        std::vector<long long> offs(p->B + 1, 0);
+        long long maxn = 0;
+        for (int b = 0; b < p->B; ++b) {
+            if (counts[b] < 1 || counts[b] > p->N) throw Err{VDAMP_ERR_ARG, "mask selects no samples or too many"};
+            if (noise_var[b] < 0) throw Err{VDAMP_ERR_ARG, "noise variance must be >= 0"};
+            offs[b + 1] = offs[b] + counts[b];
+            maxn = std::max(maxn, (long long)counts[b]);
+        }
+        CK(cudaSetDevice(p->dev));
+        cudaStream_t st = (cudaStream_t)stream;
+        const size_t img = (size_t)p->B * p->N;
+        const size_t rs = p->prec == VDAMP_FP32 ? sizeof(float) : sizeof(double);
+        CK(cudaMemsetAsync(p->yg, 0, img * p->csz, st));
+        CK(cudaMemsetAsync(p->pinv, 0, img * rs, st));
+        CK(cudaMemcpyAsync(p->nvar, noise_var, p->B * sizeof(double), cudaMemcpyHostToDevice, st));
+        long long* doffs = nullptr;
+        CK(cudaMallocAsync((void**)&doffs, (p->B + 1) * sizeof(long long), st));
+        CK(cudaMemcpyAsync(doffs, offs.data(), (p->B + 1) * sizeof(long long), cudaMemcpyHostToDevice, st));
+        dim3 grid((unsigned)std::min<long long>((maxn + 255) / 256, 1024), p->B);
+        if (p->prec == VDAMP_FP32)
+            scatter_measurements<float><<<grid, 256, 0, st>>>(p->geo, (const float2*)y, (const long long*)indices, doffs,
+                                                              probs, probs_batch_stride, (float2*)p->yg, (float*)p->pinv);
+        else
+            scatter_measurements<double><<<grid, 256, 0, st>>>(p->geo, (const double2*)y, (const long long*)indices, doffs,
+                                                               probs, probs_batch_stride, (double2*)p->yg, (double*)p->pinv);
+        p->launches++;
+        CK(cudaGetLastError());
+        CK(cudaFreeAsync(doffs, st));
+        // the host arrays above must outlive the async copies
+        CK(cudaStreamSynchronize(st));
+        p->have_meas = true;
+    });
+}
+
+int vdamp_set_ground_truth(vdamp_plan_t plan, const void* x0, void* stream) {
+    return guard([&] {
+        Plan* p = P(plan);
+        if (!x0) { p->have_gt = false; return; }
+        CK(cudaSetDevice(p->dev));
+        const size_t bytes = (size_t)p->B * p->N * p->csz;
+        if (!p->x0) { p->x0 = dalloc(p, bytes); p->w0 = dalloc(p, bytes); p->xtmp = dalloc(p, bytes); }
+        CK(cudaMemcpyAsync(p->x0, x0, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+        dispatch(p, stream, [&](auto& s) {
+            typedef typename std::remove_reference<decltype(s)>::type S_;
+            typedef typename S_::C C;
+            s.analysis((const C*)p->x0, false, (C*)p->w0, nullptr, false, 5);
+        });
+        p->have_gt = true;
+    });
+}
+
+int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double* nmse, void* const* snapshots,
+              void* stream) {
+    return guard([&] {
+        Plan* p = P(plan);
+        if (n_iters < 1) throw Err{VDAMP_ERR_ARG, "need at least one iteration, got " + std::to_string(n_iters)};
+        if (!p->have_meas) throw Err{VDAMP_ERR_STATE, "vdamp_set_measurements must be called first"};
+        if (nmse && !p->have_gt) throw Err{VDAMP_ERR_STATE, "NMSE trace requested without ground truth"};
+        if (!x_hat) throw Err{VDAMP_ERR_ARG, "null x_hat"};
+        dispatch(p, stream, [&](auto& s) {
+            typedef typename std::remove_reference<decltype(s)>::type S_;
+            s.run(n_iters, (typename S_::C*)x_hat, trace, nmse, snapshots);
+        });
+    });
+}
+
+int vdamp_iterate(vdamp_plan_t plan, const void* r_tilde, void* r, void* r_tilde_next, void* w_hat, double* trace,
+                  void* stream) {
+    return guard([&] {
+        Plan* p = P(plan);
+        if (!p->have_meas) throw Err{VDAMP_ERR_STATE, "vdamp_set_measurements must be called first"};
+        if (!r_tilde) throw Err{VDAMP_ERR_ARG, "null r_tilde"};
+        dispatch(p, stream, [&](auto& s) {
+            typedef typename std::remove_reference<decltype(s)>::type S_;
+            typedef typename S_::C C;
+            const size_t bytes = (size_t)p->B * p->N * sizeof(C);
+            CK(cudaMemcpyAsync(p->r, r_tilde, bytes, cudaMemcpyDeviceToDevice, s.st));
+            s.identity_params();   // r~ enters as r with (t, alpha, gain) = (0, 0, 1)
+            s.iteration(trace, nullptr);
+            if (r) CK(cudaMemcpyAsync(r, p->r, bytes, cudaMemcpyDeviceToDevice, s.st));
+            if (r_tilde_next) s.apply((const C*)p->r, (C*)r_tilde_next, p->par);
+            if (w_hat) s.apply((const C*)p->r, (C*)w_hat, p->parf);
+        });
+    });
+}
+
+int vdamp_dwt(vdamp_plan_t plan, const void* image, void* coeffs, void* stream) {
+    return guard([&] {
+        Plan* p = P(plan);
+        dispatch(p, stream, [&](auto& s) {
+            typedef typename std::remove_reference<decltype(s)>::type S_;
+            typedef typename S_::C C;
+            s.analysis((const C*)image, false, (C*)coeffs, nullptr, false, 5);
+        });
+    });
+}
+
+int vdamp_idwt(vdamp_plan_t plan, const void* coeffs, void* image, void* stream) {
+    return guard([&] {
+        Plan* p = P(plan);
+        dispatch(p, stream, [&](auto& s) {
+            typedef typename std::remove_reference<decltype(s)>::type S_;
+            typedef typename S_::C C;
+            s.synth((const C*)coeffs, nullptr, false, (C*)image, 5);
+        });
+    });
+}
+
+int vdamp_fft2c(vdamp_plan_t plan, const void* in, void* out, int inverse, void* stream) {
+    return guard([&] {
+        Plan* p = P(plan);
+        dispatch(p, stream, [&](auto& s) {
+            typedef typename std::remove_reference<decltype(s)>::type S_;
+            typedef typename S_::C C;
+            if (inverse) {
+                s.template rows<true, true, false>((const C*)in, (C*)p->T1, 5);
+                s.col(COL_INV, (const C*)p->T1, (C*)out, 5);
+            } else {
+                s.template rows<false, true, false>((const C*)in, (C*)p->T1, 5);
+                s.col(COL_FWD, (const C*)p->T1, (C*)out, 5);
+            }
+        });
+    });
+}
+
+int vdamp_finalize(vdamp_plan_t plan, const void* w_hat, void* x_hat, void* stream) {
+    return guard([&] {
+        Plan* p = P(plan);
+        if (!p->have_meas) throw Err{VDAMP_ERR_STATE, "vdamp_set_measurements must be called first"};
+        dispatch(p, stream, [&](auto& s) {
+            typedef typename std::remove_reference<decltype(s)>::type S_;
+            typedef typename S_::C C;
+            s.synth((const C*)w_hat, nullptr, true, nullptr, 4);
+            s.col(COL_FINAL, (const C*)p->T1, (C*)p->T2, 4);
+            s.template rows<true, false, true>((const C*)p->T2, (C*)x_hat, 4);
+        });
+    });
+}
+
+int vdamp_denoise_colored(vdamp_plan_t plan, const void* r, const double* tau, void* w_hat, double* trace,
+                          void* stream) {
+    return guard([&] {
+        Plan* p = P(plan);
+        if (!r || !tau) throw Err{VDAMP_ERR_ARG, "null r or tau"};
+        dispatch(p, stream, [&](auto& s) {
+            typedef typename std::remove_reference<decltype(s)>::type S_;
+            typedef typename S_::C C;
+            s.select((const C*)r, tau, trace, false);
+            if (w_hat) s.apply((const C*)r, (C*)w_hat, p->parf);
+        });
+    });
+}
+
+int vdamp_set_timing(vdamp_plan_t plan, int enable) {
+    return guard([&] {
+        Plan* p = P(plan);
+        p->timing = enable != 0;
+        for (auto& e : p->ev) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
+        p->ev.clear();
+        for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) { p->ms[c] = 0; p->cls_launches[c] = 0; }
+    });
+}
+
+int vdamp_kernel_times(vdamp_plan_t plan, double* ms, int64_t* launches) {
+    return guard([&] {
+        Plan* p = P(plan);
+        for (auto& e : p->ev) {
+            CK(cudaEventSynchronize(e.second.second));
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, e.second.first, e.second.second));
+            p->ms[e.first] += t;
+            cudaEventDestroy(e.second.first);
+            cudaEventDestroy(e.second.second);
+        }
+        p->ev.clear();
+        for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) {
+            if (ms) ms[c] = p->ms[c];
+            if (launches) launches[c] = p->cls_launches[c];
+        }
+    });
+}
+
+int vdamp_launch_count(vdamp_plan_t plan, int64_t* count, int reset) {
+    return guard([&] {
+        Plan* p = P(plan);
+        if (count) *count = p->launches;
+        if (reset) p->launches = 0;
+    });
+}
+
+}  // extern "C"

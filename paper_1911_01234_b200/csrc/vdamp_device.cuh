@@ -1,0 +1,242 @@
+// Device building blocks for the VDAMP hot path on sm_100a:
+// complex helpers, the shared-memory Stockham FFT, Haar lifting steps,
+// the Onsager/soft-threshold apply, and deterministic block scans.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+namespace vdamp {
+
+template <typename R> struct CT;
+template <> struct CT<float>  { typedef float2 T; };
+template <> struct CT<double> { typedef double2 T; };
+
+template <typename C> __device__ __forceinline__ C mk(decltype(C::x) a, decltype(C::x) b) { C c; c.x = a; c.y = b; return c; }
+template <typename C> __device__ __forceinline__ C cadd(C a, C b) { return mk<C>(a.x + b.x, a.y + b.y); }
+template <typename C> __device__ __forceinline__ C csub(C a, C b) { return mk<C>(a.x - b.x, a.y - b.y); }
+template <typename C> __device__ __forceinline__ C cmul(C a, C b) { return mk<C>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+template <typename C, typename R> __device__ __forceinline__ C cscale(C a, R s) { return mk<C>(a.x * s, a.y * s); }
+template <typename C> __device__ __forceinline__ C cconj(C a) { return mk<C>(a.x, -a.y); }
+// multiply by -i (forward) or +i (inverse)
+template <typename C, bool INV> __device__ __forceinline__ C cmul_mi(C a) {
+    return INV ? mk<C>(-a.y, a.x) : mk<C>(a.y, -a.x);
+}
+
+// |r| exactly as used by both the SURE scan and the apply (they must agree).
+__device__ __forceinline__ float cmag(float2 a) { return hypotf(a.x, a.y); }
+__device__ __forceinline__ double cmag(double2 a) { return hypot(a.x, a.y); }
+
+// Haar taps: the reference divides by sqrt(2) (src/wavelet.py:109-128); the
+// fp64 instantiation does the same so it tracks numpy to the last bit, the
+// fp32 one multiplies by the rounded reciprocal.
+template <typename R> struct Haar;
+template <> struct Haar<double> {
+    static __device__ __forceinline__ double2 sum(double2 a, double2 b) {
+        return mk<double2>((a.x + b.x) / 1.4142135623730951, (a.y + b.y) / 1.4142135623730951);
+    }
+    static __device__ __forceinline__ double2 dif(double2 a, double2 b) {
+        return mk<double2>((a.x - b.x) / 1.4142135623730951, (a.y - b.y) / 1.4142135623730951);
+    }
+};
+template <> struct Haar<float> {
+    static __device__ __forceinline__ float2 sum(float2 a, float2 b) {
+        return mk<float2>((a.x + b.x) * 0.70710678118654752f, (a.y + b.y) * 0.70710678118654752f);
+    }
+    static __device__ __forceinline__ float2 dif(float2 a, float2 b) {
+        return mk<float2>((a.x - b.x) * 0.70710678118654752f, (a.y - b.y) * 0.70710678118654752f);
+    }
+};
+
+// Onsager-corrected soft threshold of one coefficient (src/vdamp.py:125-131,
+// src/denoise.py:166-168):  (r * max(1 - t/|r|, 0) - alpha * r) * gain,
+// |r| == t -> shrunk to 0.  (t, alpha, gain) = (0, 0, 1) is the identity.
+template <typename R, typename C>
+__device__ __forceinline__ C onsager(C r, R t, R alpha, R gain) {
+    R m = cmag(r);
+    R sh = (m > t) ? (R(1) - t / m) : R(0);
+    R wx = r.x * sh, wy = r.y * sh;
+    return mk<C>((wx - alpha * r.x) * gain, (wy - alpha * r.y) * gain);
+}
+
+// ---------------------------------------------------------------------------
+// Stockham radix-4/2 FFT over `nseq` sequences of length L held in shared
+// memory. Element e of sequence q lives at buf[q*sstr + e*estr].  Every
+// thread keeps its butterflies in registers between the load and the store
+// half of a pass, so the transform is in place.  SEQ_FAST maps consecutive
+// threads to consecutive sequences (column tiles: conflict-free), otherwise
+// to consecutive elements of one sequence (rows).  tw[m] = exp(-2 pi i m / L).
+// ---------------------------------------------------------------------------
+template <typename C, bool INV, int NT, int MAXB, bool SEQ_FAST>
+__device__ __forceinline__ void fft_pass_r4(C* buf, int logL, int logNs, int lognseq,
+                                            int sstr, int estr, const C* tw) {
+    const int logQ = logL - 2;
+    const int Q = 1 << logQ;
+    const int Ns = 1 << logNs;
+    const int total = 1 << (lognseq + logQ);
+    const int twshift = logL - logNs - 2;
+    C v[MAXB][4];
+#pragma unroll
+    for (int i = 0; i < MAXB; ++i) {
+        int bf = threadIdx.x + i * NT;
+        if (bf < total) {
+            int q, j;
+            if (SEQ_FAST) { q = bf & ((1 << lognseq) - 1); j = bf >> lognseq; }
+            else          { q = bf >> logQ; j = bf & (Q - 1); }
+            const C* base = buf + q * sstr;
+            int k = j & (Ns - 1);
+            C a0 = base[(j) * estr];
+            C a1 = base[(j + Q) * estr];
+            C a2 = base[(j + 2 * Q) * estr];
+            C a3 = base[(j + 3 * Q) * estr];
+            if (k) {
+                C w1 = tw[(k) << twshift], w2 = tw[(2 * k) << twshift], w3 = tw[(3 * k) << twshift];
+                if (INV) { w1 = cconj(w1); w2 = cconj(w2); w3 = cconj(w3); }
+                a1 = cmul(a1, w1); a2 = cmul(a2, w2); a3 = cmul(a3, w3);
+            }
+            C b0 = cadd(a0, a2), b1 = csub(a0, a2), b2 = cadd(a1, a3);
+            C b3 = cmul_mi<C, INV>(csub(a1, a3));
+            v[i][0] = cadd(b0, b2);
+            v[i][1] = cadd(b1, b3);
+            v[i][2] = csub(b0, b2);
+            v[i][3] = csub(b1, b3);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < MAXB; ++i) {
+        int bf = threadIdx.x + i * NT;
+        if (bf < total) {
+            int q, j;
+            if (SEQ_FAST) { q = bf & ((1 << lognseq) - 1); j = bf >> lognseq; }
+            else          { q = bf >> logQ; j = bf & (Q - 1); }
+            C* base = buf + q * sstr;
+            int k = j & (Ns - 1);
+            int d = ((j - k) << 2) + k;
+            base[(d) * estr] = v[i][0];
+            base[(d + Ns) * estr] = v[i][1];
+            base[(d + 2 * Ns) * estr] = v[i][2];
+            base[(d + 3 * Ns) * estr] = v[i][3];
+        }
+    }
+    __syncthreads();
+}
+
+template <typename C, bool INV, int NT, int MAXB, bool SEQ_FAST>
+__device__ __forceinline__ void fft_pass_r2(C* buf, int logL, int lognseq, int sstr, int estr) {
+    // first pass only (Ns = 1): no twiddles
+    const int logQ = logL - 1;
+    const int Q = 1 << logQ;
+    const int total = 1 << (lognseq + logQ);
+    C v[MAXB][2];
+#pragma unroll
+    for (int i = 0; i < MAXB; ++i) {
+        int bf = threadIdx.x + i * NT;
+        if (bf < total) {
+            int q, j;
+            if (SEQ_FAST) { q = bf & ((1 << lognseq) - 1); j = bf >> lognseq; }
+            else          { q = bf >> logQ; j = bf & (Q - 1); }
+            const C* base = buf + q * sstr;
+            C a0 = base[j * estr], a1 = base[(j + Q) * estr];
+            v[i][0] = cadd(a0, a1);
+            v[i][1] = csub(a0, a1);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < MAXB; ++i) {
+        int bf = threadIdx.x + i * NT;
+        if (bf < total) {
+            int q, j;
+            if (SEQ_FAST) { q = bf & ((1 << lognseq) - 1); j = bf >> lognseq; }
+            else          { q = bf >> logQ; j = bf & (Q - 1); }
+            C* base = buf + q * sstr;
+            base[(2 * j) * estr] = v[i][0];
+            base[(2 * j + 1) * estr] = v[i][1];
+        }
+    }
+    __syncthreads();
+}
+
+// Full unnormalised DFT (sign -1 forward, +1 inverse) of every sequence.
+// CAP = max nseq * L handled by the caller's block.
+template <typename C, bool INV, int NT, int CAP, bool SEQ_FAST>
+__device__ __forceinline__ void block_fft(C* buf, int logL, int lognseq, int sstr, int estr, const C* tw) {
+    int logNs = 0;
+    if (logL & 1) {
+        fft_pass_r2<C, INV, NT, (CAP / 2 + NT - 1) / NT, SEQ_FAST>(buf, logL, lognseq, sstr, estr);
+        logNs = 1;
+    }
+    for (; logNs < logL; logNs += 2)
+        fft_pass_r4<C, INV, NT, (CAP / 4 + NT - 1) / NT, SEQ_FAST>(buf, logL, logNs, lognseq, sstr, estr, tw);
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic block reductions / scans over doubles (fixed shuffle trees).
+// ---------------------------------------------------------------------------
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x < 32) {
+        t = (l < NT / 32) ? sh[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (l == 0) sh[0] = t;
+    }
+    __syncthreads();
+    t = sh[0];
+    __syncthreads();
+    return t;
+}
+
+// Exclusive warp scan without subtraction (the inverse-magnitude sums span
+// many decades, so "inclusive - own" would cancel catastrophically).
+template <bool REV>
+__device__ __forceinline__ double warp_excl_scan(double v, double& total) {
+    const int l = threadIdx.x & 31;
+    double inc = v;
+    if (!REV) {
+        for (int o = 1; o < 32; o <<= 1) { double u = __shfl_up_sync(0xffffffffu, inc, o); if (l >= o) inc += u; }
+        double ex = __shfl_up_sync(0xffffffffu, inc, 1);
+        total = __shfl_sync(0xffffffffu, inc, 31);
+        return l == 0 ? 0.0 : ex;
+    } else {
+        for (int o = 1; o < 32; o <<= 1) { double u = __shfl_down_sync(0xffffffffu, inc, o); if (l + o < 32) inc += u; }
+        double ex = __shfl_down_sync(0xffffffffu, inc, 1);
+        total = __shfl_sync(0xffffffffu, inc, 0);
+        return l == 31 ? 0.0 : ex;
+    }
+}
+
+// Exclusive scan in thread order (REV = false: sum over lower threads;
+// REV = true: sum over higher threads). `sh` needs NT/32 doubles.
+template <int NT, bool REV>
+__device__ __forceinline__ double block_excl_scan(double v, double* sh) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    double wtot;
+    double ex = warp_excl_scan<REV>(v, wtot);
+    __syncthreads();
+    if (l == 0) sh[w] = wtot;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int NW = NT / 32;
+        double t = (l < NW) ? sh[l] : 0.0;
+        double dummy;
+        double wex = warp_excl_scan<REV>(t, dummy);
+        if (REV && NW < 32) {
+            // lanes >= NW hold zeros; the reverse exclusive scan is unaffected
+        }
+        __syncwarp();
+        if (l < NW) sh[l] = wex;
+    }
+    __syncthreads();
+    double r = sh[w] + ex;
+    __syncthreads();
+    return r;
+}
+
+}  // namespace vdamp

@@ -1,0 +1,741 @@
+// VDAMP hot-path kernels (sm_100a).  One iteration of Algorithm 1
+// (/root/reference/pkg/src/csmri/vdamp.py:99-144) is four kernel stages:
+//
+//   K1 synth_pass   (coarse -> fine):  r~ = Onsager(r_{k-1}) ; Haar synthesis ;
+//                   (-1)^(n1+n2) ; row FFT                       -> T1
+//   K2 col_pass     column FFT ; z = y - M F x ; v = P^-1 z ; tau partials ;
+//                   column IFFT                                   -> T2
+//   K3 analysis_pass (fine -> coarse): row IFFT ; sign ; Haar analysis ;
+//                   r_k = Onsager(r_{k-1}) + Psi u  (in place)    -> r
+//   K4 sure_select  per (subband, image): exact SURE argmin, alpha, gain
+//
+// Haar is block-local, so a strip of 2^k image rows maps to contiguous row
+// ranges of every subband (layout of src/wavelet.py:52-61); deeper levels
+// than fit one strip are handled by extra coarse passes through a small
+// scratch image.  The centred FFT is a plain FFT with (-1)^(n1+n2) sign
+// modulation; the output sign is folded into y at setup.
+#pragma once
+#include "vdamp_device.cuh"
+
+namespace vdamp {
+
+constexpr int MAXS = 64;          // subbands supported (scales <= 21)
+constexpr int PNT = 256;          // threads of strip / column kernels
+constexpr int PCAP = 4096;        // complex elements per strip / column tile
+constexpr int SNT = 1024;         // threads of the SURE kernel
+constexpr int SCAP = 16384;       // magnitudes sorted in shared memory at once
+constexpr int MAXTILES = 256;     // SCAP-tiles per subband (n <= 4M)
+constexpr double ALPHA_CLAMP = 1.0 - 1e-9;   // src/vdamp.py:25
+constexpr double TAU_FLOOR = 1e-300;         // src/vdamp.py:118
+constexpr int TRACE_F = 8;
+
+struct Geo {
+    int H, W, s, S, logH, logW;
+    int sign_c;                   // (-1)^(H/2 + W/2)
+    long long N;
+    long long off[MAXS];
+    int len[MAXS];
+};
+
+__host__ __device__ inline int band_of(int s, int level, int orient) { return 1 + 3 * (s - level) + orient; }
+
+// ------------------------------------------------------------------ K1 ----
+enum { SYN_PLAIN = 0, SYN_ROWFFT = 1 };
+
+template <typename R>
+struct SynArgs {
+    const typename CT<R>::T* coef;   // [B][N]
+    const double* par;               // [B][S][3] (t, alpha, gain) or null = identity
+    const typename CT<R>::T* asrc;   // approx_b image (null -> subband 0 of coef)
+    typename CT<R>::T* dst;          // level a-1 image / scratch / T1
+    const typename CT<R>::T* tw;     // twiddles, length W (ROWFFT)
+    int a, b, k, Wa, logWa;
+    long long asrc_bs, dst_bs;
+};
+
+template <typename R, int MODE>
+__global__ void __launch_bounds__(PNT) synth_pass(Geo g, SynArgs<R> p) {
+    typedef typename CT<R>::T C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* buf = reinterpret_cast<C*>(smem_raw);
+    const int st = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
+    const int k = p.k, Wa = p.Wa;
+    const C* coef = p.coef + (long long)bi * g.N;
+    const double* par = p.par ? p.par + (long long)bi * g.S * 3 : nullptr;
+    C* tws = buf + (Wa << k);
+    if (MODE == SYN_ROWFFT)
+        for (int e = tid; e < g.W; e += PNT) tws[e] = p.tw[e];
+
+    // gather the strip's coefficients into the mosaic (Onsager applied)
+    for (int q = 1; q <= k; ++q) {
+        const int l = p.a + q - 1;
+        const int logCq = p.logWa - q, Cq = 1 << logCq, Rq = 1 << (k - q);
+        const int cnt = Rq * Cq;
+        for (int o = 0; o < 3; ++o) {
+            const int j = band_of(g.s, l, o);
+            R t = 0, al = 0, ga = 1;
+            if (par) { t = (R)par[3 * j]; al = (R)par[3 * j + 1]; ga = (R)par[3 * j + 2]; }
+            const C* src = coef + g.off[j] + (long long)st * cnt;
+            const int r0 = (o >= 1) ? Rq : 0, c0 = (o != 1) ? Cq : 0;
+            for (int e = tid; e < cnt; e += PNT) {
+                C v = src[e];
+                if (par) v = onsager<R, C>(v, t, al, ga);
+                buf[(r0 + (e >> logCq)) * Wa + c0 + (e & (Cq - 1))] = v;
+            }
+        }
+    }
+    {
+        const int Ck = Wa >> k;
+        if (p.asrc) {
+            const C* src = p.asrc + (long long)bi * p.asrc_bs + (long long)st * Ck;
+            for (int e = tid; e < Ck; e += PNT) buf[e] = src[e];
+        } else {
+            R t = 0, al = 0, ga = 1;
+            if (par) { t = (R)par[0]; al = (R)par[1]; ga = (R)par[2]; }
+            const C* src = coef + g.off[0] + (long long)st * Ck;
+            for (int e = tid; e < Ck; e += PNT) {
+                C v = src[e];
+                if (par) v = onsager<R, C>(v, t, al, ga);
+                buf[e] = v;
+            }
+        }
+    }
+    __syncthreads();
+
+    // synthesis, coarse to fine (src/wavelet.py:118-129)
+    constexpr int MQ = PCAP / 4 / PNT;
+    for (int q = k; q >= 1; --q) {
+        const int logCq = p.logWa - q, Cq = 1 << logCq, Rq = 1 << (k - q);
+        const int P = Rq * Cq;
+        C o[MQ][4];
+#pragma unroll
+        for (int i = 0; i < MQ; ++i) {
+            const int e = tid + i * PNT;
+            if (e < P) {
+                const int ii = e >> logCq, jj = e & (Cq - 1);
+                C ll = buf[ii * Wa + jj], lh = buf[ii * Wa + Cq + jj];
+                C hl = buf[(Rq + ii) * Wa + jj], hh = buf[(Rq + ii) * Wa + Cq + jj];
+                C lo0 = Haar<R>::sum(ll, lh), lo1 = Haar<R>::dif(ll, lh);
+                C hi0 = Haar<R>::sum(hl, hh), hi1 = Haar<R>::dif(hl, hh);
+                o[i][0] = Haar<R>::sum(lo0, hi0);
+                o[i][1] = Haar<R>::sum(lo1, hi1);
+                o[i][2] = Haar<R>::dif(lo0, hi0);
+                o[i][3] = Haar<R>::dif(lo1, hi1);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < MQ; ++i) {
+            const int e = tid + i * PNT;
+            if (e < P) {
+                const int ii = e >> logCq, jj = e & (Cq - 1);
+                C* d = buf + (2 * ii) * Wa + 2 * jj;
+                d[0] = o[i][0]; d[1] = o[i][1]; d[Wa] = o[i][2]; d[Wa + 1] = o[i][3];
+            }
+        }
+        __syncthreads();
+    }
+
+    const int E = Wa << k;
+    C* dst = p.dst + (long long)bi * p.dst_bs + (long long)st * E;
+    if (MODE == SYN_PLAIN) {
+        for (int e = tid; e < E; e += PNT) dst[e] = buf[e];
+        return;
+    }
+    // (-1)^(n1+n2) then row FFT (unitary 1/sqrt(W))
+    const int rowbase = st << k;
+    for (int e = tid; e < E; e += PNT) {
+        const int n1 = rowbase + (e >> p.logWa), n2 = e & (Wa - 1);
+        if ((n1 + n2) & 1) { C v = buf[e]; buf[e] = mk<C>(-v.x, -v.y); }
+    }
+    __syncthreads();
+    block_fft<C, false, PNT, PCAP, false>(buf, g.logW, k, Wa, 1, tws);
+    const R sc = R(1) / sqrt(R(g.W));
+    for (int e = tid; e < E; e += PNT) dst[e] = cscale(buf[e], sc);
+}
+
+// ------------------------------------------------------------------ K3 ----
+enum { ANA_IN_PLAIN = 0, ANA_IN_ROWIFFT = 1 };
+enum { ANA_OUT_COEF = 0, ANA_OUT_VDAMP = 1 };
+
+template <typename R>
+struct AnaArgs {
+    const typename CT<R>::T* src;    // level a-1 image / scratch / T2
+    typename CT<R>::T* coef;         // [B][N] coefficients (in/out for VDAMP)
+    const double* par;               // Onsager params of r_{k-1} (VDAMP)
+    typename CT<R>::T* adst;         // approx_b scratch (null -> subband 0)
+    const typename CT<R>::T* tw;
+    int a, b, k, Wa, logWa;
+    long long src_bs, adst_bs;
+};
+
+template <typename R, int IN, int OUT>
+__global__ void __launch_bounds__(PNT) analysis_pass(Geo g, AnaArgs<R> p) {
+    typedef typename CT<R>::T C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* buf = reinterpret_cast<C*>(smem_raw);
+    const int st = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
+    const int k = p.k, Wa = p.Wa;
+    const int E = Wa << k;
+    const C* src = p.src + (long long)bi * p.src_bs + (long long)st * E;
+    if (IN == ANA_IN_PLAIN) {
+        for (int e = tid; e < E; e += PNT) buf[e] = src[e];
+        __syncthreads();
+    } else {
+        C* tws = buf + E;
+        for (int e = tid; e < g.W; e += PNT) tws[e] = p.tw[e];
+        for (int e = tid; e < E; e += PNT) buf[e] = src[e];
+        __syncthreads();
+        block_fft<C, true, PNT, PCAP, false>(buf, g.logW, k, Wa, 1, tws);
+        // unitary scale and the output sign c * (-1)^(n1+n2) of ifft2c
+        const R sc = R(1) / sqrt(R(g.W));
+        const int rowbase = st << k;
+        for (int e = tid; e < E; e += PNT) {
+            const int n1 = rowbase + (e >> p.logWa), n2 = e & (Wa - 1);
+            const R s = (((n1 + n2) & 1) ? -sc : sc) * (R)g.sign_c;
+            buf[e] = cscale(buf[e], s);
+        }
+        __syncthreads();
+    }
+
+    // analysis, fine to coarse (src/wavelet.py:107-115)
+    constexpr int MQ = PCAP / 4 / PNT;
+    for (int q = 1; q <= k; ++q) {
+        const int logCq = p.logWa - q, Cq = 1 << logCq, Rq = 1 << (k - q);
+        const int P = Rq * Cq;
+        C o[MQ][4];
+#pragma unroll
+        for (int i = 0; i < MQ; ++i) {
+            const int e = tid + i * PNT;
+            if (e < P) {
+                const int ii = e >> logCq, jj = e & (Cq - 1);
+                const C* s0 = buf + (2 * ii) * Wa + 2 * jj;
+                C x00 = s0[0], x01 = s0[1], x10 = s0[Wa], x11 = s0[Wa + 1];
+                C lo0 = Haar<R>::sum(x00, x10), hi0 = Haar<R>::dif(x00, x10);
+                C lo1 = Haar<R>::sum(x01, x11), hi1 = Haar<R>::dif(x01, x11);
+                o[i][0] = Haar<R>::sum(lo0, lo1);   // ll
+                o[i][1] = Haar<R>::dif(lo0, lo1);   // lh  horizontal
+                o[i][2] = Haar<R>::sum(hi0, hi1);   // hl  vertical
+                o[i][3] = Haar<R>::dif(hi0, hi1);   // hh  diagonal
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < MQ; ++i) {
+            const int e = tid + i * PNT;
+            if (e < P) {
+                const int ii = e >> logCq, jj = e & (Cq - 1);
+                buf[ii * Wa + jj] = o[i][0];
+                buf[ii * Wa + Cq + jj] = o[i][1];
+                buf[(Rq + ii) * Wa + jj] = o[i][2];
+                buf[(Rq + ii) * Wa + Cq + jj] = o[i][3];
+            }
+        }
+        __syncthreads();
+    }
+
+    // scatter the mosaic back to the flat layout
+    C* coef = p.coef + (long long)bi * g.N;
+    const double* par = (OUT == ANA_OUT_VDAMP) ? p.par + (long long)bi * g.S * 3 : nullptr;
+    for (int q = 1; q <= k; ++q) {
+        const int l = p.a + q - 1;
+        const int logCq = p.logWa - q, Cq = 1 << logCq, Rq = 1 << (k - q);
+        const int cnt = Rq * Cq;
+        for (int o = 0; o < 3; ++o) {
+            const int j = band_of(g.s, l, o);
+            C* d = coef + g.off[j] + (long long)st * cnt;
+            const int r0 = (o >= 1) ? Rq : 0, c0 = (o != 1) ? Cq : 0;
+            R t = 0, al = 0, ga = 1;
+            if (OUT == ANA_OUT_VDAMP) { t = (R)par[3 * j]; al = (R)par[3 * j + 1]; ga = (R)par[3 * j + 2]; }
+            for (int e = tid; e < cnt; e += PNT) {
+                C u = buf[(r0 + (e >> logCq)) * Wa + c0 + (e & (Cq - 1))];
+                if (OUT == ANA_OUT_VDAMP) u = cadd(onsager<R, C>(d[e], t, al, ga), u);
+                d[e] = u;
+            }
+        }
+    }
+    const int Ck = Wa >> k;
+    if (p.adst) {
+        C* d = p.adst + (long long)bi * p.adst_bs + (long long)st * Ck;
+        for (int e = tid; e < Ck; e += PNT) d[e] = buf[e];
+    } else {
+        C* d = coef + g.off[0] + (long long)st * Ck;
+        R t = 0, al = 0, ga = 1;
+        if (OUT == ANA_OUT_VDAMP) { t = (R)par[0]; al = (R)par[1]; ga = (R)par[2]; }
+        for (int e = tid; e < Ck; e += PNT) {
+            C u = buf[e];
+            if (OUT == ANA_OUT_VDAMP) u = cadd(onsager<R, C>(d[e], t, al, ga), u);
+            d[e] = u;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K2 ----
+enum { COL_FWD = 0, COL_INV = 1, COL_VDAMP = 2, COL_FINAL = 3 };
+
+template <typename R>
+struct ColArgs {
+    const typename CT<R>::T* src;    // [B][H][W]
+    typename CT<R>::T* dst;          // [B][H][W]
+    const typename CT<R>::T* yg;     // sign-folded y on the grid (0 off mask)
+    const R* pinv;                   // 1/p on the grid, 0 off mask
+    const double* noise_var;         // [B]
+    const double* prow;              // [2s][H] row (axis-0) profiles
+    const double* pcol;              // [2s][W] column profiles
+    double* taupart;                 // [B][ntiles][S]
+    const typename CT<R>::T* tw;     // length H
+    int cw, logcw, ntiles;
+};
+
+__device__ __forceinline__ void band_profiles(int s, int j, int& prow, int& pcol) {
+    if (j == 0) { prow = 2 * (s - 1); pcol = 2 * (s - 1); return; }
+    const int l = s - (j - 1) / 3, o = (j - 1) % 3;
+    prow = 2 * (l - 1) + (o >= 1 ? 1 : 0);
+    pcol = 2 * (l - 1) + (o != 1 ? 1 : 0);
+}
+
+template <typename R, int MODE>
+__global__ void __launch_bounds__(PNT) col_pass(Geo g, ColArgs<R> p) {
+    typedef typename CT<R>::T C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* buf = reinterpret_cast<C*>(smem_raw);
+    const int H = g.H, W = g.W, cw = p.cw, lc = p.logcw;
+    const int E = H << lc;
+    C* tws = buf + E;
+    double* wv = reinterpret_cast<double*>(tws + H);
+    const int tile = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
+    const int c0 = tile << lc;
+    const long long ib = (long long)bi * g.N;
+    for (int e = tid; e < H; e += PNT) tws[e] = p.tw[e];
+    for (int e = tid; e < E; e += PNT) buf[e] = p.src[ib + (long long)(e >> lc) * W + c0 + (e & (cw - 1))];
+    __syncthreads();
+    if (MODE == COL_INV) block_fft<C, true, PNT, PCAP, true>(buf, g.logH, lc, 1, cw, tws);
+    else                 block_fft<C, false, PNT, PCAP, true>(buf, g.logH, lc, 1, cw, tws);
+    const R sc = R(1) / sqrt(R(H));
+    if (MODE == COL_FWD || MODE == COL_INV) {
+        // centred output sign c * (-1)^(k1+k2)
+        for (int e = tid; e < E; e += PNT) {
+            const int n = e >> lc, col = c0 + (e & (cw - 1));
+            const R s = (((n + col) & 1) ? -sc : sc) * (R)g.sign_c;
+            p.dst[ib + (long long)n * W + col] = cscale(buf[e], s);
+        }
+        return;
+    }
+    const R cs = (R)g.sign_c;
+    const double nv = (MODE == COL_VDAMP) ? p.noise_var[bi] : 0.0;
+    for (int e = tid; e < E; e += PNT) {
+        const long long gi = ib + (long long)(e >> lc) * W + c0 + (e & (cw - 1));
+        const C X = cscale(buf[e], sc * cs);     // c * FFT2u, so (-1)^(k1+k2) X_centred
+        const R pv = p.pinv[gi];
+        C v;
+        if (MODE == COL_VDAMP) {
+            double w = 0.0;
+            if (pv != R(0)) {
+                const C zc = csub(p.yg[gi], X);          // (-1)^(k1+k2) z  (src/vdamp.py:112)
+                v = cscale(zc, pv);                      // P^-1 z           (src/vdamp.py:113)
+                const double pd = (double)pv;
+                const double z2 = (double)zc.x * (double)zc.x + (double)zc.y * (double)zc.y;
+                w = pd * ((pd - 1.0) * z2 + nv);         // tau weight       (src/vdamp.py:74-75)
+            } else {
+                v = mk<C>(R(0), R(0));
+            }
+            wv[e] = w;
+        } else {  // COL_FINAL: measured k-space where sampled (src/vdamp.py:147-150)
+            v = (pv != R(0)) ? p.yg[gi] : X;
+        }
+        buf[e] = v;
+    }
+    __syncthreads();
+    block_fft<C, true, PNT, PCAP, true>(buf, g.logH, lc, 1, cw, tws);
+    for (int e = tid; e < E; e += PNT)
+        p.dst[ib + (long long)(e >> lc) * W + c0 + (e & (cw - 1))] = cscale(buf[e], sc);
+    if (MODE != COL_VDAMP) return;
+
+    // tau partials: tau_j = sum_w a_j(w1) b_j(w2) weight(w)  (separable |F psi_j|^2)
+    double* part = wv + E;                        // max(PNT, pairs) doubles
+    const int np = 2 * g.s;
+    const int pairs = np * cw;
+    int G = PNT / pairs; if (G < 1) G = 1;
+    double* psum = part + (pairs * G > PNT ? pairs * G : PNT);
+    for (int it = tid; it < pairs * G; it += PNT) {
+        const int pr = it % pairs, gg = it / pairs;
+        const int pf = pr / cw, c = pr % cw;
+        const double* A = p.prow + (long long)pf * H;
+        double acc = 0.0;
+        for (int n = gg; n < H; n += G) acc += A[n] * wv[(n << lc) + c];
+        part[it] = acc;
+    }
+    __syncthreads();
+    for (int pr = tid; pr < pairs; pr += PNT) {
+        double acc = 0.0;
+        for (int gg = 0; gg < G; ++gg) acc += part[gg * pairs + pr];
+        psum[pr] = acc;
+    }
+    __syncthreads();
+    for (int j = tid; j < g.S; j += PNT) {
+        int pr_, pc_;
+        band_profiles(g.s, j, pr_, pc_);
+        const double* Bc = p.pcol + (long long)pc_ * W + c0;
+        double acc = 0.0;
+        for (int c = 0; c < cw; ++c) acc += Bc[c] * psum[pr_ * cw + c];
+        p.taupart[((long long)bi * p.ntiles + tile) * g.S + j] = acc;
+    }
+}
+
+// Row FFT pass over strips of rows (fft2c/ifft2c operators, finalize output).
+template <typename R, bool INV, bool PRE_SIGN, bool POST_SIGN>
+__global__ void __launch_bounds__(PNT) row_pass(Geo g, const typename CT<R>::T* src,
+                                                typename CT<R>::T* dst, const typename CT<R>::T* tw,
+                                                int logrows) {
+    typedef typename CT<R>::T C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* buf = reinterpret_cast<C*>(smem_raw);
+    const int W = g.W, E = W << logrows;
+    C* tws = buf + E;
+    const int st = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
+    const long long base = (long long)bi * g.N + (long long)st * E;
+    const int rowbase = st << logrows;
+    for (int e = tid; e < W; e += PNT) tws[e] = tw[e];
+    for (int e = tid; e < E; e += PNT) {
+        C v = src[base + e];
+        if (PRE_SIGN && (((rowbase + (e >> g.logW)) + (e & (W - 1))) & 1)) v = mk<C>(-v.x, -v.y);
+        buf[e] = v;
+    }
+    __syncthreads();
+    block_fft<C, INV, PNT, PCAP, false>(buf, g.logW, logrows, W, 1, tws);
+    const R sc = R(1) / sqrt(R(W));
+    for (int e = tid; e < E; e += PNT) {
+        R s = sc;
+        if (POST_SIGN) s = ((((rowbase + (e >> g.logW)) + (e & (W - 1))) & 1) ? -sc : sc) * (R)g.sign_c;
+        dst[base + e] = cscale(buf[e], s);
+    }
+}
+
+// ------------------------------------------------------------------ K4 ----
+template <typename R>
+struct SelArgs {
+    const typename CT<R>::T* r;      // [B][N]
+    const double* taupart;           // [B][ntiles][S] (or null when tau_in given)
+    const double* tau_in;            // [B][S] or null
+    int ntiles;
+    double* par;                     // [B][S][3] Onsager params out
+    double* parf;                    // [B][S][3] soft-threshold-only params out
+    double* trace;                   // [B][S][TRACE_F] or null
+    const typename CT<R>::T* w0;     // [B][N] ground-truth coefficients or null
+    R* kA;                           // [B][N] key scratch (subbands > SCAP)
+    R* kB;
+};
+
+struct Best { double risk, t, cnt, inv; };
+
+__device__ __forceinline__ bool better(const Best& a, const Best& b) {
+    return a.risk < b.risk || (a.risk == b.risk && a.t < b.t);
+}
+
+__device__ __forceinline__ void consider(Best& b, double risk, double t, double cnt, double inv) {
+    Best c{risk, t, cnt, inv};
+    if (better(c, b)) b = c;
+}
+
+template <typename R>
+__device__ void bitonic_sort(R* s, int n) {
+    for (int k = 2; k <= n; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int p = threadIdx.x; p < (n >> 1); p += SNT) {
+                const int i = 2 * p - (p & (j - 1));
+                const int l = i + j;
+                const bool asc = (i & k) == 0;
+                R x = s[i], y = s[l];
+                if ((x > y) == asc) { s[i] = y; s[l] = x; }
+            }
+            __syncthreads();
+        }
+}
+
+// Evaluate the candidates owned by this thread on one tile of sorted
+// magnitudes (src/denoise.py:62-118):  candidate t = m_i at the end of each
+// tie run, plus the stationary point of the quadratic piece that starts there.
+template <typename R>
+__device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, int n, double tau,
+                                          double pre_tile, double suf_tile, double next_tile_first,
+                                          double* sh, Best& best) {
+    const int tid = threadIdx.x;
+    const int E = T >= SNT ? T / SNT : 1;
+    const bool act = tid * E < T;
+    const int b0 = tid * E;
+    double ssq = 0.0, sinv = 0.0;
+    if (act) {
+        for (int e = 0; e < E; ++e) { const double m = (double)keys[b0 + e]; ssq += m * m; }
+        for (int e = E - 1; e >= 0; --e) { const double m = (double)keys[b0 + e]; if (m > 0) sinv += 1.0 / m; }
+    }
+    const double pre = block_excl_scan<SNT, false>(ssq, sh) + pre_tile;
+    const double suf = block_excl_scan<SNT, true>(sinv, sh) + suf_tile;
+    if (!act) return;
+    const double nt = (double)n * tau;
+    double inv_above = suf, sq_after = 0.0;
+    for (int e = E - 1; e >= 0; --e) {
+        const int il = b0 + e;
+        const double m = (double)keys[il];
+        const double nxt = (il + 1 < T) ? (double)keys[il + 1] : next_tile_first;
+        if (m != nxt) {
+            const double zeroed = pre + (ssq - sq_after);       // sum_{j <= i} m_j^2
+            const double cnt = (double)(n - (tilebase + il + 1));
+            const double risk = zeroed + m * m * cnt - nt + tau * (2.0 * cnt - m * inv_above);
+            consider(best, risk, m, cnt, inv_above);
+            if (cnt > 0) {
+                const double ts = tau * inv_above / (2.0 * cnt);
+                if (ts > m && ts < nxt) {
+                    const double rs = zeroed + ts * ts * cnt - nt + tau * (2.0 * cnt - ts * inv_above);
+                    consider(best, rs, ts, cnt, inv_above);
+                }
+            }
+        }
+        if (m > 0) inv_above += 1.0 / m;
+        sq_after += m * m;
+    }
+}
+
+template <typename R>
+__global__ void __launch_bounds__(SNT, 1) sure_select(Geo g, SelArgs<R> a) {
+    typedef typename CT<R>::T C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    R* keys = reinterpret_cast<R*>(smem_raw);
+    __shared__ double sh[SNT / 32 + 2];
+    __shared__ double tsq[MAXTILES], tinv[MAXTILES], tpre[MAXTILES], tsuf[MAXTILES];
+    __shared__ double s_tau, s_totinv;
+    __shared__ Best s_best[SNT / 32];
+    const int j = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
+    const int n = g.len[j];
+    const long long base = (long long)bi * g.N + g.off[j];
+    if (tid == 0) {
+        double t = 0.0;
+        if (a.tau_in) t = a.tau_in[(long long)bi * g.S + j];
+        else for (int i = 0; i < a.ntiles; ++i) t += a.taupart[((long long)bi * a.ntiles + i) * g.S + j];
+        s_tau = t;
+    }
+    const C* rs = a.r + base;
+    const C* w0 = a.w0 ? a.w0 + base : nullptr;
+    double err = 0.0, ref = 0.0;
+    const bool large = n > SCAP;
+    const int T = large ? SCAP : n;
+    const int ntl = large ? n / SCAP : 1;
+    const R* sorted = keys;
+    for (int c0 = 0; c0 < n; c0 += T) {
+        for (int e = tid; e < T; e += SNT) {
+            const C v = rs[c0 + e];
+            keys[e] = cmag(v);
+            if (w0) {
+                const C w = w0[c0 + e];
+                const double dx = (double)v.x - (double)w.x, dy = (double)v.y - (double)w.y;
+                err += dx * dx + dy * dy;
+                ref += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
+            }
+        }
+        __syncthreads();
+        bitonic_sort(keys, T);
+        if (large) {
+            for (int e = tid; e < T; e += SNT) a.kA[base + c0 + e] = keys[e];
+            __syncthreads();
+        }
+    }
+    if (large) {
+        // merge sorted runs pairwise in global memory (merge path per thread)
+        R* srcb = a.kA + base;
+        R* dstb = a.kB + base;
+        const int per = n / SNT;
+        for (int w = SCAP; w < n; w <<= 1) {
+            const int o0 = tid * per;
+            const int pb = o0 / (2 * w) * (2 * w);
+            const R* A = srcb + pb;
+            const R* Bv = srcb + pb + w;
+            const int d = o0 - pb;
+            int lo = d > w ? d - w : 0, hi = d < w ? d : w;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (A[mid] <= Bv[d - 1 - mid]) lo = mid + 1; else hi = mid;
+            }
+            int ia = lo, ib = d - lo;
+            for (int e = 0; e < per; ++e) {
+                R v;
+                if (ib >= w || (ia < w && A[ia] <= Bv[ib])) v = A[ia++]; else v = Bv[ib++];
+                dstb[o0 + e] = v;
+            }
+            __syncthreads();
+            R* t = srcb; srcb = dstb; dstb = t;
+        }
+        sorted = srcb;
+        // tile totals (ascending squares, descending inverses)
+        for (int t = 0; t < ntl; ++t) {
+            double q = 0.0, v = 0.0;
+            for (int e = tid; e < SCAP; e += SNT) {
+                const double m = (double)sorted[t * SCAP + e];
+                q += m * m;
+            }
+            q = block_sum<SNT>(q, sh);
+            for (int e = tid; e < SCAP; e += SNT) {
+                const double m = (double)sorted[t * SCAP + e];
+                if (m > 0) v += 1.0 / m;
+            }
+            v = block_sum<SNT>(v, sh);
+            if (tid == 0) { tsq[t] = q; tinv[t] = v; }
+        }
+        __syncthreads();
+    }
+    if (w0) { err = block_sum<SNT>(err, sh); ref = block_sum<SNT>(ref, sh); }
+    if (tid == 0) {
+        double acc = 0.0;
+        for (int t = 0; t < ntl; ++t) { tpre[t] = acc; acc += large ? tsq[t] : 0.0; }
+        acc = 0.0;
+        for (int t = ntl - 1; t >= 0; --t) { tsuf[t] = acc; acc += large ? tinv[t] : 0.0; }
+        s_totinv = acc;
+    }
+    __syncthreads();
+    const double tau = fmax(s_tau, TAU_FLOOR);
+
+    Best best{INFINITY, INFINITY, 0.0, 0.0};
+    for (int t = 0; t < ntl; ++t) {
+        if (large) {
+            __syncthreads();
+            for (int e = tid; e < SCAP; e += SNT) keys[e] = sorted[t * SCAP + e];
+            __syncthreads();
+        }
+        const double nf = (t + 1 < ntl) ? (double)sorted[(t + 1) * SCAP] : INFINITY;
+        scan_tile<R>(keys, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, best);
+    }
+    // candidate t = 0 when no magnitude is zero (src/denoise.py:84)
+    __syncthreads();
+    if (!large) {
+        // single tile: total of inverses = exclusive suffix of thread 0 + its own
+        double v = 0.0;
+        const int E = T >= SNT ? T / SNT : 1;
+        if (tid * E < T)
+            for (int e = E - 1; e >= 0; --e) { const double m = (double)keys[tid * E + e]; if (m > 0) v += 1.0 / m; }
+        const double ex = block_excl_scan<SNT, true>(v, sh);
+        if (tid == 0) s_totinv = ex + v;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const double m0 = (double)sorted[0];
+        if (m0 > 0) {
+            const double totinv = s_totinv;
+            const double nn = (double)n;
+            consider(best, 0.0 + 0.0 * nn - nn * tau + tau * (2.0 * nn - 0.0 * totinv), 0.0, nn, totinv);
+            const double ts = tau * totinv / (2.0 * nn);
+            if (ts > 0.0 && ts < m0) {
+                const double rsk = 0.0 + ts * ts * nn - nn * tau + tau * (2.0 * nn - ts * totinv);
+                consider(best, rsk, ts, nn, totinv);
+            }
+        }
+    }
+    // block argmin, ties -> smaller t
+    for (int o = 16; o > 0; o >>= 1) {
+        Best c;
+        c.risk = __shfl_xor_sync(0xffffffffu, best.risk, o);
+        c.t = __shfl_xor_sync(0xffffffffu, best.t, o);
+        c.cnt = __shfl_xor_sync(0xffffffffu, best.cnt, o);
+        c.inv = __shfl_xor_sync(0xffffffffu, best.inv, o);
+        if (better(c, best)) best = c;
+    }
+    if ((tid & 31) == 0) s_best[tid >> 5] = best;
+    __syncthreads();
+    if (tid == 0) {
+        Best bb = s_best[0];
+        for (int w = 1; w < SNT / 32; ++w) if (better(s_best[w], bb)) bb = s_best[w];
+        const double alpha = (bb.cnt - 0.5 * bb.t * bb.inv) / (double)n;   // src/denoise.py:169
+        const bool clamped = alpha >= ALPHA_CLAMP;                         // src/vdamp.py:121-124
+        const double ac = clamped ? ALPHA_CLAMP : alpha;
+        const long long pj = ((long long)bi * g.S + j);
+        if (a.par) { a.par[3 * pj] = bb.t; a.par[3 * pj + 1] = ac; a.par[3 * pj + 2] = 1.0 / (1.0 - ac); }
+        if (a.parf) { a.parf[3 * pj] = bb.t; a.parf[3 * pj + 1] = 0.0; a.parf[3 * pj + 2] = 1.0; }
+        if (a.trace) {
+            double* tr = a.trace + pj * TRACE_F;
+            tr[0] = s_tau; tr[1] = bb.t; tr[2] = bb.t / tau; tr[3] = ac; tr[4] = alpha;
+            tr[5] = clamped ? 1.0 : 0.0; tr[6] = err; tr[7] = ref;
+        }
+    }
+}
+
+// --------------------------------------------------------------- misc ----
+// out = Onsager(in; par) per subband (r~_{k+1} or w_hat = soft(r, t)).
+template <typename R>
+__global__ void apply_params(Geo g, const typename CT<R>::T* in, typename CT<R>::T* out, const double* par) {
+    const int j = blockIdx.y, bi = blockIdx.z;
+    const double* pp = par + ((long long)bi * g.S + j) * 3;
+    const R t = (R)pp[0], al = (R)pp[1], ga = (R)pp[2];
+    const long long base = (long long)bi * g.N + g.off[j];
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < g.len[j]; e += gridDim.x * blockDim.x)
+        out[base + e] = onsager<R, typename CT<R>::T>(in[base + e], t, al, ga);
+}
+
+// y on the grid with the centred-FFT sign folded in, and 1/p (0 off mask).
+template <typename R>
+__global__ void scatter_measurements(Geo g, const typename CT<R>::T* y, const long long* idx,
+                                     const long long* offs, const double* probs, long long pstride,
+                                     typename CT<R>::T* yg, R* pinv) {
+    const int bi = blockIdx.y;
+    const long long o0 = offs[bi], n = offs[bi + 1] - o0;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const long long gi = idx[o0 + e];
+        const int k1 = (int)(gi >> g.logW), k2 = (int)(gi & (g.W - 1));
+        typename CT<R>::T v = y[o0 + e];
+        if ((k1 + k2) & 1) { v.x = -v.x; v.y = -v.y; }
+        yg[(long long)bi * g.N + gi] = v;
+        pinv[(long long)bi * g.N + gi] = (R)(1.0 / probs[(long long)bi * pstride + gi]);
+    }
+}
+
+template <typename R>
+__global__ void fill_identity_params(double* par, int count) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+        par[3 * i] = 0.0; par[3 * i + 1] = 0.0; par[3 * i + 2] = 1.0;
+    }
+}
+
+template <typename R>
+__global__ void make_twiddles(typename CT<R>::T* tw, int L) {
+    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < L; m += gridDim.x * blockDim.x) {
+        double s, c;
+        sincospi(-2.0 * (double)m / (double)L, &s, &c);
+        tw[m].x = (R)c; tw[m].y = (R)s;
+    }
+}
+
+// |fft1c(atom)|^2 of the 1D Haar atom, profile p = 2*(level-1) + high (src/vdamp.py:41-51, separable)
+__global__ void make_profiles(double* prof, int L, int s) {
+    const int pidx = blockIdx.y;
+    const int level = pidx / 2 + 1, high = pidx & 1;
+    const int M = 1 << level;
+    const double amp = exp2(-0.5 * level);
+    for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < L; w += gridDim.x * blockDim.x) {
+        const long long kf = (long long)w - L / 2;
+        double re = 0.0, im = 0.0;
+        for (int nn = 0; nn < M; ++nn) {
+            const double a = (high && nn >= M / 2) ? -amp : amp;
+            long long ph = (kf * nn) % L; if (ph < 0) ph += L;
+            double sn, cs;
+            sincospi(-2.0 * (double)ph / (double)L, &sn, &cs);
+            re += a * cs; im += a * sn;
+        }
+        prof[(long long)pidx * L + w] = (re * re + im * im) / (double)L;
+    }
+}
+
+// per-image |x - x0|^2 and |x0|^2 (src/diagnostics.py:21-34), deterministic
+template <typename R>
+__global__ void __launch_bounds__(SNT) nmse_sums(Geo g, const typename CT<R>::T* x, const typename CT<R>::T* x0, double* out) {
+    __shared__ double sh[SNT / 32 + 2];
+    const int bi = blockIdx.x;
+    const long long base = (long long)bi * g.N;
+    double e = 0.0, r = 0.0;
+    for (long long i = threadIdx.x; i < g.N; i += SNT) {
+        const typename CT<R>::T a = x[base + i], b = x0[base + i];
+        const double dx = (double)a.x - (double)b.x, dy = (double)a.y - (double)b.y;
+        e += dx * dx + dy * dy;
+        r += (double)b.x * (double)b.x + (double)b.y * (double)b.y;
+    }
+    e = block_sum<SNT>(e, sh);
+    r = block_sum<SNT>(r, sh);
+    if (threadIdx.x == 0) { out[2 * bi] = e; out[2 * bi + 1] = r; }
+}
+
+}  // namespace vdamp

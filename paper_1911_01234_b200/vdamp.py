@@ -1,0 +1,252 @@
+"""VDAMP reconstruction loop on B200 -- drop-in for ``csmri.vdamp`` (src/vdamp.py).
+
+``run(y, mask, pmap, noise_var, scales, n_iters, ground_truth=None,
+keep_r_iters=())`` keeps the reference signature, return types and errors.
+The whole loop (K1..K4 per iteration, finalize) runs on the device through
+``libvdamp_b200.so``; the host only validates, uploads and reads back.
+
+Extensions (keyword-only): ``precision`` ("fp64" = the reference's
+complex128 arithmetic, the parity mode and the default; "fp32" = complex64
+throughput mode) and ``device``.  ``run_batch`` reconstructs many
+independent images in one launch sequence.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .denoise import SubbandVector
+from .fourier import SamplingMask
+from .trace import IterationRecord, RunTrace
+from .wavelet import SubbandLayout, WaveletCoeffs
+
+ALPHA_CLAMP = 1.0 - 1e-9          # src/vdamp.py:25
+NMSE_FLOOR_DB = -320.0            # src/diagnostics.py:17
+
+
+def _probs(pmap, shape):
+    probs = np.asarray(getattr(pmap, "probs", pmap), dtype=np.float64)
+    if probs.shape != tuple(shape):
+        raise ValueError(f"probability map shape {probs.shape} != mask shape {tuple(shape)}")
+    if np.any(probs <= 0) or np.any(probs > 1):
+        raise ValueError("probabilities must lie in (0, 1]")
+    return probs
+
+
+def _nmse_db(err: float, ref: float) -> float:
+    # src/diagnostics.py:21-34
+    if ref == 0.0:
+        raise ValueError("reference signal is identically zero")
+    if err == 0.0:
+        return NMSE_FLOOR_DB
+    return max(10.0 * np.log10(err / ref), NMSE_FLOOR_DB)
+
+
+def _subband_nmse(err: np.ndarray, ref: np.ndarray) -> np.ndarray:
+    # src/diagnostics.py:37-51 (NaN sentinel for zero-energy subbands)
+    out = np.full(err.shape, np.nan)
+    nz = ref != 0.0
+    with np.errstate(divide="ignore"):
+        v = np.where(err > 0, 10.0 * np.log10(np.where(err > 0, err, 1.0) / np.where(nz, ref, 1.0)), NMSE_FLOOR_DB)
+    out[nz] = np.maximum(v[nz], NMSE_FLOOR_DB)
+    return out
+
+
+@dataclass
+class BatchInputs:
+    """Host-side concatenation of a batch's measurements (what the C ABI takes)."""
+
+    y: np.ndarray
+    indices: np.ndarray
+    counts: np.ndarray
+    probs: np.ndarray
+    shared_probs: bool
+    noise_var: np.ndarray
+    height: int
+    width: int
+
+
+def prepare_batch(ys, masks, pmaps, noise_vars) -> BatchInputs:
+    """Validate like the reference (src/fourier.py:62-77, src/sampling.py:45-46) and concatenate."""
+    masks = list(masks)
+    B = len(masks)
+    if B < 1:
+        raise ValueError("empty batch")
+    ys = list(ys)
+    if len(ys) != B:
+        raise ValueError("one measurement vector per mask required")
+    shape = masks[0].shape
+    for m in masks:
+        if m.shape != shape:
+            raise ValueError("all images of a batch must share one shape")
+    if not isinstance(pmaps, (list, tuple)):
+        probs = _probs(pmaps, shape)
+        shared = True
+    else:
+        if len(pmaps) != B:
+            raise ValueError("one probability map per mask required")
+        if all(p is pmaps[0] for p in pmaps):
+            probs, shared = _probs(pmaps[0], shape), True
+        else:
+            probs, shared = np.stack([_probs(p, shape) for p in pmaps]), False
+    nv = np.asarray(noise_vars, dtype=np.float64).reshape(-1)
+    if nv.size == 1 and B > 1:
+        nv = np.full(B, float(nv[0]))
+    if nv.shape != (B,):
+        raise ValueError("one noise variance per image required")
+    if np.any(nv < 0):
+        raise ValueError("noise variance must be >= 0")
+    for y, m in zip(ys, masks):
+        if np.shape(y) != (m.n,):
+            raise ValueError(f"measurement length {np.shape(y)} != mask count {m.n}")
+    counts = np.array([m.n for m in masks], dtype=np.int64)
+    idx = np.concatenate([m.indices for m in masks]).astype(np.int64)
+    y = np.concatenate([np.asarray(v) for v in ys])
+    return BatchInputs(y, idx, counts, probs, shared, nv, shape[0], shape[1])
+
+
+def _records(trace_np, nmse_np, b, n_iters, wall):
+    recs = []
+    for k in range(n_iters):
+        tr = trace_np[k, b]
+        tau = tr[:, 0].copy()
+        lam = tr[:, 2].copy()
+        rec = IterationRecord(
+            k=k, wall_time=wall, tau=tau, thresholds=lam * tau, lambdas=lam,
+            alphas=tr[:, 3].copy(), alpha_clamped=bool(np.any(tr[:, 5] != 0)))
+        if nmse_np is not None:
+            rec.nmse_db = _nmse_db(float(nmse_np[k, b, 0]), float(nmse_np[k, b, 1]))
+            rec.subband_nmse_db = _subband_nmse(tr[:, 6], tr[:, 7])
+        recs.append(rec)
+    return recs
+
+
+def run_batch(ys, masks, pmaps, noise_vars, scales, n_iters, ground_truths=None, keep_r_iters=(),
+              *, precision="fp64", device=None, return_tensor=False):
+    """VDAMP on a batch of independent images (one launch sequence for all).
+
+    Returns (x_hat (B, H, W) complex ndarray, [RunTrace per image]).
+    """
+    import torch
+    from .plan import get_plan
+    if n_iters < 1:
+        raise ValueError(f"need at least one iteration, got {n_iters}")
+    masks = list(masks)
+    inp = prepare_batch(ys, masks, pmaps, noise_vars)
+    layout = SubbandLayout.create(inp.height, inp.width, scales)
+    B = len(masks)
+    t0 = time.perf_counter()
+    plan = get_plan(inp.height, inp.width, scales, B, precision, device)
+    plan.set_measurements(inp.y, inp.indices, inp.counts, inp.probs, inp.noise_var, inp.shared_probs)
+    gt = None
+    if ground_truths is not None:
+        gt = np.stack([np.asarray(g) for g in ground_truths])
+        if gt.shape != (B, inp.height, inp.width):
+            raise ValueError("ground truth shape mismatch")
+        plan.set_ground_truth(gt)
+    else:
+        plan.set_ground_truth(None)
+    torch.cuda.synchronize(plan.device)
+    precompute = time.perf_counter() - t0
+    trace = plan.new_trace(n_iters)
+    nmse = (torch.zeros((n_iters, B, _lib.NMSE_FIELDS), dtype=torch.float64, device=plan.device)
+            if gt is not None else None)
+    snaps = {k: plan.empty_coeffs() for k in keep_r_iters if 0 <= k < n_iters} or None
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    x = plan.run(n_iters, trace=trace, nmse=nmse, snapshots=snaps)
+    e1.record()
+    e1.synchronize()
+    wall = e0.elapsed_time(e1) / 1e3 / n_iters
+    trace_np = trace.cpu().numpy()
+    nmse_np = nmse.cpu().numpy() if nmse is not None else None
+    traces = []
+    for b in range(B):
+        rt = RunTrace("vdamp", _records(trace_np, nmse_np, b, n_iters, wall), precompute)
+        if snaps:
+            for k, t in snaps.items():
+                rt.r_snapshots[k] = WaveletCoeffs(t[b].cpu().numpy().astype(np.complex128), layout)
+        traces.append(rt)
+    if return_tensor:
+        return x, traces
+    return x.cpu().numpy().astype(np.complex128), traces
+
+
+def run(y, mask: SamplingMask, pmap, noise_var, scales, n_iters, ground_truth=None, keep_r_iters=(),
+        *, precision="fp64", device=None):
+    """Full reconstruction loop (src/vdamp.py:153-197); trace metrics only with ground truth."""
+    if n_iters < 1:
+        raise ValueError(f"need at least one iteration, got {n_iters}")
+    SubbandLayout.create(mask.shape[0], mask.shape[1], scales)
+    x, traces = run_batch([y], [mask], pmap, [noise_var], scales, n_iters,
+                          None if ground_truth is None else [ground_truth], keep_r_iters,
+                          precision=precision, device=device)
+    return x[0], traces[0]
+
+
+# ---------------------------------------------------------------------------
+# Step-wise interface (src/vdamp.py:81-150)
+# ---------------------------------------------------------------------------
+@dataclass
+class VdampState:
+    r_tilde: WaveletCoeffs
+    r: WaveletCoeffs | None = None
+    z: np.ndarray | None = None          # fused on device, not materialised
+    tau: SubbandVector | None = None
+    w_hat: WaveletCoeffs | None = None
+    alpha: SubbandVector | None = None
+    thresholds: np.ndarray | None = None
+    lambdas: SubbandVector | None = None
+    k: int = 0
+    alpha_clamped: bool = False
+
+
+def initial_state(layout: SubbandLayout) -> VdampState:
+    return VdampState(WaveletCoeffs(np.zeros(layout.size, dtype=np.complex128), layout))
+
+
+def iterate(state: VdampState, y, mask: SamplingMask, pmap, noise_var, spectra=None,
+            masked_profiles=None, *, precision="fp64", device=None) -> VdampState:
+    """One iteration from state.r_tilde (src/vdamp.py:99-144); spectra args are accepted and unused
+    (the plan builds the separable subband spectra on the device)."""
+    import torch
+    from .plan import get_plan
+    lay = state.r_tilde.layout
+    inp = prepare_batch([y], [mask], pmap, [noise_var])
+    plan = get_plan(lay.image_height, lay.image_width, lay.scales, 1, precision, device)
+    plan.set_measurements(inp.y, inp.indices, inp.counts, inp.probs, inp.noise_var, inp.shared_probs)
+    plan.set_ground_truth(None)
+    rt = plan.to_device(state.r_tilde.values, plan.cdtype).reshape(1, -1).contiguous()
+    r = plan.empty_coeffs()
+    rn = plan.empty_coeffs()
+    wh = plan.empty_coeffs()
+    tr = torch.zeros((1, plan.S, _lib.TRACE_FIELDS), dtype=torch.float64, device=plan.device)
+    plan.iterate(rt, r, rn, wh, tr)
+    t = tr[0].cpu().numpy()
+    tau = t[:, 0].copy()
+    lam = t[:, 2].copy()
+    as_np = lambda v: v[0].cpu().numpy().astype(np.complex128)
+    return VdampState(
+        r_tilde=WaveletCoeffs(as_np(rn), lay), r=WaveletCoeffs(as_np(r), lay), z=None,
+        tau=SubbandVector(tau, "variance"), w_hat=WaveletCoeffs(as_np(wh), lay),
+        alpha=SubbandVector(t[:, 3].copy(), "derivative"), thresholds=lam * tau,
+        lambdas=SubbandVector(lam, "weight"), k=state.k + 1,
+        alpha_clamped=bool(np.any(t[:, 5] != 0)))
+
+
+def finalize(w_hat: WaveletCoeffs, y, mask: SamplingMask, *, precision="fp64", device=None) -> np.ndarray:
+    """Exact data consistency: replace sampled frequencies by y (src/vdamp.py:147-150)."""
+    from .plan import get_plan
+    lay = w_hat.layout
+    inp = prepare_batch([y], [mask], np.ones(mask.shape), [0.0])
+    plan = get_plan(lay.image_height, lay.image_width, lay.scales, 1, precision, device)
+    plan.set_measurements(inp.y, inp.indices, inp.counts, inp.probs, inp.noise_var, True)
+    w = plan.to_device(w_hat.values, plan.cdtype).reshape(1, -1).contiguous()
+    out = plan.empty_images()
+    plan.finalize(w, out)
+    return out[0].cpu().numpy().astype(np.complex128)

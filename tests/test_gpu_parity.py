@@ -1,0 +1,164 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the reference fixtures and the oracle.
+
+Tolerances:
+  operators  fp64 <= 1e-12 relative, fp32 <= 1e-6 relative (max-abs / max)
+  end to end fp64 x_hat <= 1e-3 relative L2 (expected ~1e-10), NMSE <= 0.05 dB
+  masks / layouts bit-exact.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def relmax(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300))
+
+
+def rel2(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def _shapes(ops):
+    for k in ops:
+        if k.startswith("dwt_in_"):
+            key = k[len("dwt_in_"):]
+            h, rest = key.split("x")
+            w, s = rest.split("s")
+            yield key, int(h), int(w), int(s)
+
+
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-13), ("fp32", 1e-6)])
+def test_operators_vs_reference(precision, tol):
+    from paper_1911_01234_b200 import fourier, wavelet
+    ops = golden("operators")
+    for key, h, w, s in _shapes(ops):
+        x = ops[f"dwt_in_{key}"]
+        c = wavelet.dwt(x, s, precision=precision)
+        assert relmax(c.values, ops[f"dwt_out_{key}"]) <= tol, key
+        lay = wavelet.SubbandLayout.create(h, w, s)
+        assert [b.offset for b in lay.subbands] == list(ops[f"offsets_{key}"])
+        img = wavelet.idwt(wavelet.WaveletCoeffs(ops[f"idwt_in_{key}"], lay), precision=precision)
+        assert relmax(img, ops[f"idwt_out_{key}"]) <= tol, key
+        ftol = tol * 10 * np.log2(h * w)
+        assert relmax(fourier.fft2c(x, precision=precision), ops[f"fft_out_{key}"]) <= ftol, key
+        assert relmax(fourier.ifft2c(x, precision=precision), ops[f"ifft_out_{key}"]) <= ftol, key
+
+
+def test_forward_adjoint_vs_oracle(oracle):
+    from paper_1911_01234_b200 import fourier
+    g = golden("run_shepp64")
+    m = fourier.SamplingMask(g["sampled"])
+    x = g["x0"]
+    assert relmax(fourier.forward(x, m), oracle.forward(x, m.indices)) <= 1e-12
+    assert relmax(fourier.adjoint(g["y"], m), oracle.adjoint(g["y"], m.indices, m.shape)) <= 1e-12
+
+
+def test_denoise_colored_vs_reference():
+    from paper_1911_01234_b200 import denoise, wavelet
+    g = golden("denoise")
+    for (h, w, s) in [(32, 32, 2), (64, 32, 3)]:
+        key = f"{h}x{w}s{s}"
+        lay = wavelet.SubbandLayout.create(h, w, s)
+        wh, al, lam = denoise.denoise_colored(wavelet.WaveletCoeffs(g[f"r_{key}"], lay),
+                                              denoise.SubbandVector(g[f"tau_{key}"]))
+        assert relmax(wh.values, g[f"what_{key}"]) <= 1e-12
+        assert np.allclose(al.values, g[f"alpha_{key}"], rtol=1e-12, atol=1e-15)
+        assert np.allclose(lam.values, g[f"lambda_{key}"], rtol=1e-12)
+
+
+def _tricky_coeffs(rng, n, kind):
+    r = rng.normal(size=n) + 1j * rng.normal(size=n)
+    if kind == "ties":
+        r = np.round(r, 1)
+    elif kind == "zeros":
+        r[rng.random(n) < 0.3] = 0
+    elif kind == "sparse":
+        r = r * 0.05
+        idx = rng.choice(n, n // 20, replace=False)
+        r[idx] += rng.exponential(3.0, idx.size)
+    return r
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 3), (256, 256, 4), (512, 512, 2)])
+@pytest.mark.parametrize("kind", ["gauss", "ties", "zeros", "sparse"])
+def test_sure_select_vs_oracle(oracle, shape, kind):
+    """Exact SURE argmin incl. ties, zeros, interior points; 512x512 s=2 has 65,536-entry
+    subbands (multi-tile merge path)."""
+    from paper_1911_01234_b200 import denoise, wavelet
+    h, w, s = shape
+    rng = np.random.default_rng(hash((shape, kind)) % 2**32)
+    lay = wavelet.SubbandLayout.create(h, w, s)
+    r = _tricky_coeffs(rng, h * w, kind)
+    tau = rng.uniform(0.2, 2.0, lay.n_subbands)
+    bands = oracle.band_table(h, w, s)
+    wh_o, al_o, lam_o, t_o = oracle.denoise_colored(r, tau, bands)
+    wh, al, lam = denoise.denoise_colored(wavelet.WaveletCoeffs(r, lay), denoise.SubbandVector(tau))
+    assert np.allclose(lam.values * tau, t_o, rtol=1e-12, atol=0)
+    assert np.allclose(al.values, al_o, rtol=1e-10, atol=1e-14)
+    assert relmax(wh.values, wh_o) <= 1e-12
+
+
+RUNS = ["shepp32", "shepp64", "rect64x32", "shepp128", "full64"]
+
+
+@pytest.mark.parametrize("name", RUNS)
+def test_run_vs_reference_fp64(name):
+    from paper_1911_01234_b200 import fourier, vdamp
+    g = golden("run_" + name)
+    mask = fourier.SamplingMask(g["sampled"])
+    gt = g["x0"] if "nmse_db" in g else None
+    keep = tuple(int(k[5:]) for k in g if k.startswith("snap_"))
+    x, tr = vdamp.run(g["y"], mask, g["probs"], float(g["noise_var"]), int(g["scales"]), int(g["n_iters"]),
+                      ground_truth=gt, keep_r_iters=keep)
+    assert rel2(x, g["x_hat"]) <= 1e-8, rel2(x, g["x_hat"])
+    assert len(tr) == int(g["n_iters"])
+    tau = np.array([r.tau for r in tr.records])
+    assert np.allclose(tau, g["tau"], rtol=1e-9, atol=1e-300)
+    assert np.allclose(np.array([r.thresholds for r in tr.records]), g["thresholds"], rtol=1e-8)
+    assert np.allclose(np.array([r.alphas for r in tr.records]), g["alphas"], rtol=1e-8, atol=1e-12)
+    assert [r.alpha_clamped for r in tr.records] == list(g["clamped"])
+    if gt is not None:
+        nm = tr.nmse_curve()
+        assert np.abs(nm - g["nmse_db"]).max() <= 0.05
+        assert np.abs(nm - g["nmse_db"]).max() <= 1e-6
+        sb = np.array([r.subband_nmse_db for r in tr.records])
+        assert np.allclose(sb, g["subband_nmse_db"], atol=1e-6, equal_nan=True)
+    for k in keep:
+        assert relmax(tr.r_snapshots[k].values, g[f"snap_{k}"]) <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["shepp32", "shepp64", "rect64x32"])
+def test_teacher_forced_iterate_fp64(name):
+    from paper_1911_01234_b200 import fourier, vdamp, wavelet
+    g = golden("run_" + name)
+    mask = fourier.SamplingMask(g["sampled"])
+    H, W = mask.shape
+    lay = wavelet.SubbandLayout.create(H, W, int(g["scales"]))
+    for k in range(int(g["steps"])):
+        st = vdamp.VdampState(wavelet.WaveletCoeffs(g[f"step{k}_rtilde_in"], lay), k=k)
+        nx = vdamp.iterate(st, g["y"], mask, g["probs"], float(g["noise_var"]))
+        assert relmax(nx.r.values, g[f"step{k}_r"]) <= 1e-11
+        assert np.allclose(nx.tau.values, g[f"step{k}_tau"], rtol=1e-11, atol=1e-300)
+        assert np.allclose(nx.thresholds, g[f"step{k}_thr"], rtol=1e-10)
+        assert np.allclose(nx.alpha.values, g[f"step{k}_alpha"], rtol=1e-10, atol=1e-14)
+        assert relmax(nx.w_hat.values, g[f"step{k}_what"]) <= 1e-10
+        assert relmax(nx.r_tilde.values, g[f"step{k}_rtilde_out"]) <= 1e-9
+        assert nx.k == k + 1
+
+
+def test_finalize_vs_reference(oracle):
+    from paper_1911_01234_b200 import fourier, vdamp, wavelet
+    g = golden("run_shepp32")
+    mask = fourier.SamplingMask(g["sampled"])
+    lay = wavelet.SubbandLayout.create(32, 32, 2)
+    rng = np.random.default_rng(2)
+    w = rng.normal(size=1024) + 1j * rng.normal(size=1024)
+    p = oracle.Problem(g["y"], mask.indices, g["probs"], float(g["noise_var"]), 2)
+    x = vdamp.finalize(wavelet.WaveletCoeffs(w, lay), g["y"], mask)
+    assert relmax(x, oracle.finalize(w, p)) <= 1e-12
+    # consistency: sampled frequencies equal y
+    assert relmax(oracle.forward(x, mask.indices), g["y"]) <= 1e-12
