@@ -123,10 +123,18 @@ def test_run_vs_reference_fp64(name):
     assert [r.alpha_clamped for r in tr.records] == list(g["clamped"])
     if gt is not None:
         nm = tr.nmse_curve()
-        assert np.abs(nm - g["nmse_db"]).max() <= 0.05
-        assert np.abs(nm - g["nmse_db"]).max() <= 1e-6
+        ref = g["nmse_db"]
+        # below -200 dB the error is round-off (exact recovery): compare only that both are there
+        live = ref > -200
+        assert np.all(nm[~live] <= -200)
+        assert np.abs(nm[live] - ref[live]).max(initial=0) <= 0.05
+        assert np.abs(nm[live] - ref[live]).max(initial=0) <= 1e-6
         sb = np.array([r.subband_nmse_db for r in tr.records])
-        assert np.allclose(sb, g["subband_nmse_db"], atol=1e-6, equal_nan=True)
+        sref = g["subband_nmse_db"]
+        slive = sref > -200
+        assert np.all(sb[~slive & ~np.isnan(sref)] <= -200)
+        assert np.allclose(sb[slive], sref[slive], atol=1e-6)
+        assert np.array_equal(np.isnan(sb), np.isnan(sref))
     for k in keep:
         assert relmax(tr.r_snapshots[k].values, g[f"snap_{k}"]) <= 1e-10
 
