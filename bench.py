@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""VDAMP image-iterations/s on B200 (BASELINE.json metric), one process per GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1] [--impl ours|reference]
+
+A step = one VDAMP reconstruction (setup scatter, 30 iterations, finalize)
+of one batch of synthetic slices of ``--config`` (default cfg1: 64 x 256^2
+complex64, Haar s=4, R=4, 40 dB).  Each rank reconstructs its own batch of
+distinct slices (weak scaling, no collective in the data path).
+
+value    device-resident: inputs already in HBM, CUDA events per step, L2
+         flushed (256 MiB write) between steps, max over ranks.
+e2e      the public BatchReconstructor call with pinned host inputs; H2D of
+         y / indices / density and D2H of x_hat inside the timed region.
+roofline dominant kernel class: algorithmic bytes / its
+         CUDA-event time inside the timed region, vs MEASURED_PEAKS hbm_gbs.
+cpu_baseline  the numpy oracle port (oracle/vdamp_oracle.py) on a bounded
+         sample of the same slices, one slice per process, all host cores.
+--impl reference  times that oracle port alone (rank 0; other ranks exit 0).
+"""
+
+from __future__ import annotations
+
+import os
+
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import argparse
+import json
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1911_01234_b200 import workload  # noqa: E402
+
+METRIC = "VDAMP image-iterations/s"
+UNIT = "img-iter/s"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------- CPU leg --
+_W = None
+
+
+def _oracle_slice(b):
+    from oracle import vdamp_oracle as O
+    w = _W
+    O.run(w.ys[b].astype(np.complex128), w.masks[b].indices, w.pmap.probs, float(w.noise_vars[b]),
+          w.config.scales, w.config.n_iters)
+    return b
+
+
+def cpu_oracle_rate(w, n_images, procs, repeats=1):
+    """img-iter/s of the oracle on the first n_images slices of w, `procs` processes (fork)."""
+    import multiprocessing as mp
+    global _W
+    _W = w
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        pool.map(_oracle_slice, [0])                        # warm the workers' imports
+        times = []
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            pool.map(_oracle_slice, [i % len(w.masks) for i in range(n_images)], chunksize=1)
+            times.append(time.perf_counter() - t0)
+    return n_images * w.config.n_iters / float(np.mean(times)), times
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi equivalent via NVML, sampled in a thread during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock"}
+
+    def __init__(self, index, period=0.02):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self.period = period
+        self.samples = []
+        self.reasons = 0
+        self._stop = threading.Event()
+
+    def _loop(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._loop, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        reasons = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": float(self.max_mhz),
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def class_bytes(cfg, N, n_mean, images, iters, b_c):
+    """Algorithmic bytes per kernel class over `iters` iterations of `images` images."""
+    f = b_c / 8.0
+    it = images * iters
+    return {
+        "synth_rowfft": 16 * N * f * it,                         # read r, write T1
+        "col_residual": (16 * N + 12 * n_mean) * f * it + N / 8 * it,   # T1, y, 1/p, mask -> T2
+        "rowifft_analysis": 24 * N * f * it,                     # T2, r -> r
+        "sure_select": 8 * N * f * it,                           # read r
+        "finalize": (48 * N + 8 * n_mean) * f * images,          # once per run
+    }
+
+
+def traffic_from_profiles(kernel_class):
+    """dram bytes per launch from the committed ncu summary (profiles/), if present."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(kernel_class)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------- main --
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--batch", type=int, default=None, help="images per rank (default: config batch)")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    cfg = workload.CONFIGS[args.config]
+    B = args.batch or cfg.batch
+    cores = host_cores()
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        ns = max(4, min(cores, 64))
+        w = workload.make_workload(cfg, batch=min(ns, B))
+        rates = []
+        t_all = []
+        rate, _ = cpu_oracle_rate(w, ns, cores, repeats=args.warmup)    # warm-up steps
+        for _ in range(args.steps):
+            r, t = cpu_oracle_rate(w, ns, cores, repeats=1)
+            rates.append(r)
+            t_all += t
+        value = ns * cfg.n_iters * args.steps / float(np.sum(t_all))
+        line = {
+            "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(t_all)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (seeded BASELINE workload generator)",
+            "config": {"workload": f"{cfg.name}: {cfg.size}^2 complex, Haar s={cfg.scales}, R={cfg.undersampling:g}, "
+                                   f"{cfg.snr_db:g} dB, {cfg.n_iters} iterations", "images_per_step": ns},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{ns} slices x {cfg.n_iters} iterations per step, one slice per process "
+                                       f"(oracle/vdamp_oracle.py, numpy float64)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
+
+    # ---- our arm ------------------------------------------------------
+    w = workload.make_workload(cfg, batch=B, first=rank * B)
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ns = max(4, min(cores, 32))
+        rate, ts = cpu_oracle_rate(w, ns, cores, repeats=1)
+        cpu_base = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                    "sample": f"{ns} of the {B} slices x {cfg.n_iters} iterations, one slice per process, "
+                              f"{cores} processes (oracle/vdamp_oracle.py, numpy float64), {ts[0]:.1f} s"}
+
+    import torch
+    import torch.distributed as dist
+    from paper_1911_01234_b200 import vdamp
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    inp = vdamp.prepare_batch(w.ys, w.masks, w.pmap, w.noise_vars)
+    rec = vdamp.BatchReconstructor(cfg.size, cfg.size, cfg.scales, B, precision=args.precision, device=local)
+    plan = rec.plan
+    cd = plan.cdtype
+    dev_in = dict(y=torch.from_numpy(inp.y).to(dev, cd), indices=torch.from_numpy(inp.indices).to(dev),
+                  counts=inp.counts, probs=torch.from_numpy(inp.probs).to(dev), noise_var=inp.noise_var)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        return rec(dev_in["y"], dev_in["indices"], dev_in["counts"], dev_in["probs"], dev_in["noise_var"],
+                   cfg.n_iters, shared_probs=True, sync=False)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---- device-resident timed region --------------------------------
+    plan.set_timing(True)
+    plan.launch_count(reset=True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))                       # evict L2 between steps (untimed)
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    launches = plan.launch_count()
+    ktimes = plan.kernel_times()
+    plan.set_timing(False)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_s = max_over_ranks(float(np.sum(step_ms)) / 1e3)
+    images_all = B * world
+    value = images_all * cfg.n_iters * args.steps / total_s
+    ms_per_step = 1e3 * total_s / args.steps
+
+    # ---- end to end through the public call, pinned host buffers -----
+    e2e = None
+    if not args.no_e2e:
+        host = rec.upload(inp, pin=True)
+        out = torch.empty((B, cfg.size, cfg.size), dtype=cd).pin_memory()
+        h2d = (host["y"].numel() * host["y"].element_size() + host["indices"].numel() * 8
+               + host["probs"].numel() * 8 + B * 8)
+        d2h = out.numel() * out.element_size()
+        for _ in range(args.warmup):
+            rec(host["y"], host["indices"], host["counts"], host["probs"], host["noise_var"], cfg.n_iters, out=out)
+        barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            rec(host["y"], host["indices"], host["counts"], host["probs"], host["noise_var"], cfg.n_iters, out=out)
+        t_e2e = max_over_ranks(time.perf_counter() - t0)
+        barrier()
+        e2e = {"value": images_all * cfg.n_iters * args.steps / t_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1e3 * t_e2e / args.steps}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel class -----------------------
+    N = cfg.size * cfg.size
+    n_mean = float(np.mean(inp.counts))
+    b_c = 8 if args.precision == "fp32" else 16
+    cb = class_bytes(cfg, N, n_mean, B, cfg.n_iters * args.steps, b_c)
+    cb["finalize"] *= args.steps
+    peak, peak_src = measured_peak()
+    dom = max((k for k in cb), key=lambda k: ktimes[k][0])
+    kms, kl = ktimes[dom]
+    achieved = cb[dom] / (kms / 1e3) / 1e9
+    traffic = traffic_from_profiles(dom)
+    kernels = {k: {"ms_per_step": ktimes[k][0] / args.steps, "launches_per_step": ktimes[k][1] / args.steps,
+                   "GBps": (cb[k] / (ktimes[k][0] / 1e3) / 1e9) if ktimes[k][0] > 0 and k in cb else None}
+               for k in ktimes}
+    b_iter = workload.algorithmic_bytes_per_image_iter(N, n_mean, b_c)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c64" if args.precision == "fp32" else "c128",
+        "data": "synthetic (seeded BASELINE workload generator: random ellipses x smooth phase, offset-law masks)",
+        "config": {"workload": f"{cfg.name}: {B} x {cfg.size}^2 complex slices per GPU, Haar s={cfg.scales}, "
+                               f"R={cfg.undersampling:g}, {cfg.snr_db:g} dB, {cfg.n_iters} iterations",
+                   "images_per_gpu": B, "n_iters": cfg.n_iters, "precision": args.precision,
+                   "l2": "flushed between timed steps (256 MiB write, untimed)",
+                   "parallelism": f"images sharded, {world} process(es), 1 GPU each, no collective"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": cb[dom] / max(kl, 1),
+                     "avg_launch_ms": kms / max(kl, 1)},
+        "iteration_roofline": {"B_iter_bytes": b_iter, "achieved_GBps": value / world * b_iter / 1e9,
+                               "frac": value / world * b_iter / 1e9 / peak},
+        "kernels": kernels,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if cpu_base is not None:
+        line["cpu_baseline"] = cpu_base
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -61,6 +61,7 @@ struct Plan {
     double* prow = nullptr;         // [2s][H]
     double* pcol = nullptr;         // [2s][W]
     double* nvar = nullptr;         // [B]
+    long long* offs = nullptr;      // [B+1] measurement offsets
     void* twH = nullptr;
     void* twW = nullptr;
     void* kA = nullptr;             // sort scratch (large subbands only)
@@ -333,7 +334,7 @@ void free_plan(Plan* p) {
     if (!p) return;
     cudaSetDevice(p->dev);
     void* bufs[] = {p->r, p->T1, p->T2, p->yg, p->pinv, p->par, p->parf, p->taupart, p->prow, p->pcol,
-                    p->nvar, p->twH, p->twW, p->kA, p->kB, p->x0, p->w0, p->xtmp, p->trtmp};
+                    p->nvar, p->offs, p->twH, p->twW, p->kA, p->kB, p->x0, p->w0, p->xtmp, p->trtmp};
     for (void* b : bufs) if (b) cudaFree(b);
     for (void* b : p->scratch) if (b) cudaFree(b);
     for (auto& e : p->ev) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
@@ -416,6 +417,7 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         p->prow = (double*)dalloc(p, (size_t)2 * scales * height * sizeof(double));
         p->pcol = (double*)dalloc(p, (size_t)2 * scales * width * sizeof(double));
         p->nvar = (double*)dalloc(p, (size_t)batch * sizeof(double));
+        p->offs = (long long*)dalloc(p, (size_t)(batch + 1) * sizeof(long long));
         p->twH = dalloc(p, (size_t)height * cs);
         p->twW = dalloc(p, (size_t)width * cs);
         p->trtmp = (double*)dalloc(p, (size_t)batch * p->S * TRACE_F * sizeof(double));
@@ -481,22 +483,27 @@ int vdamp_set_measurements(vdamp_plan_t plan, const void* y, const int64_t* indi
         const size_t rs = p->prec == VDAMP_FP32 ? sizeof(float) : sizeof(double);
         CK(cudaMemsetAsync(p->yg, 0, img * p->csz, st));
         CK(cudaMemsetAsync(p->pinv, 0, img * rs, st));
+        // pageable host sources are staged before cudaMemcpyAsync returns, so the
+        // locals above may die right after; no stream synchronisation needed
         CK(cudaMemcpyAsync(p->nvar, noise_var, p->B * sizeof(double), cudaMemcpyHostToDevice, st));
-        long long* doffs = nullptr;
-        CK(cudaMallocAsync((void**)&doffs, (p->B + 1) * sizeof(long long), st));
-        CK(cudaMemcpyAsync(doffs, offs.data(), (p->B + 1) * sizeof(long long), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(p->offs, offs.data(), (p->B + 1) * sizeof(long long), cudaMemcpyHostToDevice, st));
         dim3 grid((unsigned)std::min<long long>((maxn + 255) / 256, 1024), p->B);
-        if (p->prec == VDAMP_FP32)
-            scatter_measurements<float><<<grid, 256, 0, st>>>(p->geo, (const float2*)y, (const long long*)indices, doffs,
-                                                              probs, probs_batch_stride, (float2*)p->yg, (float*)p->pinv);
-        else
-            scatter_measurements<double><<<grid, 256, 0, st>>>(p->geo, (const double2*)y, (const long long*)indices, doffs,
-                                                               probs, probs_batch_stride, (double2*)p->yg, (double*)p->pinv);
-        p->launches++;
-        CK(cudaGetLastError());
-        CK(cudaFreeAsync(doffs, st));
-        // the host arrays above must outlive the async copies
-        CK(cudaStreamSynchronize(st));
+        {
+            Launch L(p, 5, st);
+            if (p->prec == VDAMP_FP32)
+                scatter_measurements<float><<<grid, 256, 0, st>>>(p->geo, (const float2*)y, (const long long*)indices,
+                                                                  p->offs, probs, probs_batch_stride, (float2*)p->yg,
+                                                                  (float*)p->pinv);
+            else
+                scatter_measurements<double><<<grid, 256, 0, st>>>(p->geo, (const double2*)y, (const long long*)indices,
+                                                                   p->offs, probs, probs_batch_stride, (double2*)p->yg,
+                                                                   (double*)p->pinv);
+        }
+        if (p->pend != cudaSuccess) {
+            cudaError_t e = p->pend;
+            p->pend = cudaSuccess;
+            throw Err{VDAMP_ERR_CUDA, std::string("scatter_measurements: ") + cudaGetErrorString(e)};
+        }
         p->have_meas = true;
     });
 }

@@ -250,3 +250,46 @@ def finalize(w_hat: WaveletCoeffs, y, mask: SamplingMask, *, precision="fp64", d
     out = plan.empty_images()
     plan.finalize(w, out)
     return out[0].cpu().numpy().astype(np.complex128)
+
+
+# ---------------------------------------------------------------------------
+# Repeated batched reconstruction (serving / benchmark entry point)
+# ---------------------------------------------------------------------------
+class BatchReconstructor:
+    """Reconstruct batches of B images of one geometry, reusing the device plan.
+
+    ``__call__`` takes the concatenated measurements (see :func:`prepare_batch`)
+    as numpy arrays or torch tensors -- host (ideally pinned) or device -- and
+    returns x_hat (B, H, W).  With ``out`` a pinned host tensor the result is
+    copied back asynchronously into it; the call synchronises before returning.
+    """
+
+    def __init__(self, height, width, scales, batch, *, precision="fp32", device=None):
+        from .plan import get_plan
+        SubbandLayout.create(height, width, scales)
+        self.plan = get_plan(height, width, scales, batch, precision, device)
+        self._x = self.plan.empty_images()
+
+    def upload(self, inp: BatchInputs, pin=True):
+        """Host BatchInputs -> torch host tensors (pinned) ready for __call__."""
+        import torch
+        t = lambda a, dt: (torch.from_numpy(np.ascontiguousarray(a)).to(dt).pin_memory() if pin
+                           else torch.from_numpy(np.ascontiguousarray(a)).to(dt))
+        return dict(y=t(inp.y, self.plan.cdtype), indices=t(inp.indices, torch.int64),
+                    counts=inp.counts, probs=t(inp.probs, torch.float64), noise_var=inp.noise_var,
+                    shared_probs=inp.shared_probs)
+
+    def __call__(self, y, indices, counts, probs, noise_var, n_iters, *, shared_probs=True, out=None,
+                 stream=None, sync=True):
+        if n_iters < 1:
+            raise ValueError(f"need at least one iteration, got {n_iters}")
+        p = self.plan
+        p.set_measurements(y, indices, counts, probs, noise_var, shared_probs, stream=stream)
+        x = p.run(n_iters, x_hat=self._x, stream=stream)
+        if out is not None:
+            out.copy_(x, non_blocking=True)
+            x = out
+        if sync:
+            import torch
+            torch.cuda.current_stream(p.device).synchronize() if stream is None else stream.synchronize()
+        return x
