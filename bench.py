@@ -175,6 +175,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="print a short human summary instead of JSON")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -347,7 +348,12 @@ def main():
         line["e2e"] = e2e
     if cpu_base is not None:
         line["cpu_baseline"] = cpu_base
-    print(json.dumps(line), flush=True)
+    if args.quick:
+        print(f"value={value:.0f} ms/step={ms_per_step:.3f} clocks={line['clocks']}")
+        for k, v in kernels.items():
+            print(f"  {k:18s} {v['ms_per_step']:.3f} ms/step  {v['GBps'] or 0:.0f} GB/s")
+    else:
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

@@ -46,6 +46,8 @@ struct Plan {
     long long N;
     Geo geo;
     std::vector<Pass> passes;       // fine -> coarse
+    std::vector<int> item_start;    // SURE work items (balanced subband groups)
+    std::vector<int> item_list;
     size_t csz;                     // bytes per complex element
     int cw, logcw, ntiles, rowlog;  // column tile width, row_pass rows per CTA
     // device buffers
@@ -202,11 +204,10 @@ struct Seq {
     }
 
     size_t col_smem() const {
-        const int np = 2 * p->s, pairs = np * p->cw;
-        int G = PNT / pairs; if (G < 1) G = 1;
+        const int np = 2 * p->s;
         const size_t E = (size_t)p->H << p->logcw;
-        return E * sizeof(C) + (size_t)p->H * sizeof(C) + E * sizeof(double) +
-               (size_t)std::max(pairs * G, PNT) * sizeof(double) + (size_t)pairs * sizeof(double);
+        return E * sizeof(C) + (size_t)p->H * sizeof(C) + (size_t)np * PNT * sizeof(double) +
+               (size_t)np * p->cw * sizeof(double) + (size_t)np * p->H * sizeof(double);
     }
 
     void col(int mode, const C* src, C* dst, int cls) {
@@ -242,9 +243,14 @@ struct Seq {
         a.par = p->par; a.parf = p->parf; a.trace = trace;
         a.w0 = use_w0 ? (const C*)p->w0 : nullptr;
         a.kA = (R*)p->kA; a.kB = (R*)p->kB;
-        dim3 grid(p->S, p->B);
+        for (size_t i = 0; i <= p->item_start.size() - 1; ++i) a.item_start[i] = p->item_start[i];
+        for (size_t i = 0; i < p->item_list.size(); ++i) a.item_list[i] = p->item_list[i];
+        dim3 grid((unsigned)p->item_start.size() - 1, p->B);
         const int maxlen = *std::max_element(p->geo.len, p->geo.len + p->S);
-        const size_t sm = (size_t)std::min(maxlen, SCAP) * sizeof(R);
+        const int cap = Scap<R>::v;
+        const size_t slots = (size_t)(cap + cap / 32 + 1) + 1;       // padded key slots (KI) per buffer
+        const size_t sm = slots * sizeof(R);
+        (void)maxlen;
         auto k = sure_select<R>;
         set_smem(k, sm);
         Launch L(p, 3, st);
@@ -362,7 +368,7 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         if (!pow2(height) || !pow2(width) || height < 2 || width < 2 || height > 2048 || width > 2048)
             throw Err{VDAMP_ERR_UNSUPPORTED, "this build supports power-of-two image sizes in [2, 2048] only"};
         if (precision != VDAMP_FP32 && precision != VDAMP_FP64) throw Err{VDAMP_ERR_ARG, "precision must be 0 (fp32) or 1 (fp64)"};
-        if (1 + 3 * scales > MAXS) throw Err{VDAMP_ERR_UNSUPPORTED, "too many scales"};
+        if (1 + 3 * scales > MAXS || scales > 12) throw Err{VDAMP_ERR_UNSUPPORTED, "too many scales (max 12)"};
         p = new Plan();
         p->H = height; p->W = width; p->s = scales; p->B = batch; p->prec = precision; p->dev = device;
         p->S = 1 + 3 * scales;
@@ -394,6 +400,32 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
             p->passes.push_back(ps);
             lvl += k;
         }
+        {
+            // SURE work items: subbands > SCAP/2 alone, the rest optionally packed
+            // first-fit (largest first) into bins of SCAP keys.  Packing is off:
+            // measured slower at 1 CTA/SM (round 1, cfg1: 10.0 vs 6.9 ms/step)
+            const bool pack_small = false;
+            std::vector<int> order(p->S);
+            for (int j = 0; j < p->S; ++j) order[j] = j;
+            std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return g.len[x] > g.len[y]; });
+            std::vector<std::vector<int>> bins;
+            std::vector<long long> fill;
+            for (int j : order) {
+                const long long L = g.len[j];
+                int placed = -1;
+                if (L <= SCAP / 2 && pack_small)
+                    for (size_t bi = 0; bi < bins.size(); ++bi)
+                        if (fill[bi] + L <= SCAP && fill[bi] > 0 && g.len[bins[bi][0]] <= SCAP / 2) { placed = (int)bi; break; }
+                if (placed < 0) { bins.push_back({}); fill.push_back(0); placed = (int)bins.size() - 1; }
+                bins[placed].push_back(j);
+                fill[placed] += L;
+            }
+            p->item_start.assign(1, 0);
+            for (auto& b : bins) {
+                for (int j : b) p->item_list.push_back(j);
+                p->item_start.push_back((int)p->item_list.size());
+            }
+        }
         p->cw = std::max(1, std::min(width, PCAP / height));
         p->logcw = ilog2(p->cw);
         p->ntiles = width / p->cw;
@@ -422,8 +454,9 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         p->twW = dalloc(p, (size_t)width * cs);
         p->trtmp = (double*)dalloc(p, (size_t)batch * p->S * TRACE_F * sizeof(double));
         const int maxlen = *std::max_element(g.len, g.len + p->S);
-        if (maxlen > SCAP) {
-            if (maxlen / SCAP > MAXTILES) throw Err{VDAMP_ERR_UNSUPPORTED, "subband too large"};
+        const int capk = precision == VDAMP_FP32 ? Scap<float>::v : Scap<double>::v;
+        if (maxlen > capk) {
+            if (maxlen / capk > MAXTILES) throw Err{VDAMP_ERR_UNSUPPORTED, "subband too large"};
             p->kA = dalloc(p, img * rs);
             p->kB = dalloc(p, img * rs);
         }

@@ -24,7 +24,7 @@ template <typename C, bool INV> __device__ __forceinline__ C cmul_mi(C a) {
 }
 
 // |r| exactly as used by both the SURE scan and the apply (they must agree).
-__device__ __forceinline__ float cmag(float2 a) { return hypotf(a.x, a.y); }
+__device__ __forceinline__ float cmag(float2 a) { return sqrtf(fmaf(a.x, a.x, a.y * a.y)); }
 __device__ __forceinline__ double cmag(double2 a) { return hypot(a.x, a.y); }
 
 // Haar taps: the reference divides by sqrt(2) (src/wavelet.py:109-128); the
@@ -51,10 +51,13 @@ template <> struct Haar<float> {
 // Onsager-corrected soft threshold of one coefficient (src/vdamp.py:125-131,
 // src/denoise.py:166-168):  (r * max(1 - t/|r|, 0) - alpha * r) * gain,
 // |r| == t -> shrunk to 0.  (t, alpha, gain) = (0, 0, 1) is the identity.
+__device__ __forceinline__ float sdiv(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double sdiv(double a, double b) { return a / b; }
+
 template <typename R, typename C>
 __device__ __forceinline__ C onsager(C r, R t, R alpha, R gain) {
     R m = cmag(r);
-    R sh = (m > t) ? (R(1) - t / m) : R(0);
+    R sh = (m > t) ? (R(1) - sdiv(t, m)) : R(0);   // m > t >= 0, so m is normal
     R wx = r.x * sh, wy = r.y * sh;
     return mk<C>((wx - alpha * r.x) * gain, (wy - alpha * r.y) * gain);
 }

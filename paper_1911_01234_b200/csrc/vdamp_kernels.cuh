@@ -23,7 +23,8 @@ constexpr int MAXS = 64;          // subbands supported (scales <= 21)
 constexpr int PNT = 256;          // threads of strip / column kernels
 constexpr int PCAP = 4096;        // complex elements per strip / column tile
 constexpr int SNT = 1024;         // threads of the SURE kernel
-constexpr int SCAP = 16384;       // magnitudes sorted in shared memory at once
+constexpr int SCAP = 16384;       // fp32 magnitudes sorted in shared memory at once
+template <typename R> struct Scap { static constexpr int v = SCAP; };
 constexpr int MAXTILES = 256;     // SCAP-tiles per subband (n <= 4M)
 constexpr double ALPHA_CLAMP = 1.0 - 1e-9;   // src/vdamp.py:25
 constexpr double TAU_FLOOR = 1e-300;         // src/vdamp.py:118
@@ -295,14 +296,13 @@ __device__ __forceinline__ void band_profiles(int s, int j, int& prow, int& pcol
 }
 
 template <typename R, int MODE>
-__global__ void __launch_bounds__(PNT) col_pass(Geo g, ColArgs<R> p) {
+__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass(Geo g, ColArgs<R> p) {
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* buf = reinterpret_cast<C*>(smem_raw);
     const int H = g.H, W = g.W, cw = p.cw, lc = p.logcw;
     const int E = H << lc;
     C* tws = buf + E;
-    double* wv = reinterpret_cast<double*>(tws + H);
     const int tile = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
     const int c0 = tile << lc;
     const long long ib = (long long)bi * g.N;
@@ -323,27 +323,38 @@ __global__ void __launch_bounds__(PNT) col_pass(Geo g, ColArgs<R> p) {
     }
     const R cs = (R)g.sign_c;
     const double nv = (MODE == COL_VDAMP) ? p.noise_var[bi] : 0.0;
-    for (int e = tid; e < E; e += PNT) {
-        const long long gi = ib + (long long)(e >> lc) * W + c0 + (e & (cw - 1));
-        const C X = cscale(buf[e], sc * cs);     // c * FFT2u, so (-1)^(k1+k2) X_centred
-        const R pv = p.pinv[gi];
-        C v;
-        if (MODE == COL_VDAMP) {
-            double w = 0.0;
-            if (pv != R(0)) {
-                const C zc = csub(p.yg[gi], X);          // (-1)^(k1+k2) z  (src/vdamp.py:112)
-                v = cscale(zc, pv);                      // P^-1 z           (src/vdamp.py:113)
-                const double pd = (double)pv;
-                const double z2 = (double)zc.x * (double)zc.x + (double)zc.y * (double)zc.y;
-                w = pd * ((pd - 1.0) * z2 + nv);         // tau weight       (src/vdamp.py:74-75)
-            } else {
-                v = mk<C>(R(0), R(0));
+    // tau partials: tau_j = sum_w a_j(w1) b_j(w2) weight(w) (separable |F psi_j|^2,
+    // src/vdamp.py:59-78).  Thread tid always sees column c = tid % cw (PNT is a
+    // multiple of cw), so it accumulates its rows' weights per row profile in
+    // registers; the cw-column partials are combined in a fixed order below.
+    constexpr int PER = PCAP / PNT;               // elements per thread
+    R wreg[PER];                                  // tau weights of this thread's elements
+    const int np = 2 * g.s;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int e = tid + i * PNT;
+        wreg[i] = R(0);
+        if (e < E) {
+            const int n = e >> lc;
+            const long long gi = ib + (long long)n * W + c0 + (e & (cw - 1));
+            const C X = cscale(buf[e], sc * cs);     // c * FFT2u, so (-1)^(k1+k2) X_centred
+            const R pv = p.pinv[gi];
+            C v;
+            if (MODE == COL_VDAMP) {
+                if (pv != R(0)) {
+                    const C zc = csub(p.yg[gi], X);          // (-1)^(k1+k2) z  (src/vdamp.py:112)
+                    v = cscale(zc, pv);                      // P^-1 z           (src/vdamp.py:113)
+                    const double pd = (double)pv;
+                    const double z2 = (double)zc.x * (double)zc.x + (double)zc.y * (double)zc.y;
+                    wreg[i] = (R)(pd * ((pd - 1.0) * z2 + nv));   // tau weight (src/vdamp.py:74-75)
+                } else {
+                    v = mk<C>(R(0), R(0));
+                }
+            } else {  // COL_FINAL: measured k-space where sampled (src/vdamp.py:147-150)
+                v = (pv != R(0)) ? p.yg[gi] : X;
             }
-            wv[e] = w;
-        } else {  // COL_FINAL: measured k-space where sampled (src/vdamp.py:147-150)
-            v = (pv != R(0)) ? p.yg[gi] : X;
+            buf[e] = v;
         }
-        buf[e] = v;
     }
     __syncthreads();
     block_fft<C, true, PNT, PCAP, true>(buf, g.logH, lc, 1, cw, tws);
@@ -351,34 +362,38 @@ __global__ void __launch_bounds__(PNT) col_pass(Geo g, ColArgs<R> p) {
         p.dst[ib + (long long)(e >> lc) * W + c0 + (e & (cw - 1))] = cscale(buf[e], sc);
     if (MODE != COL_VDAMP) return;
 
-    // tau partials: tau_j = sum_w a_j(w1) b_j(w2) weight(w)  (separable |F psi_j|^2)
-    double* part = wv + E;                        // max(PNT, pairs) doubles
-    const int np = 2 * g.s;
-    const int pairs = np * cw;
-    int G = PNT / pairs; if (G < 1) G = 1;
-    double* psum = part + (pairs * G > PNT ? pairs * G : PNT);
-    for (int it = tid; it < pairs * G; it += PNT) {
-        const int pr = it % pairs, gg = it / pairs;
-        const int pf = pr / cw, c = pr % cw;
-        const double* A = p.prow + (long long)pf * H;
-        double acc = 0.0;
-        for (int n = gg; n < H; n += G) acc += A[n] * wv[(n << lc) + c];
-        part[it] = acc;
+    // thread tid always sees column c = tid % cw (PNT is a multiple of cw):
+    // per row profile q, sum its rows in registers, then combine the threads
+    // of each column in a fixed order (deterministic)
+    double* part = reinterpret_cast<double*>(tws + H);   // [np][PNT] thread partials
+    double* prs = part + np * PNT + np * cw;             // [np][H] row profiles
+    for (int i = tid; i < np * H; i += PNT) prs[i] = p.prow[i];
+    __syncthreads();
+    for (int q = 0; q < np; ++q) {
+        double a = 0.0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = tid + i * PNT;
+            if (e < E) a += prs[q * H + (e >> lc)] * (double)wreg[i];
+        }
+        part[q * PNT + tid] = a;
     }
     __syncthreads();
-    for (int pr = tid; pr < pairs; pr += PNT) {
-        double acc = 0.0;
-        for (int gg = 0; gg < G; ++gg) acc += part[gg * pairs + pr];
-        psum[pr] = acc;
+    double* psum = part + np * PNT;                       // [np][cw] column partials
+    for (int it = tid; it < np * cw; it += PNT) {
+        const int q = it / cw, c = it % cw;
+        double sacc = 0.0;
+        for (int t = c; t < PNT; t += cw) sacc += part[q * PNT + t];
+        psum[q * cw + c] = sacc;
     }
     __syncthreads();
     for (int j = tid; j < g.S; j += PNT) {
         int pr_, pc_;
         band_profiles(g.s, j, pr_, pc_);
         const double* Bc = p.pcol + (long long)pc_ * W + c0;
-        double acc = 0.0;
-        for (int c = 0; c < cw; ++c) acc += Bc[c] * psum[pr_ * cw + c];
-        p.taupart[((long long)bi * p.ntiles + tile) * g.S + j] = acc;
+        double sacc = 0.0;
+        for (int c = 0; c < cw; ++c) sacc += Bc[c] * psum[pr_ * cw + c];
+        p.taupart[((long long)bi * p.ntiles + tile) * g.S + j] = sacc;
     }
 }
 
@@ -424,6 +439,8 @@ struct SelArgs {
     const typename CT<R>::T* w0;     // [B][N] ground-truth coefficients or null
     R* kA;                           // [B][N] key scratch (subbands > SCAP)
     R* kB;
+    int item_start[MAXS + 1];        // work items: subbands item_list[item_start[i] .. item_start[i+1])
+    int item_list[MAXS];
 };
 
 struct Best { double risk, t, cnt, inv; };
@@ -437,19 +454,115 @@ __device__ __forceinline__ void consider(Best& b, double risk, double t, double 
     if (better(c, b)) b = c;
 }
 
-template <typename R>
-__device__ void bitonic_sort(R* s, int n) {
-    for (int k = 2; k <= n; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int p = threadIdx.x; p < (n >> 1); p += SNT) {
-                const int i = 2 * p - (p & (j - 1));
-                const int l = i + j;
-                const bool asc = (i & k) == 0;
-                R x = s[i], y = s[l];
-                if ((x > y) == asc) { s[i] = y; s[l] = x; }
+// ---------------------------------------------------------------------------
+// Block bitonic sort of n (power of two) magnitudes.  Thread t of the A = n/E
+// active threads owns the E consecutive keys [t*E, t*E+E) in registers:
+// partner distances j < E are register compare-exchanges, E <= j < 32E warp
+// shuffles, larger ones go through shared memory.
+// ---------------------------------------------------------------------------
+// shared-memory key slot of sorted position i: one pad word per 32 keys, so
+// the blocked per-thread ownership (lane stride E) is bank-conflict free
+__device__ __forceinline__ int KI(int i) { return i + (i >> 5); }
+
+__device__ __forceinline__ float kmin(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ float kmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double kmin(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ double kmax(double a, double b) { return fmax(a, b); }
+
+template <typename R, int E, int J>
+__device__ __forceinline__ void reg_stage(R (&v)[E], int base, int k) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        if ((e & J) == 0) {
+            const int f = e | J;
+            const bool asc = ((base + e) & k) == 0;
+            const R a = v[e], b = v[f];
+            const R lo = kmin(a, b), hi = kmax(a, b);
+            v[e] = asc ? lo : hi;
+            v[f] = asc ? hi : lo;
+        }
+    }
+}
+
+template <typename R, int E>
+__device__ __forceinline__ void reg_stages(R (&v)[E], int base, int k, int j) {
+    // j < E: all remaining distances of this k down to 1
+    if (E > 16 && j >= 16) { reg_stage<R, E, (E > 16 ? 16 : 1)>(v, base, k); }
+    if (E > 8 && j >= 8)   { reg_stage<R, E, (E > 8 ? 8 : 1)>(v, base, k); }
+    if (E > 4 && j >= 4)   { reg_stage<R, E, (E > 4 ? 4 : 1)>(v, base, k); }
+    if (E > 2 && j >= 2)   { reg_stage<R, E, (E > 2 ? 2 : 1)>(v, base, k); }
+    if (E > 1 && j >= 1)   { reg_stage<R, E, 1>(v, base, k); }
+}
+
+template <typename R, int E>
+__device__ __noinline__ void block_sort_e(R* s, int n) {
+    const int A = n / E;
+    const int tid = threadIdx.x;
+    const bool act = tid < A;
+    const int base = tid * E;
+    const unsigned mask = A >= 32 ? 0xffffffffu : ((1u << A) - 1u);
+    R v[E];
+    if (act) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = s[KI(base + e)];
+    }
+    for (int k = 2; k <= n; k <<= 1) {
+        int j = k >> 1;
+        for (; j >= 32 * E; j >>= 1) {                     // cross-warp: shared memory
+            __syncthreads();
+            if (act) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) s[KI(base + e)] = v[e];
             }
             __syncthreads();
+            if (act) {
+                const bool asc = (base & k) == 0;
+                const bool lower = (base & j) == 0;
+                const bool keep_min = lower == asc;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const R p = s[KI((base + e) ^ j)];
+                    v[e] = keep_min ? kmin(v[e], p) : kmax(v[e], p);
+                }
+            }
         }
+        if (act) {
+            for (; j >= E; j >>= 1) {                      // cross-lane: shuffles
+                const int m = j / E;
+                const bool asc = (base & k) == 0;
+                const bool keep_min = ((tid & m) == 0) == asc;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const R p = __shfl_xor_sync(mask, v[e], m);
+                    v[e] = keep_min ? kmin(v[e], p) : kmax(v[e], p);
+                }
+            }
+            if (j >= 1) reg_stages<R, E>(v, base, k, j);
+        }
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) s[KI(base + e)] = v[e];
+    }
+    __syncthreads();
+}
+
+template <typename R>
+__device__ void block_sort(R* s, int n) {
+    if (n < 2) { __syncthreads(); return; }
+    int E = n / SNT;
+    const int small = n / 32 < 8 ? n / 32 : 8;
+    if (E < small) E = small;
+    if (E < 1) E = 1;
+    switch (E) {
+        case 1: block_sort_e<R, 1>(s, n); break;
+        case 2: block_sort_e<R, 2>(s, n); break;
+        case 4: block_sort_e<R, 4>(s, n); break;
+        case 8: block_sort_e<R, 8>(s, n); break;
+        case 16: block_sort_e<R, 16>(s, n); break;
+        default: block_sort_e<R, 16>(s, n); break;
+    }
 }
 
 // Evaluate the candidates owned by this thread on one tile of sorted
@@ -458,25 +571,26 @@ __device__ void bitonic_sort(R* s, int n) {
 template <typename R>
 __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, int n, double tau,
                                           double pre_tile, double suf_tile, double next_tile_first,
-                                          double* sh, Best& best) {
+                                          double* sh, Best& best, double* totinv) {
     const int tid = threadIdx.x;
     const int E = T >= SNT ? T / SNT : 1;
     const bool act = tid * E < T;
     const int b0 = tid * E;
     double ssq = 0.0, sinv = 0.0;
     if (act) {
-        for (int e = 0; e < E; ++e) { const double m = (double)keys[b0 + e]; ssq += m * m; }
-        for (int e = E - 1; e >= 0; --e) { const double m = (double)keys[b0 + e]; if (m > 0) sinv += 1.0 / m; }
+        for (int e = 0; e < E; ++e) { const double m = (double)keys[KI(b0 + e)]; ssq += m * m; }
+        for (int e = E - 1; e >= 0; --e) { const double m = (double)keys[KI(b0 + e)]; if (m > 0) sinv += 1.0 / m; }
     }
     const double pre = block_excl_scan<SNT, false>(ssq, sh) + pre_tile;
     const double suf = block_excl_scan<SNT, true>(sinv, sh) + suf_tile;
+    if (tid == 0 && tilebase == 0) *totinv = suf + sinv;     // sum of all inverses
     if (!act) return;
     const double nt = (double)n * tau;
     double inv_above = suf, sq_after = 0.0;
     for (int e = E - 1; e >= 0; --e) {
         const int il = b0 + e;
-        const double m = (double)keys[il];
-        const double nxt = (il + 1 < T) ? (double)keys[il + 1] : next_tile_first;
+        const double m = (double)keys[KI(il)];
+        const double nxt = (il + 1 < T) ? (double)keys[KI(il + 1)] : next_tile_first;
         if (m != nxt) {
             const double zeroed = pre + (ssq - sq_after);       // sum_{j <= i} m_j^2
             const double cnt = (double)(n - (tilebase + il + 1));
@@ -495,16 +609,24 @@ __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, in
     }
 }
 
+struct SelShared {
+    double sh[SNT / 32 + 2];
+    double tsq[MAXTILES], tinv[MAXTILES], tpre[MAXTILES], tsuf[MAXTILES];
+    double tau, totinv;
+    Best best[SNT / 32];
+};
+
+// Exact SURE selection for subband j of image bi (src/denoise.py:62-118,
+// 165-173; clamp src/vdamp.py:121-124).
 template <typename R>
-__global__ void __launch_bounds__(SNT, 1) sure_select(Geo g, SelArgs<R> a) {
+__device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R* keys, SelShared& S_) {
     typedef typename CT<R>::T C;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    R* keys = reinterpret_cast<R*>(smem_raw);
-    __shared__ double sh[SNT / 32 + 2];
-    __shared__ double tsq[MAXTILES], tinv[MAXTILES], tpre[MAXTILES], tsuf[MAXTILES];
-    __shared__ double s_tau, s_totinv;
-    __shared__ Best s_best[SNT / 32];
-    const int j = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
+    double* sh = S_.sh;
+    double* tsq = S_.tsq; double* tinv = S_.tinv; double* tpre = S_.tpre; double* tsuf = S_.tsuf;
+    double& s_tau = S_.tau;
+    double& s_totinv = S_.totinv;
+    Best* s_best = S_.best;
+    const int tid = threadIdx.x;
     const int n = g.len[j];
     const long long base = (long long)bi * g.N + g.off[j];
     if (tid == 0) {
@@ -516,14 +638,15 @@ __global__ void __launch_bounds__(SNT, 1) sure_select(Geo g, SelArgs<R> a) {
     const C* rs = a.r + base;
     const C* w0 = a.w0 ? a.w0 + base : nullptr;
     double err = 0.0, ref = 0.0;
-    const bool large = n > SCAP;
-    const int T = large ? SCAP : n;
-    const int ntl = large ? n / SCAP : 1;
+    constexpr int CAPK = Scap<R>::v;
+    const bool large = n > CAPK;
+    const int T = large ? CAPK : n;
+    const int ntl = large ? n / CAPK : 1;
     const R* sorted = keys;
     for (int c0 = 0; c0 < n; c0 += T) {
         for (int e = tid; e < T; e += SNT) {
             const C v = rs[c0 + e];
-            keys[e] = cmag(v);
+            keys[KI(e)] = cmag(v);
             if (w0) {
                 const C w = w0[c0 + e];
                 const double dx = (double)v.x - (double)w.x, dy = (double)v.y - (double)w.y;
@@ -532,9 +655,9 @@ __global__ void __launch_bounds__(SNT, 1) sure_select(Geo g, SelArgs<R> a) {
             }
         }
         __syncthreads();
-        bitonic_sort(keys, T);
+        block_sort(keys, T);
         if (large) {
-            for (int e = tid; e < T; e += SNT) a.kA[base + c0 + e] = keys[e];
+            for (int e = tid; e < T; e += SNT) a.kA[base + c0 + e] = keys[KI(e)];
             __syncthreads();
         }
     }
@@ -543,7 +666,7 @@ __global__ void __launch_bounds__(SNT, 1) sure_select(Geo g, SelArgs<R> a) {
         R* srcb = a.kA + base;
         R* dstb = a.kB + base;
         const int per = n / SNT;
-        for (int w = SCAP; w < n; w <<= 1) {
+        for (int w = CAPK; w < n; w <<= 1) {
             const int o0 = tid * per;
             const int pb = o0 / (2 * w) * (2 * w);
             const R* A = srcb + pb;
@@ -567,13 +690,13 @@ __global__ void __launch_bounds__(SNT, 1) sure_select(Geo g, SelArgs<R> a) {
         // tile totals (ascending squares, descending inverses)
         for (int t = 0; t < ntl; ++t) {
             double q = 0.0, v = 0.0;
-            for (int e = tid; e < SCAP; e += SNT) {
-                const double m = (double)sorted[t * SCAP + e];
+            for (int e = tid; e < CAPK; e += SNT) {
+                const double m = (double)sorted[t * CAPK + e];
                 q += m * m;
             }
             q = block_sum<SNT>(q, sh);
-            for (int e = tid; e < SCAP; e += SNT) {
-                const double m = (double)sorted[t * SCAP + e];
+            for (int e = tid; e < CAPK; e += SNT) {
+                const double m = (double)sorted[t * CAPK + e];
                 if (m > 0) v += 1.0 / m;
             }
             v = block_sum<SNT>(v, sh);
@@ -587,7 +710,6 @@ __global__ void __launch_bounds__(SNT, 1) sure_select(Geo g, SelArgs<R> a) {
         for (int t = 0; t < ntl; ++t) { tpre[t] = acc; acc += large ? tsq[t] : 0.0; }
         acc = 0.0;
         for (int t = ntl - 1; t >= 0; --t) { tsuf[t] = acc; acc += large ? tinv[t] : 0.0; }
-        s_totinv = acc;
     }
     __syncthreads();
     const double tau = fmax(s_tau, TAU_FLOOR);
@@ -596,26 +718,17 @@ __global__ void __launch_bounds__(SNT, 1) sure_select(Geo g, SelArgs<R> a) {
     for (int t = 0; t < ntl; ++t) {
         if (large) {
             __syncthreads();
-            for (int e = tid; e < SCAP; e += SNT) keys[e] = sorted[t * SCAP + e];
+            for (int e = tid; e < CAPK; e += SNT) keys[KI(e)] = sorted[t * CAPK + e];
             __syncthreads();
         }
-        const double nf = (t + 1 < ntl) ? (double)sorted[(t + 1) * SCAP] : INFINITY;
-        scan_tile<R>(keys, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, best);
+        const double nf = (t + 1 < ntl) ? (double)sorted[(t + 1) * CAPK] : INFINITY;
+        scan_tile<R>(keys, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, best, &s_totinv);
     }
     // candidate t = 0 when no magnitude is zero (src/denoise.py:84)
     __syncthreads();
-    if (!large) {
-        // single tile: total of inverses = exclusive suffix of thread 0 + its own
-        double v = 0.0;
-        const int E = T >= SNT ? T / SNT : 1;
-        if (tid * E < T)
-            for (int e = E - 1; e >= 0; --e) { const double m = (double)keys[tid * E + e]; if (m > 0) v += 1.0 / m; }
-        const double ex = block_excl_scan<SNT, true>(v, sh);
-        if (tid == 0) s_totinv = ex + v;
-        __syncthreads();
-    }
+    __syncthreads();
     if (tid == 0) {
-        const double m0 = (double)sorted[0];
+        const double m0 = large ? (double)sorted[0] : (double)keys[0];
         if (m0 > 0) {
             const double totinv = s_totinv;
             const double nn = (double)n;
@@ -652,6 +765,19 @@ __global__ void __launch_bounds__(SNT, 1) sure_select(Geo g, SelArgs<R> a) {
             tr[0] = s_tau; tr[1] = bb.t; tr[2] = bb.t / tau; tr[3] = ac; tr[4] = alpha;
             tr[5] = clamped ? 1.0 : 0.0; tr[6] = err; tr[7] = ref;
         }
+    }
+}
+
+template <typename R>
+__global__ void __launch_bounds__(SNT, 1) sure_select(Geo g, SelArgs<R> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    R* keys = reinterpret_cast<R*>(smem_raw);
+    __shared__ SelShared S_;
+    const int it = blockIdx.x, bi = blockIdx.y;
+    // one work item = one large subband, or several small ones packed to ~SCAP keys
+    for (int q = a.item_start[it]; q < a.item_start[it + 1]; ++q) {
+        select_band<R>(g, a, a.item_list[q], bi, keys, S_);
+        __syncthreads();
     }
 }
 
