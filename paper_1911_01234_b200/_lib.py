@@ -12,7 +12,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvdamp_b200.so")
+LIB_PATH = os.environ.get("VDAMP_LIB") or os.path.join(_HERE, "libvdamp_b200.so")
 
 VDAMP_OK = 0
 VDAMP_ERR_ARG = 1

@@ -131,6 +131,7 @@ struct Seq {
     typedef typename CT<R>::T C;
     Plan* p;
     cudaStream_t st;
+    cudaStream_t& st_ = st;
     C* r() { return (C*)p->r; }
 
     // Haar synthesis of coefficients `coef` with params `par`; FFT -> T1 when
@@ -243,18 +244,32 @@ struct Seq {
         a.par = p->par; a.parf = p->parf; a.trace = trace;
         a.w0 = use_w0 ? (const C*)p->w0 : nullptr;
         a.kA = (R*)p->kA; a.kB = (R*)p->kB;
-        for (size_t i = 0; i <= p->item_start.size() - 1; ++i) a.item_start[i] = p->item_start[i];
-        for (size_t i = 0; i < p->item_list.size(); ++i) a.item_list[i] = p->item_list[i];
-        dim3 grid((unsigned)p->item_start.size() - 1, p->B);
-        const int maxlen = *std::max_element(p->geo.len, p->geo.len + p->S);
-        const int cap = Scap<R>::v;
-        const size_t slots = (size_t)(cap + cap / 32 + 1) + 1;       // padded key slots (KI) per buffer
-        const size_t sm = slots * sizeof(R);
-        (void)maxlen;
-        auto k = sure_select<R>;
-        set_smem(k, sm);
-        Launch L(p, 3, st);
-        k<<<grid, SNT, sm, st>>>(p->geo, a);
+        // big subbands: 1024-thread CTAs with the full sort workspace; small ones:
+        // 256-thread CTAs with little shared memory, many per SM
+        for (int big = 1; big >= 0; --big) {
+            std::vector<int> st{0}, li;
+            for (int j = 0; j < p->S; ++j)
+                if ((p->geo.len[j] > SMALL_N) == (big == 1)) { li.push_back(j); st.push_back((int)li.size()); }
+            if (li.empty()) continue;
+            for (size_t i = 0; i < st.size(); ++i) a.item_start[i] = st[i];
+            for (size_t i = 0; i < li.size(); ++i) a.item_list[i] = li[i];
+            dim3 grid((unsigned)li.size(), p->B);
+            Launch L(p, 3, st_);
+            if (big) {
+                const int cap = Scap<R>::v;
+                const size_t slots = (size_t)(cap + cap / 32 + 1) + 1;
+                const size_t sm = sizeof(R) == 4 ? 2 * (slots + 1) * sizeof(R) + (CS_BUCKETS / 2) * sizeof(unsigned)
+                                                 : slots * sizeof(R);
+                auto k = sure_select<R, SNT>;
+                set_smem(k, sm);
+                k<<<grid, SNT, sm, st_>>>(p->geo, a);
+            } else {
+                const size_t sm = (size_t)(SMALL_N + SMALL_N / 32 + 2) * sizeof(R);
+                auto k = sure_select<R, SNT_SMALL>;
+                set_smem(k, sm);
+                k<<<grid, SNT_SMALL, sm, st_>>>(p->geo, a);
+            }
+        }
     }
 
     void apply(const C* in, C* out, const double* par) {
@@ -688,6 +703,13 @@ int vdamp_kernel_times(vdamp_plan_t plan, double* ms, int64_t* launches) {
         }
     });
 }
+
+#ifdef VDAMP_PHASE_TIMING
+// debug build only: copy the per-(image, subband) phase clocks of the last select launch
+extern "C" VDAMP_API int vdamp_debug_phase_times(long long* out, int images) {
+    return guard([&] { CK(cudaMemcpyFromSymbol(out, g_phase, (size_t)images * 64 * 4 * sizeof(long long))); });
+}
+#endif
 
 int vdamp_launch_count(vdamp_plan_t plan, int64_t* count, int reset) {
     return guard([&] {

@@ -22,7 +22,9 @@ namespace vdamp {
 constexpr int MAXS = 64;          // subbands supported (scales <= 21)
 constexpr int PNT = 256;          // threads of strip / column kernels
 constexpr int PCAP = 4096;        // complex elements per strip / column tile
-constexpr int SNT = 1024;         // threads of the SURE kernel
+constexpr int SNT = 1024;         // threads of the SURE kernel (subbands > SMALL_N)
+constexpr int SNT_SMALL = 256;    // threads of the small-subband SURE kernel
+constexpr int SMALL_N = 4096;     // subbands up to this size use the small kernel
 constexpr int SCAP = 16384;       // fp32 magnitudes sorted in shared memory at once
 template <typename R> struct Scap { static constexpr int v = SCAP; };
 constexpr int MAXTILES = 256;     // SCAP-tiles per subband (n <= 4M)
@@ -548,10 +550,10 @@ __device__ __noinline__ void block_sort_e(R* s, int n) {
     __syncthreads();
 }
 
-template <typename R>
+template <typename R, int NT>
 __device__ void block_sort(R* s, int n) {
     if (n < 2) { __syncthreads(); return; }
-    int E = n / SNT;
+    int E = n / NT;
     const int small = n / 32 < 8 ? n / 32 : 8;
     if (E < small) E = small;
     if (E < 1) E = 1;
@@ -560,66 +562,207 @@ __device__ void block_sort(R* s, int n) {
         case 2: block_sort_e<R, 2>(s, n); break;
         case 4: block_sort_e<R, 4>(s, n); break;
         case 8: block_sort_e<R, 8>(s, n); break;
-        case 16: block_sort_e<R, 16>(s, n); break;
         default: block_sort_e<R, 16>(s, n); break;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Counting sort of n <= SCAP float magnitudes (fp32 path).  Bucket = the key's
+// IEEE bits (monotone for x >= 0) shifted so that the nonzero range fits
+// CS_BUCKETS-1 buckets (float bits are logarithmic: ~1000 buckets per octave);
+// zeros go to bucket 0.  Histogram and scatter use packed 16-bit shared
+// counters; the scatter order inside a bucket is arbitrary, so every bucket
+// is finished by an insertion sort on the full key.  The sorted sequence is
+// unique, so the result is deterministic.  out must not alias keys.
+// ---------------------------------------------------------------------------
+constexpr int CS_BUCKETS = 32768;
+
+__device__ void counting_sort(const float* keys, float* out, unsigned* cnt, int n, double* sh) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const unsigned* kb = reinterpret_cast<const unsigned*>(keys);
+    unsigned* ob = reinterpret_cast<unsigned*>(out);
+    unsigned mn = 0xffffffffu, mx = 0;
+    for (int i = tid; i < n; i += SNT) {
+        const unsigned k = kb[KI(i)];
+        if (k) mn = min(mn, k);
+        mx = max(mx, k);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    unsigned* red = reinterpret_cast<unsigned*>(sh);
+    __syncthreads();
+    if (lane == 0) { red[w] = mn; red[32 + w] = mx; }
+    for (int i = tid; i < CS_BUCKETS / 2; i += SNT) cnt[i] = 0;
+    __syncthreads();
+    if (tid < 32) {
+        unsigned a = red[tid], b = red[32 + tid];
+        for (int o = 16; o > 0; o >>= 1) {
+            a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+        }
+        if (tid == 0) { red[64] = a; red[65] = b; }
+    }
+    __syncthreads();
+    mn = red[64]; mx = red[65];
+    if (mn > mx) mn = mx;                            // all zeros
+    int lo = 0;
+    while (((mx >> lo) - (mn >> lo)) >= (unsigned)(CS_BUCKETS - 2)) ++lo;
+    const unsigned base = mn >> lo;
+    // histogram
+    for (int i = tid; i < n; i += SNT) {
+        const unsigned k = kb[KI(i)];
+        const unsigned b = k ? (k >> lo) - base + 1u : 0u;
+        atomicAdd(&cnt[b >> 1], 1u << ((b & 1u) * 16));
+    }
+    __syncthreads();
+    // exclusive scan of the CS_BUCKETS 16-bit counts (thread t: buckets [32t, 32t+32))
+    {
+        constexpr int PER = CS_BUCKETS / 2 / SNT;    // packed words per thread
+        unsigned v[PER];
+        unsigned tot = 0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            v[i] = cnt[tid * PER + i];
+            tot += (v[i] & 0xffffu) + (v[i] >> 16);
+        }
+        // block exclusive scan of integer totals (exact in double)
+        unsigned run = (unsigned)block_excl_scan<SNT, false>((double)tot, sh + 66);
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const unsigned c0 = v[i] & 0xffffu, c1 = v[i] >> 16;
+            cnt[tid * PER + i] = run | ((run + c0) << 16);
+            run += c0 + c1;
+        }
+    }
+    __syncthreads();
+    // scatter (cursor = packed 16-bit half, never carries: offsets + counts <= n <= 16384)
+    for (int i = tid; i < n; i += SNT) {
+        const unsigned k = kb[KI(i)];
+        const unsigned b = k ? (k >> lo) - base + 1u : 0u;
+        const unsigned sft = (b & 1u) * 16;
+        const unsigned old = atomicAdd(&cnt[b >> 1], 1u << sft);
+        ob[KI((old >> sft) & 0xffffu)] = k;
+    }
+    __syncthreads();
+    // finish every bucket: insertion sort by the full key (owner = thread of the run start)
+    const int E = n >= SNT ? n / SNT : 1;
+    const int b0 = tid * E;
+    if (b0 < n) {
+        for (int e = 0; e < E; ++e) {
+            const int i = b0 + e;
+            const unsigned k0 = ob[KI(i)];
+            const unsigned bk = k0 ? (k0 >> lo) - base + 1u : 0u;
+            if (i > 0) {
+                const unsigned kp = ob[KI(i - 1)];
+                if ((kp ? (kp >> lo) - base + 1u : 0u) == bk) continue;   // not a run start
+            }
+            int end = i + 1;
+            while (end < n) {
+                const unsigned kn = ob[KI(end)];
+                if ((kn ? (kn >> lo) - base + 1u : 0u) != bk) break;
+                ++end;
+            }
+            for (int a = i + 1; a < end; ++a) {
+                const unsigned x = ob[KI(a)];
+                int c = a - 1;
+                while (c >= i && ob[KI(c)] > x) { ob[KI(c + 1)] = ob[KI(c)]; --c; }
+                ob[KI(c + 1)] = x;
+            }
+        }
+    }
+    __syncthreads();
 }
 
 // Evaluate the candidates owned by this thread on one tile of sorted
 // magnitudes (src/denoise.py:62-118):  candidate t = m_i at the end of each
 // tie run, plus the stationary point of the quadratic piece that starts there.
-template <typename R>
+template <typename R, int NT>
 __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, int n, double tau,
                                           double pre_tile, double suf_tile, double next_tile_first,
                                           double* sh, Best& best, double* totinv) {
     const int tid = threadIdx.x;
-    const int E = T >= SNT ? T / SNT : 1;
+    const int E = T >= NT ? T / NT : 1;
     const bool act = tid * E < T;
     const int b0 = tid * E;
     double ssq = 0.0, sinv = 0.0;
     if (act) {
         for (int e = 0; e < E; ++e) { const double m = (double)keys[KI(b0 + e)]; ssq += m * m; }
-        for (int e = E - 1; e >= 0; --e) { const double m = (double)keys[KI(b0 + e)]; if (m > 0) sinv += 1.0 / m; }
+        for (int e = E - 1; e >= 0; --e) { const double m = (double)keys[KI(b0 + e)]; if (m > 0) sinv += __drcp_rn(m); }
     }
-    const double pre = block_excl_scan<SNT, false>(ssq, sh) + pre_tile;
-    const double suf = block_excl_scan<SNT, true>(sinv, sh) + suf_tile;
+    const double pre = block_excl_scan<NT, false>(ssq, sh) + pre_tile;
+    const double suf = block_excl_scan<NT, true>(sinv, sh) + suf_tile;
     if (tid == 0 && tilebase == 0) *totinv = suf + sinv;     // sum of all inverses
     if (!act) return;
     const double nt = (double)n * tau;
-    double inv_above = suf, sq_after = 0.0;
-    for (int e = E - 1; e >= 0; --e) {
-        const int il = b0 + e;
-        const double m = (double)keys[KI(il)];
-        const double nxt = (il + 1 < T) ? (double)keys[KI(il + 1)] : next_tile_first;
-        if (m != nxt) {
-            const double zeroed = pre + (ssq - sq_after);       // sum_{j <= i} m_j^2
-            const double cnt = (double)(n - (tilebase + il + 1));
-            const double risk = zeroed + m * m * cnt - nt + tau * (2.0 * cnt - m * inv_above);
-            consider(best, risk, m, cnt, inv_above);
-            if (cnt > 0) {
-                const double ts = tau * inv_above / (2.0 * cnt);
-                if (ts > m && ts < nxt) {
-                    const double rs = zeroed + ts * ts * cnt - nt + tau * (2.0 * cnt - ts * inv_above);
-                    consider(best, rs, ts, cnt, inv_above);
+    // exact suffix of inverses per owned key (accumulated from the large keys
+    // down, no subtraction), then a forward walk for the prefix of squares:
+    // both sums are built in the direction that never cancels
+    constexpr int EMAX = 16;
+    double sufv[EMAX];
+    {
+        double acc = suf;
+#pragma unroll
+        for (int e = EMAX - 1; e >= 0; --e) {
+            if (e < E) {
+                sufv[e] = acc;
+                const double m = (double)keys[KI(b0 + e)];
+                if (m > 0) acc += __drcp_rn(m);
+            }
+        }
+    }
+    double zacc = pre;
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) {
+        if (e < E) {
+            const int il = b0 + e;
+            const double m = (double)keys[KI(il)];
+            zacc += m * m;                                     // sum_{j <= i} m_j^2
+            const double nxt = (il + 1 < T) ? (double)keys[KI(il + 1)] : next_tile_first;
+            if (m != nxt) {
+                const double zeroed = zacc;
+                const double inv_above = sufv[e];
+                const double cnt = (double)(n - (tilebase + il + 1));
+                const double risk = zeroed + m * m * cnt - nt + tau * (2.0 * cnt - m * inv_above);
+                consider(best, risk, m, cnt, inv_above);
+                if (cnt > 0) {
+                    // stationary point ts = tau*inv/(2 cnt) inside (m, nxt)?  Pre-test by
+                    // multiplication with a relative guard, divide only for survivors.
+                    const double ti = tau * inv_above, c2 = 2.0 * cnt;
+                    if (ti > c2 * m * (1.0 - 1e-12) && ti < c2 * nxt * (1.0 + 1e-12)) {
+                        const double ts = ti / c2;
+                        if (ts > m && ts < nxt) {
+                            const double rs = zeroed + ts * ts * cnt - nt + tau * (2.0 * cnt - ts * inv_above);
+                            consider(best, rs, ts, cnt, inv_above);
+                        }
+                    }
                 }
             }
         }
-        if (m > 0) inv_above += 1.0 / m;
-        sq_after += m * m;
     }
 }
 
+#ifdef VDAMP_PHASE_TIMING
+// [image][subband][phase]: clock64 deltas of thread 0 (debug builds only)
+__device__ long long g_phase[4096][64][4];
+#define PHASE_MARK(i) do { if (threadIdx.x == 0 && bi < 4096) { long long c_ = clock64(); g_phase[bi][j][i] = c_ - ph0_; ph0_ = c_; } } while (0)
+#else
+#define PHASE_MARK(i) do { } while (0)
+#endif
+
+template <int NT>
 struct SelShared {
-    double sh[SNT / 32 + 2];
+    double sh[66 + NT / 32 + 2];     // counting-sort min/max words + block scans
     double tsq[MAXTILES], tinv[MAXTILES], tpre[MAXTILES], tsuf[MAXTILES];
     double tau, totinv;
-    Best best[SNT / 32];
+    Best best[NT / 32];
 };
 
 // Exact SURE selection for subband j of image bi (src/denoise.py:62-118,
 // 165-173; clamp src/vdamp.py:121-124).
-template <typename R>
-__device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R* keys, SelShared& S_) {
+template <typename R, int NT>
+__device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R* keys, SelShared<NT>& S_) {
     typedef typename CT<R>::T C;
     double* sh = S_.sh;
     double* tsq = S_.tsq; double* tinv = S_.tinv; double* tpre = S_.tpre; double* tsuf = S_.tsuf;
@@ -629,6 +772,9 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
     const int tid = threadIdx.x;
     const int n = g.len[j];
     const long long base = (long long)bi * g.N + g.off[j];
+#ifdef VDAMP_PHASE_TIMING
+    long long ph0_ = clock64();
+#endif
     if (tid == 0) {
         double t = 0.0;
         if (a.tau_in) t = a.tau_in[(long long)bi * g.S + j];
@@ -643,10 +789,15 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
     const int T = large ? CAPK : n;
     const int ntl = large ? n / CAPK : 1;
     const R* sorted = keys;
+    // fp32: counting sort from the staging buffer `stage` into `keys`
+    R* stage = keys + KI(CAPK) + 2;
+    unsigned* ccnt = reinterpret_cast<unsigned*>(stage + KI(CAPK) + 2);
+    const bool csort = NT == SNT && sizeof(R) == 4 && T >= 4096;
     for (int c0 = 0; c0 < n; c0 += T) {
-        for (int e = tid; e < T; e += SNT) {
+        R* dstk = csort ? stage : keys;
+        for (int e = tid; e < T; e += NT) {
             const C v = rs[c0 + e];
-            keys[KI(e)] = cmag(v);
+            dstk[KI(e)] = cmag(v);
             if (w0) {
                 const C w = w0[c0 + e];
                 const double dx = (double)v.x - (double)w.x, dy = (double)v.y - (double)w.y;
@@ -655,9 +806,14 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             }
         }
         __syncthreads();
-        block_sort(keys, T);
+        if constexpr (NT == SNT) {
+            if (csort) counting_sort(reinterpret_cast<const float*>(stage), reinterpret_cast<float*>(keys), ccnt, T, sh);
+            else block_sort<R, NT>(keys, T);
+        } else {
+            block_sort<R, NT>(keys, T);
+        }
         if (large) {
-            for (int e = tid; e < T; e += SNT) a.kA[base + c0 + e] = keys[KI(e)];
+            for (int e = tid; e < T; e += NT) a.kA[base + c0 + e] = keys[KI(e)];
             __syncthreads();
         }
     }
@@ -665,7 +821,7 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
         // merge sorted runs pairwise in global memory (merge path per thread)
         R* srcb = a.kA + base;
         R* dstb = a.kB + base;
-        const int per = n / SNT;
+        const int per = n / NT;
         for (int w = CAPK; w < n; w <<= 1) {
             const int o0 = tid * per;
             const int pb = o0 / (2 * w) * (2 * w);
@@ -690,21 +846,21 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
         // tile totals (ascending squares, descending inverses)
         for (int t = 0; t < ntl; ++t) {
             double q = 0.0, v = 0.0;
-            for (int e = tid; e < CAPK; e += SNT) {
+            for (int e = tid; e < CAPK; e += NT) {
                 const double m = (double)sorted[t * CAPK + e];
                 q += m * m;
             }
-            q = block_sum<SNT>(q, sh);
-            for (int e = tid; e < CAPK; e += SNT) {
+            q = block_sum<NT>(q, sh);
+            for (int e = tid; e < CAPK; e += NT) {
                 const double m = (double)sorted[t * CAPK + e];
                 if (m > 0) v += 1.0 / m;
             }
-            v = block_sum<SNT>(v, sh);
+            v = block_sum<NT>(v, sh);
             if (tid == 0) { tsq[t] = q; tinv[t] = v; }
         }
         __syncthreads();
     }
-    if (w0) { err = block_sum<SNT>(err, sh); ref = block_sum<SNT>(ref, sh); }
+    if (w0) { err = block_sum<NT>(err, sh); ref = block_sum<NT>(ref, sh); }
     if (tid == 0) {
         double acc = 0.0;
         for (int t = 0; t < ntl; ++t) { tpre[t] = acc; acc += large ? tsq[t] : 0.0; }
@@ -712,17 +868,18 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
         for (int t = ntl - 1; t >= 0; --t) { tsuf[t] = acc; acc += large ? tinv[t] : 0.0; }
     }
     __syncthreads();
+    PHASE_MARK(0);                                   // load + sort (+ merges)
     const double tau = fmax(s_tau, TAU_FLOOR);
 
     Best best{INFINITY, INFINITY, 0.0, 0.0};
     for (int t = 0; t < ntl; ++t) {
         if (large) {
             __syncthreads();
-            for (int e = tid; e < CAPK; e += SNT) keys[KI(e)] = sorted[t * CAPK + e];
+            for (int e = tid; e < CAPK; e += NT) keys[KI(e)] = sorted[t * CAPK + e];
             __syncthreads();
         }
         const double nf = (t + 1 < ntl) ? (double)sorted[(t + 1) * CAPK] : INFINITY;
-        scan_tile<R>(keys, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, best, &s_totinv);
+        scan_tile<R, NT>(keys, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, best, &s_totinv);
     }
     // candidate t = 0 when no magnitude is zero (src/denoise.py:84)
     __syncthreads();
@@ -740,6 +897,7 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             }
         }
     }
+    PHASE_MARK(1);                                   // scans + candidates
     // block argmin, ties -> smaller t
     for (int o = 16; o > 0; o >>= 1) {
         Best c;
@@ -753,7 +911,7 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
     __syncthreads();
     if (tid == 0) {
         Best bb = s_best[0];
-        for (int w = 1; w < SNT / 32; ++w) if (better(s_best[w], bb)) bb = s_best[w];
+        for (int w = 1; w < NT / 32; ++w) if (better(s_best[w], bb)) bb = s_best[w];
         const double alpha = (bb.cnt - 0.5 * bb.t * bb.inv) / (double)n;   // src/denoise.py:169
         const bool clamped = alpha >= ALPHA_CLAMP;                         // src/vdamp.py:121-124
         const double ac = clamped ? ALPHA_CLAMP : alpha;
@@ -766,17 +924,18 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             tr[5] = clamped ? 1.0 : 0.0; tr[6] = err; tr[7] = ref;
         }
     }
+    PHASE_MARK(2);                                   // argmin + outputs
 }
 
-template <typename R>
-__global__ void __launch_bounds__(SNT, 1) sure_select(Geo g, SelArgs<R> a) {
+template <typename R, int NT>
+__global__ void __launch_bounds__(NT, NT == SNT ? 1 : 4) sure_select(Geo g, SelArgs<R> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     R* keys = reinterpret_cast<R*>(smem_raw);
-    __shared__ SelShared S_;
+    __shared__ SelShared<NT> S_;
     const int it = blockIdx.x, bi = blockIdx.y;
     // one work item = one large subband, or several small ones packed to ~SCAP keys
     for (int q = a.item_start[it]; q < a.item_start[it + 1]; ++q) {
-        select_band<R>(g, a, a.item_list[q], bi, keys, S_);
+        select_band<R, NT>(g, a, a.item_list[q], bi, keys, S_);
         __syncthreads();
     }
 }

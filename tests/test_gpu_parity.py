@@ -102,6 +102,30 @@ def test_sure_select_vs_oracle(oracle, shape, kind):
     assert relmax(wh.values, wh_o) <= 1e-12
 
 
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("shape", [(64, 64, 4), (256, 256, 4)])
+def test_sure_select_tiny_tau_mixed_scales(oracle, precision, shape):
+    """Noiseless full-sampling edge (tau floored to 1e-300, round-off-sized keys mixed
+    with signal keys): prefix sums must not cancel, t = 0 must win as in the reference
+    (tests/test_vdamp.py:163-173 of the reference exercises this regime)."""
+    from paper_1911_01234_b200 import denoise, wavelet
+    h, w, s = shape
+    rng = np.random.default_rng(7)
+    lay = wavelet.SubbandLayout.create(h, w, s)
+    r = (rng.normal(size=h * w) + 1j * rng.normal(size=h * w)) * 1e-17
+    big = rng.random(h * w) < 0.08
+    r[big] = rng.normal(size=big.sum()) * 3.0
+    if precision == "fp32":
+        r = r.astype(np.complex64).astype(np.complex128)
+    tau = np.full(lay.n_subbands, 1e-300)
+    _, al, lam = denoise.denoise_colored(wavelet.WaveletCoeffs(r, lay), denoise.SubbandVector(tau),
+                                         precision=precision)
+    wh_o, al_o, lam_o, t_o = oracle.denoise_colored(r, tau, oracle.band_table(h, w, s))
+    assert np.all(t_o == 0.0)
+    assert np.array_equal(lam.values * tau, t_o)
+    assert np.allclose(al.values, al_o, rtol=1e-12)
+
+
 RUNS = ["shepp32", "shepp64", "rect64x32", "shepp128", "full64"]
 
 
