@@ -709,6 +709,9 @@ int vdamp_kernel_times(vdamp_plan_t plan, double* ms, int64_t* launches) {
 extern "C" VDAMP_API int vdamp_debug_phase_times(long long* out, int images) {
     return guard([&] { CK(cudaMemcpyFromSymbol(out, g_phase, (size_t)images * 64 * 4 * sizeof(long long))); });
 }
+extern "C" VDAMP_API int vdamp_debug_csort_times(long long* out, int images) {
+    return guard([&] { CK(cudaMemcpyFromSymbol(out, g_csort, (size_t)images * 64 * 6 * sizeof(long long))); });
+}
 #endif
 
 int vdamp_launch_count(vdamp_plan_t plan, int64_t* count, int reset) {

@@ -42,6 +42,39 @@ struct Geo {
 
 __host__ __device__ inline int band_of(int s, int level, int orient) { return 1 + 3 * (s - level) + orient; }
 
+// A strip of 2^k rows (levels a..a+k-1 plus the level-b approximation row)
+// owns E_s = Wa*2^k coefficients.  Flat order used by the batched gathers:
+// [level 1: H V D][level 2: H V D] ... [level k: H V D][approx row]; level q
+// chunks hold E_s >> 2q coefficients.  Returns the coefficient's offset within
+// its subband chunk source and its mosaic slot (row * Wa + col) in smem.
+struct StripSlot { int j; long long gofs; int smem; bool approx; };
+
+__device__ __forceinline__ StripSlot strip_slot(const Geo& g, int a, int k, int Wa, int logWa, int st, int f) {
+    const int E = Wa << k;
+    const int logE = logWa + k;
+    int base = 0;
+    for (int q = 1; q <= k; ++q) {
+        const int lcq = logE - 2 * q, cq = 1 << lcq;
+        if (f < base + 3 * cq) {
+            const int o = (f - base) >> lcq, e = (f - base) & (cq - 1);
+            const int logCq = logWa - q, Rq = 1 << (k - q), Cq = 1 << logCq;
+            const int l = a + q - 1;
+            const int j = band_of(g.s, l, o);
+            const int r0 = (o >= 1) ? Rq : 0, c0 = (o != 1) ? Cq : 0;
+            StripSlot s_;
+            s_.j = j; s_.gofs = g.off[j] + (long long)st * cq + e;
+            s_.smem = (r0 + (e >> logCq)) * Wa + c0 + (e & (Cq - 1));
+            s_.approx = false;
+            return s_;
+        }
+        base += 3 * cq;
+    }
+    const int e = f - base;                         // approximation row
+    StripSlot s_;
+    s_.j = 0; s_.gofs = g.off[0] + (long long)st * (Wa >> k) + e; s_.smem = e; s_.approx = true;
+    return s_;
+}
+
 // ------------------------------------------------------------------ K1 ----
 enum { SYN_PLAIN = 0, SYN_ROWFFT = 1 };
 
@@ -69,37 +102,35 @@ __global__ void __launch_bounds__(PNT) synth_pass(Geo g, SynArgs<R> p) {
     if (MODE == SYN_ROWFFT)
         for (int e = tid; e < g.W; e += PNT) tws[e] = p.tw[e];
 
-    // gather the strip's coefficients into the mosaic (Onsager applied)
-    for (int q = 1; q <= k; ++q) {
-        const int l = p.a + q - 1;
-        const int logCq = p.logWa - q, Cq = 1 << logCq, Rq = 1 << (k - q);
-        const int cnt = Rq * Cq;
-        for (int o = 0; o < 3; ++o) {
-            const int j = band_of(g.s, l, o);
-            R t = 0, al = 0, ga = 1;
-            if (par) { t = (R)par[3 * j]; al = (R)par[3 * j + 1]; ga = (R)par[3 * j + 2]; }
-            const C* src = coef + g.off[j] + (long long)st * cnt;
-            const int r0 = (o >= 1) ? Rq : 0, c0 = (o != 1) ? Cq : 0;
-            for (int e = tid; e < cnt; e += PNT) {
-                C v = src[e];
-                if (par) v = onsager<R, C>(v, t, al, ga);
-                buf[(r0 + (e >> logCq)) * Wa + c0 + (e & (Cq - 1))] = v;
+    // gather the strip's coefficients into the mosaic (Onsager applied); all
+    // loads of a thread are issued before any is used
+    __shared__ R spar[MAXS * 3];
+    for (int i = tid; i < g.S * 3; i += PNT) spar[i] = par ? (R)par[i] : ((i % 3) == 2 ? R(1) : R(0));
+    __syncthreads();
+    {
+        constexpr int PER = PCAP / PNT;
+        const int E = Wa << k;
+        C v[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int f = tid + i * PNT;
+            if (f < E) {
+                const StripSlot sl = strip_slot(g, p.a, k, Wa, p.logWa, st, f);
+                if (sl.approx && p.asrc) v[i] = p.asrc[(long long)bi * p.asrc_bs + (long long)st * (Wa >> k) + sl.smem];
+                else v[i] = coef[sl.gofs];
             }
         }
-    }
-    {
-        const int Ck = Wa >> k;
-        if (p.asrc) {
-            const C* src = p.asrc + (long long)bi * p.asrc_bs + (long long)st * Ck;
-            for (int e = tid; e < Ck; e += PNT) buf[e] = src[e];
-        } else {
-            R t = 0, al = 0, ga = 1;
-            if (par) { t = (R)par[0]; al = (R)par[1]; ga = (R)par[2]; }
-            const C* src = coef + g.off[0] + (long long)st * Ck;
-            for (int e = tid; e < Ck; e += PNT) {
-                C v = src[e];
-                if (par) v = onsager<R, C>(v, t, al, ga);
-                buf[e] = v;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int f = tid + i * PNT;
+            if (f < E) {
+                const StripSlot sl = strip_slot(g, p.a, k, Wa, p.logWa, st, f);
+                C x = v[i];
+                if (par && !(sl.approx && p.asrc)) {
+                    const int j = sl.j;
+                    x = onsager<R, C>(x, spar[3 * j], spar[3 * j + 1], spar[3 * j + 2]);
+                }
+                buf[sl.smem] = x;
             }
         }
     }
@@ -237,38 +268,44 @@ __global__ void __launch_bounds__(PNT) analysis_pass(Geo g, AnaArgs<R> p) {
         __syncthreads();
     }
 
-    // scatter the mosaic back to the flat layout
+    // scatter the mosaic back to the flat layout (VDAMP: r_new = Onsager(r_old) + u);
+    // all r_old loads of a thread are issued before any is used
     C* coef = p.coef + (long long)bi * g.N;
-    const double* par = (OUT == ANA_OUT_VDAMP) ? p.par + (long long)bi * g.S * 3 : nullptr;
-    for (int q = 1; q <= k; ++q) {
-        const int l = p.a + q - 1;
-        const int logCq = p.logWa - q, Cq = 1 << logCq, Rq = 1 << (k - q);
-        const int cnt = Rq * Cq;
-        for (int o = 0; o < 3; ++o) {
-            const int j = band_of(g.s, l, o);
-            C* d = coef + g.off[j] + (long long)st * cnt;
-            const int r0 = (o >= 1) ? Rq : 0, c0 = (o != 1) ? Cq : 0;
-            R t = 0, al = 0, ga = 1;
-            if (OUT == ANA_OUT_VDAMP) { t = (R)par[3 * j]; al = (R)par[3 * j + 1]; ga = (R)par[3 * j + 2]; }
-            for (int e = tid; e < cnt; e += PNT) {
-                C u = buf[(r0 + (e >> logCq)) * Wa + c0 + (e & (Cq - 1))];
-                if (OUT == ANA_OUT_VDAMP) u = cadd(onsager<R, C>(d[e], t, al, ga), u);
-                d[e] = u;
+    __shared__ R spar[MAXS * 3];
+    if (OUT == ANA_OUT_VDAMP) {
+        const double* par = p.par + (long long)bi * g.S * 3;
+        for (int i = tid; i < g.S * 3; i += PNT) spar[i] = (R)par[i];
+        __syncthreads();
+    }
+    {
+        constexpr int PER = PCAP / PNT;
+        C old[PER];
+        if (OUT == ANA_OUT_VDAMP) {
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int f = tid + i * PNT;
+                if (f < E) {
+                    const StripSlot sl = strip_slot(g, p.a, k, Wa, p.logWa, st, f);
+                    if (!(sl.approx && p.adst)) old[i] = coef[sl.gofs];
+                }
             }
         }
-    }
-    const int Ck = Wa >> k;
-    if (p.adst) {
-        C* d = p.adst + (long long)bi * p.adst_bs + (long long)st * Ck;
-        for (int e = tid; e < Ck; e += PNT) d[e] = buf[e];
-    } else {
-        C* d = coef + g.off[0] + (long long)st * Ck;
-        R t = 0, al = 0, ga = 1;
-        if (OUT == ANA_OUT_VDAMP) { t = (R)par[0]; al = (R)par[1]; ga = (R)par[2]; }
-        for (int e = tid; e < Ck; e += PNT) {
-            C u = buf[e];
-            if (OUT == ANA_OUT_VDAMP) u = cadd(onsager<R, C>(d[e], t, al, ga), u);
-            d[e] = u;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int f = tid + i * PNT;
+            if (f < E) {
+                const StripSlot sl = strip_slot(g, p.a, k, Wa, p.logWa, st, f);
+                C u = buf[sl.smem];
+                if (sl.approx && p.adst) {
+                    p.adst[(long long)bi * p.adst_bs + (long long)st * (Wa >> k) + sl.smem] = u;
+                } else {
+                    if (OUT == ANA_OUT_VDAMP) {
+                        const int j = sl.j;
+                        u = cadd(onsager<R, C>(old[i], spar[3 * j], spar[3 * j + 1], spar[3 * j + 2]), u);
+                    }
+                    coef[sl.gofs] = u;
+                }
+            }
         }
     }
 }
@@ -332,19 +369,28 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass(Geo g, C
     constexpr int PER = PCAP / PNT;               // elements per thread
     R wreg[PER];                                  // tau weights of this thread's elements
     const int np = 2 * g.s;
+    R pvs[PER];
+    C ys[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {               // issue all measurement loads first
+        const int e = tid + i * PNT;
+        if (e < E) {
+            const long long gi = ib + (long long)(e >> lc) * W + c0 + (e & (cw - 1));
+            pvs[i] = p.pinv[gi];
+            ys[i] = p.yg[gi];
+        }
+    }
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         const int e = tid + i * PNT;
         wreg[i] = R(0);
         if (e < E) {
-            const int n = e >> lc;
-            const long long gi = ib + (long long)n * W + c0 + (e & (cw - 1));
             const C X = cscale(buf[e], sc * cs);     // c * FFT2u, so (-1)^(k1+k2) X_centred
-            const R pv = p.pinv[gi];
+            const R pv = pvs[i];
             C v;
             if (MODE == COL_VDAMP) {
                 if (pv != R(0)) {
-                    const C zc = csub(p.yg[gi], X);          // (-1)^(k1+k2) z  (src/vdamp.py:112)
+                    const C zc = csub(ys[i], X);             // (-1)^(k1+k2) z  (src/vdamp.py:112)
                     v = cscale(zc, pv);                      // P^-1 z           (src/vdamp.py:113)
                     const double pd = (double)pv;
                     const double z2 = (double)zc.x * (double)zc.x + (double)zc.y * (double)zc.y;
@@ -353,7 +399,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass(Geo g, C
                     v = mk<C>(R(0), R(0));
                 }
             } else {  // COL_FINAL: measured k-space where sampled (src/vdamp.py:147-150)
-                v = (pv != R(0)) ? p.yg[gi] : X;
+                v = (pv != R(0)) ? ys[i] : X;
             }
             buf[e] = v;
         }
@@ -577,8 +623,18 @@ __device__ void block_sort(R* s, int n) {
 // ---------------------------------------------------------------------------
 constexpr int CS_BUCKETS = 32768;
 
-__device__ void counting_sort(const float* keys, float* out, unsigned* cnt, int n, double* sh) {
+#ifdef VDAMP_PHASE_TIMING
+__device__ long long g_csort[4096][64][6];
+#define CS_MARK(i) do { if (threadIdx.x == 0 && dbg) { long long c_ = clock64(); dbg[i] = c_ - cs0_; cs0_ = c_; } } while (0)
+#else
+#define CS_MARK(i) do { } while (0)
+#endif
+
+__device__ void counting_sort(const float* keys, float* out, unsigned* cnt, int n, double* sh, long long* dbg = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+#ifdef VDAMP_PHASE_TIMING
+    long long cs0_ = clock64();
+#endif
     const unsigned* kb = reinterpret_cast<const unsigned*>(keys);
     unsigned* ob = reinterpret_cast<unsigned*>(out);
     unsigned mn = 0xffffffffu, mx = 0;
@@ -606,6 +662,7 @@ __device__ void counting_sort(const float* keys, float* out, unsigned* cnt, int 
     }
     __syncthreads();
     mn = red[64]; mx = red[65];
+    CS_MARK(0);
     if (mn > mx) mn = mx;                            // all zeros
     int lo = 0;
     while (((mx >> lo) - (mn >> lo)) >= (unsigned)(CS_BUCKETS - 2)) ++lo;
@@ -617,6 +674,7 @@ __device__ void counting_sort(const float* keys, float* out, unsigned* cnt, int 
         atomicAdd(&cnt[b >> 1], 1u << ((b & 1u) * 16));
     }
     __syncthreads();
+    CS_MARK(1);
     // exclusive scan of the CS_BUCKETS 16-bit counts (thread t: buckets [32t, 32t+32))
     {
         constexpr int PER = CS_BUCKETS / 2 / SNT;    // packed words per thread
@@ -637,6 +695,7 @@ __device__ void counting_sort(const float* keys, float* out, unsigned* cnt, int 
         }
     }
     __syncthreads();
+    CS_MARK(2);
     // scatter (cursor = packed 16-bit half, never carries: offsets + counts <= n <= 16384)
     for (int i = tid; i < n; i += SNT) {
         const unsigned k = kb[KI(i)];
@@ -646,33 +705,30 @@ __device__ void counting_sort(const float* keys, float* out, unsigned* cnt, int 
         ob[KI((old >> sft) & 0xffffu)] = k;
     }
     __syncthreads();
-    // finish every bucket: insertion sort by the full key (owner = thread of the run start)
-    const int E = n >= SNT ? n / SNT : 1;
-    const int b0 = tid * E;
-    if (b0 < n) {
-        for (int e = 0; e < E; ++e) {
-            const int i = b0 + e;
-            const unsigned k0 = ob[KI(i)];
-            const unsigned bk = k0 ? (k0 >> lo) - base + 1u : 0u;
-            if (i > 0) {
-                const unsigned kp = ob[KI(i - 1)];
-                if ((kp ? (kp >> lo) - base + 1u : 0u) == bk) continue;   // not a run start
-            }
-            int end = i + 1;
-            while (end < n) {
-                const unsigned kn = ob[KI(end)];
-                if ((kn ? (kn >> lo) - base + 1u : 0u) != bk) break;
-                ++end;
-            }
-            for (int a = i + 1; a < end; ++a) {
-                const unsigned x = ob[KI(a)];
-                int c = a - 1;
-                while (c >= i && ob[KI(c)] > x) { ob[KI(c + 1)] = ob[KI(c)]; --c; }
-                ob[KI(c + 1)] = x;
-            }
+    CS_MARK(3);
+    // finish every bucket in parallel: the final slot of key x at grouped position
+    // i is start(b) + #{y in b : y < x} + #{y in b : y == x, pos(y) < i}.  Threads
+    // of a warp mostly share a bucket, so the smem reads broadcast.  The grouped
+    // keys live in `ob`; the ranked result is written back into the staging
+    // buffer (free by now) and copied to `out`.
+    unsigned* fb = const_cast<unsigned*>(kb);
+    for (int i = tid; i < n; i += SNT) {
+        const unsigned x = ob[KI(i)];
+        const unsigned bk = x ? (x >> lo) - base + 1u : 0u;
+        const unsigned e1 = cnt[bk >> 1] >> ((bk & 1u) * 16) & 0xffffu;          // end of bucket bk
+        unsigned s0 = 0;
+        if (bk > 0) { const unsigned bp = bk - 1u; s0 = cnt[bp >> 1] >> ((bp & 1u) * 16) & 0xffffu; }
+        unsigned rank = 0;
+        for (unsigned q = s0; q < e1; ++q) {
+            const unsigned y = ob[KI(q)];
+            rank += (y < x) || (y == x && (int)q < i);
         }
+        fb[KI(s0 + rank)] = x;
     }
     __syncthreads();
+    for (int i = tid; i < n; i += SNT) ob[KI(i)] = fb[KI(i)];
+    __syncthreads();
+    CS_MARK(4);
 }
 
 // Evaluate the candidates owned by this thread on one tile of sorted
@@ -795,19 +851,41 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
     const bool csort = NT == SNT && sizeof(R) == 4 && T >= 4096;
     for (int c0 = 0; c0 < n; c0 += T) {
         R* dstk = csort ? stage : keys;
-        for (int e = tid; e < T; e += NT) {
-            const C v = rs[c0 + e];
-            dstk[KI(e)] = cmag(v);
+        // issue 8 independent loads per thread before using any (memory-level parallelism)
+        constexpr int LB = 8;
+        for (int e0 = tid; e0 < T; e0 += LB * NT) {
+            C v[LB];
+#pragma unroll
+            for (int u = 0; u < LB; ++u) {
+                const int e = e0 + u * NT;
+                if (e < T) v[u] = rs[c0 + e];
+            }
+#pragma unroll
+            for (int u = 0; u < LB; ++u) {
+                const int e = e0 + u * NT;
+                if (e < T) dstk[KI(e)] = cmag(v[u]);
+            }
             if (w0) {
-                const C w = w0[c0 + e];
-                const double dx = (double)v.x - (double)w.x, dy = (double)v.y - (double)w.y;
-                err += dx * dx + dy * dy;
-                ref += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
+#pragma unroll
+                for (int u = 0; u < LB; ++u) {
+                    const int e = e0 + u * NT;
+                    if (e < T) {
+                        const C w = w0[c0 + e];
+                        const double dx = (double)v[u].x - (double)w.x, dy = (double)v[u].y - (double)w.y;
+                        err += dx * dx + dy * dy;
+                        ref += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
+                    }
+                }
             }
         }
         __syncthreads();
         if constexpr (NT == SNT) {
-            if (csort) counting_sort(reinterpret_cast<const float*>(stage), reinterpret_cast<float*>(keys), ccnt, T, sh);
+#ifdef VDAMP_PHASE_TIMING
+            long long* dbg = (bi < 4096) ? &g_csort[bi][j][0] : nullptr;
+#else
+            long long* dbg = nullptr;
+#endif
+            if (csort) counting_sort(reinterpret_cast<const float*>(stage), reinterpret_cast<float*>(keys), ccnt, T, sh, dbg);
             else block_sort<R, NT>(keys, T);
         } else {
             block_sort<R, NT>(keys, T);
