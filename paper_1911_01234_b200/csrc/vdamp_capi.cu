@@ -92,6 +92,9 @@ void* dalloc(Plan* p, size_t n) {
     return ptr;
 }
 
+// padded smem element count of a row buffer of n elements (SP layout)
+size_t SPN(long long n) { return (size_t)(n + (n >> 4) + 1); }
+
 int ilog2(long long v) { int l = 0; while ((1LL << l) < v) ++l; return l; }
 bool pow2(long long v) { return v > 0 && (v & (v - 1)) == 0; }
 
@@ -150,7 +153,7 @@ struct Seq {
             a.dst = last ? (rowfft ? (C*)p->T1 : img) : (C*)p->scratch[i];
             a.dst_bs = (long long)ps.Ha * ps.Wa;
             dim3 grid(ps.nstrips, p->B);
-            const size_t sm = (size_t)(ps.Wa << ps.k) * sizeof(C);
+            const size_t sm = (size_t)SPN(ps.Wa << ps.k) * sizeof(C);
             Launch L(p, cls, st);
             if (last && rowfft) {
                 auto k = synth_pass<R, SYN_ROWFFT>;
@@ -181,7 +184,7 @@ struct Seq {
             a.a = ps.a; a.b = ps.b; a.k = ps.k; a.Wa = ps.Wa; a.logWa = ps.logWa;
             a.tw = (const C*)p->twW;
             dim3 grid(ps.nstrips, p->B);
-            size_t sm = (size_t)(ps.Wa << ps.k) * sizeof(C);
+            size_t sm = (size_t)SPN(ps.Wa << ps.k) * sizeof(C);
             Launch L(p, cls, st);
             if (first && rowifft) {
                 sm += (size_t)p->W * sizeof(C);
@@ -231,7 +234,7 @@ struct Seq {
     template <bool INV, bool PRE, bool POST>
     void rows(const C* src, C* dst, int cls) {
         dim3 grid(p->H >> p->rowlog, p->B);
-        const size_t sm = ((size_t)p->W << p->rowlog) * sizeof(C) + (size_t)p->W * sizeof(C);
+        const size_t sm = (size_t)SPN(p->W << p->rowlog) * sizeof(C) + (size_t)p->W * sizeof(C);
         auto k = row_pass<R, INV, PRE, POST>;
         set_smem(k, sm);
         Launch L(p, cls, st);

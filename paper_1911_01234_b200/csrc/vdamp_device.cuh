@@ -175,6 +175,189 @@ __device__ __forceinline__ void block_fft(C* buf, int logL, int lognseq, int sst
 }
 
 // ---------------------------------------------------------------------------
+// Radix-16/8/4/2 Stockham FFT.  Each thread owns whole radix-R butterflies in
+// registers (R = 16 while >= 16 points remain, then 8/4/2).  Row sequences are
+// addressed through the padded index SP(i) = i + (i >> 4) so the stride-R
+// Stockham stores of the first pass hit distinct banks; column tiles
+// (SEQ_FAST) are conflict-free unpadded.  tw[m] = exp(-2 pi i m / L).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int SP(int i) { return i + (i >> 4); }
+
+template <typename C> struct Cst;
+template <> struct Cst<float2> {
+    static constexpr float c1 = 0.92387953251128676f, s1 = 0.38268343236508977f, h = 0.70710678118654752f;
+};
+template <> struct Cst<double2> {
+    static constexpr double c1 = 0.92387953251128676, s1 = 0.38268343236508977, h = 0.70710678118654752;
+};
+
+// w^m for w = exp(-+2 pi i / 16), m in 0..15 (conj for the inverse)
+template <typename C, bool INV>
+__device__ __forceinline__ C w16(int m) {
+    typedef decltype(C::x) R;
+    const R c1 = Cst<C>::c1, s1 = Cst<C>::s1, h = Cst<C>::h;
+    R re, im;
+    switch (m & 15) {
+        case 0: re = 1; im = 0; break;
+        case 1: re = c1; im = -s1; break;
+        case 2: re = h; im = -h; break;
+        case 3: re = s1; im = -c1; break;
+        case 4: re = 0; im = -1; break;
+        case 5: re = -s1; im = -c1; break;
+        case 6: re = -h; im = -h; break;
+        case 7: re = -c1; im = -s1; break;
+        case 8: re = -1; im = 0; break;
+        case 9: re = -c1; im = s1; break;
+        case 10: re = -h; im = h; break;
+        case 11: re = -s1; im = c1; break;
+        case 12: re = 0; im = 1; break;
+        case 13: re = s1; im = c1; break;
+        case 14: re = h; im = h; break;
+        default: re = c1; im = s1; break;
+    }
+    return mk<C>(re, INV ? -im : im);
+}
+
+template <typename C, bool INV>
+__device__ __forceinline__ void dft4(C& a0, C& a1, C& a2, C& a3) {
+    const C b0 = cadd(a0, a2), b1 = csub(a0, a2), b2 = cadd(a1, a3), b3 = cmul_mi<C, INV>(csub(a1, a3));
+    a0 = cadd(b0, b2); a1 = cadd(b1, b3); a2 = csub(b0, b2); a3 = csub(b1, b3);
+}
+
+// in-place DFT of v[0..R) in natural order
+template <typename C, bool INV, int R>
+__device__ __forceinline__ void dft_r(C (&v)[R]) {
+    if constexpr (R == 2) {
+        const C a = v[0], b = v[1];
+        v[0] = cadd(a, b); v[1] = csub(a, b);
+    } else if constexpr (R == 4) {
+        dft4<C, INV>(v[0], v[1], v[2], v[3]);
+    } else if constexpr (R == 8) {
+        // n = n2 + 4 n1 (n1 < 2): DFT2 over n1, twiddle W8^{n2 k1}, DFT4 over n2 -> X[k1 + 2 k2]
+        C a[4][2];
+#pragma unroll
+        for (int n2 = 0; n2 < 4; ++n2) { a[n2][0] = cadd(v[n2], v[n2 + 4]); a[n2][1] = csub(v[n2], v[n2 + 4]); }
+#pragma unroll
+        for (int n2 = 1; n2 < 4; ++n2) a[n2][1] = cmul(a[n2][1], w16<C, INV>(2 * n2));
+#pragma unroll
+        for (int k1 = 0; k1 < 2; ++k1) {
+            dft4<C, INV>(a[0][k1], a[1][k1], a[2][k1], a[3][k1]);
+#pragma unroll
+            for (int k2 = 0; k2 < 4; ++k2) v[k1 + 2 * k2] = a[k2][k1];
+        }
+    } else {
+        static_assert(R == 16, "radix");
+        // n = n2 + 4 n1: DFT4 over n1, twiddle W16^{n2 k1}, DFT4 over n2 -> X[k1 + 4 k2]
+        C a[4][4];
+#pragma unroll
+        for (int n2 = 0; n2 < 4; ++n2) {
+            a[n2][0] = v[n2]; a[n2][1] = v[n2 + 4]; a[n2][2] = v[n2 + 8]; a[n2][3] = v[n2 + 12];
+            dft4<C, INV>(a[n2][0], a[n2][1], a[n2][2], a[n2][3]);
+        }
+#pragma unroll
+        for (int n2 = 1; n2 < 4; ++n2)
+#pragma unroll
+            for (int k1 = 1; k1 < 4; ++k1) a[n2][k1] = cmul(a[n2][k1], w16<C, INV>(n2 * k1));
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) {
+            dft4<C, INV>(a[0][k1], a[1][k1], a[2][k1], a[3][k1]);
+#pragma unroll
+            for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = a[k2][k1];
+        }
+    }
+}
+
+// one Stockham pass of radix R; element e of sequence q at buf[ADR(q*sstr + e*estr)]
+template <typename C, bool INV, int NT, int MAXB, bool SEQ_FAST, bool PAD, int R>
+__device__ __forceinline__ void fft_pass(C* buf, int logL, int logNs, int lognseq, int sstr, int estr, const C* tw) {
+    constexpr int LR = R == 2 ? 1 : R == 4 ? 2 : R == 8 ? 3 : 4;
+    const int logQ = logL - LR;
+    const int Q = 1 << logQ;
+    const int Ns = 1 << logNs;
+    const int total = 1 << (lognseq + logQ);
+    const int twshift = logL - logNs - LR;
+    C v[MAXB][R];
+#pragma unroll
+    for (int i = 0; i < MAXB; ++i) {
+        const int bf = threadIdx.x + i * NT;
+        if (bf < total) {
+            int q, j;
+            if (SEQ_FAST) { q = bf & ((1 << lognseq) - 1); j = bf >> lognseq; }
+            else          { q = bf >> logQ; j = bf & (Q - 1); }
+            const int base = q * sstr;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int a = base + (j + r * Q) * estr;
+                v[i][r] = buf[PAD ? SP(a) : a];
+            }
+            const int k = j & (Ns - 1);
+            if (k) {
+                // twiddles w^(r k): load w^k, w^2k, w^4k, w^8k, build the rest by products
+                C t1 = tw[k << twshift];
+                C t2 = (R >= 4) ? tw[(2 * k) << twshift] : t1;
+                C t4 = (R >= 8) ? tw[(4 * k) << twshift] : t1;
+                C t8 = (R >= 16) ? tw[(8 * k) << twshift] : t1;
+                if (INV) { t1 = cconj(t1); t2 = cconj(t2); t4 = cconj(t4); t8 = cconj(t8); }
+#pragma unroll
+                for (int r = 1; r < R; ++r) {
+                    C w;
+                    switch (r) {
+                        case 1: w = t1; break;
+                        case 2: w = t2; break;
+                        case 3: w = cmul(t2, t1); break;
+                        case 4: w = t4; break;
+                        case 5: w = cmul(t4, t1); break;
+                        case 6: w = cmul(t4, t2); break;
+                        case 7: w = cmul(cmul(t4, t2), t1); break;
+                        case 8: w = t8; break;
+                        case 9: w = cmul(t8, t1); break;
+                        case 10: w = cmul(t8, t2); break;
+                        case 11: w = cmul(cmul(t8, t2), t1); break;
+                        case 12: w = cmul(t8, t4); break;
+                        case 13: w = cmul(cmul(t8, t4), t1); break;
+                        case 14: w = cmul(cmul(t8, t4), t2); break;
+                        default: w = cmul(cmul(cmul(t8, t4), t2), t1); break;
+                    }
+                    v[i][r] = cmul(v[i][r], w);
+                }
+            }
+            dft_r<C, INV, R>(v[i]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < MAXB; ++i) {
+        const int bf = threadIdx.x + i * NT;
+        if (bf < total) {
+            int q, j;
+            if (SEQ_FAST) { q = bf & ((1 << lognseq) - 1); j = bf >> lognseq; }
+            else          { q = bf >> logQ; j = bf & (Q - 1); }
+            const int base = q * sstr;
+            const int k = j & (Ns - 1);
+            const int d = ((j - k) << LR) + k;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int a = base + (d + r * Ns) * estr;
+                buf[PAD ? SP(a) : a] = v[i][r];
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// Full unnormalised DFT of every sequence (radix-16 passes, one final 2/4/8 pass).
+template <typename C, bool INV, int NT, int CAP, bool SEQ_FAST, bool PAD>
+__device__ __forceinline__ void block_fft16(C* buf, int logL, int lognseq, int sstr, int estr, const C* tw) {
+    int logNs = 0;
+    const int rem = logL & 3;
+    if (rem == 1) { fft_pass<C, INV, NT, (CAP / 2 + NT - 1) / NT, SEQ_FAST, PAD, 2>(buf, logL, 0, lognseq, sstr, estr, tw); logNs = 1; }
+    if (rem == 2) { fft_pass<C, INV, NT, (CAP / 4 + NT - 1) / NT, SEQ_FAST, PAD, 4>(buf, logL, 0, lognseq, sstr, estr, tw); logNs = 2; }
+    if (rem == 3) { fft_pass<C, INV, NT, (CAP / 8 + NT - 1) / NT, SEQ_FAST, PAD, 8>(buf, logL, 0, lognseq, sstr, estr, tw); logNs = 3; }
+    for (; logNs < logL; logNs += 4)
+        fft_pass<C, INV, NT, (CAP / 16 + NT - 1) / NT, SEQ_FAST, PAD, 16>(buf, logL, logNs, lognseq, sstr, estr, tw);
+}
+
+// ---------------------------------------------------------------------------
 // Deterministic block reductions / scans over doubles (fixed shuffle trees).
 // ---------------------------------------------------------------------------
 template <int NT>

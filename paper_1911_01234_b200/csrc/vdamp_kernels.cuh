@@ -90,7 +90,7 @@ struct SynArgs {
 };
 
 template <typename R, int MODE>
-__global__ void __launch_bounds__(PNT) synth_pass(Geo g, SynArgs<R> p) {
+__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) synth_pass(Geo g, SynArgs<R> p) {
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* buf = reinterpret_cast<C*>(smem_raw);
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(PNT) synth_pass(Geo g, SynArgs<R> p) {
     const int k = p.k, Wa = p.Wa;
     const C* coef = p.coef + (long long)bi * g.N;
     const double* par = p.par ? p.par + (long long)bi * g.S * 3 : nullptr;
-    C* tws = buf + (Wa << k);
+    C* tws = buf + SP((Wa << k) - 1) + 1;
     if (MODE == SYN_ROWFFT)
         for (int e = tid; e < g.W; e += PNT) tws[e] = p.tw[e];
 
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(PNT) synth_pass(Geo g, SynArgs<R> p) {
                     const int j = sl.j;
                     x = onsager<R, C>(x, spar[3 * j], spar[3 * j + 1], spar[3 * j + 2]);
                 }
-                buf[sl.smem] = x;
+                buf[SP(sl.smem)] = x;
             }
         }
     }
@@ -147,8 +147,8 @@ __global__ void __launch_bounds__(PNT) synth_pass(Geo g, SynArgs<R> p) {
             const int e = tid + i * PNT;
             if (e < P) {
                 const int ii = e >> logCq, jj = e & (Cq - 1);
-                C ll = buf[ii * Wa + jj], lh = buf[ii * Wa + Cq + jj];
-                C hl = buf[(Rq + ii) * Wa + jj], hh = buf[(Rq + ii) * Wa + Cq + jj];
+                C ll = buf[SP(ii * Wa + jj)], lh = buf[SP(ii * Wa + Cq + jj)];
+                C hl = buf[SP((Rq + ii) * Wa + jj)], hh = buf[SP((Rq + ii) * Wa + Cq + jj)];
                 C lo0 = Haar<R>::sum(ll, lh), lo1 = Haar<R>::dif(ll, lh);
                 C hi0 = Haar<R>::sum(hl, hh), hi1 = Haar<R>::dif(hl, hh);
                 o[i][0] = Haar<R>::sum(lo0, hi0);
@@ -163,8 +163,8 @@ __global__ void __launch_bounds__(PNT) synth_pass(Geo g, SynArgs<R> p) {
             const int e = tid + i * PNT;
             if (e < P) {
                 const int ii = e >> logCq, jj = e & (Cq - 1);
-                C* d = buf + (2 * ii) * Wa + 2 * jj;
-                d[0] = o[i][0]; d[1] = o[i][1]; d[Wa] = o[i][2]; d[Wa + 1] = o[i][3];
+                const int d = (2 * ii) * Wa + 2 * jj;
+                buf[SP(d)] = o[i][0]; buf[SP(d + 1)] = o[i][1]; buf[SP(d + Wa)] = o[i][2]; buf[SP(d + Wa + 1)] = o[i][3];
             }
         }
         __syncthreads();
@@ -173,19 +173,19 @@ __global__ void __launch_bounds__(PNT) synth_pass(Geo g, SynArgs<R> p) {
     const int E = Wa << k;
     C* dst = p.dst + (long long)bi * p.dst_bs + (long long)st * E;
     if (MODE == SYN_PLAIN) {
-        for (int e = tid; e < E; e += PNT) dst[e] = buf[e];
+        for (int e = tid; e < E; e += PNT) dst[e] = buf[SP(e)];
         return;
     }
     // (-1)^(n1+n2) then row FFT (unitary 1/sqrt(W))
     const int rowbase = st << k;
     for (int e = tid; e < E; e += PNT) {
         const int n1 = rowbase + (e >> p.logWa), n2 = e & (Wa - 1);
-        if ((n1 + n2) & 1) { C v = buf[e]; buf[e] = mk<C>(-v.x, -v.y); }
+        if ((n1 + n2) & 1) { C v = buf[SP(e)]; buf[SP(e)] = mk<C>(-v.x, -v.y); }
     }
     __syncthreads();
-    block_fft<C, false, PNT, PCAP, false>(buf, g.logW, k, Wa, 1, tws);
+    block_fft16<C, false, PNT, PCAP, false, true>(buf, g.logW, k, Wa, 1, tws);
     const R sc = R(1) / sqrt(R(g.W));
-    for (int e = tid; e < E; e += PNT) dst[e] = cscale(buf[e], sc);
+    for (int e = tid; e < E; e += PNT) dst[e] = cscale(buf[SP(e)], sc);
 }
 
 // ------------------------------------------------------------------ K3 ----
@@ -204,7 +204,7 @@ struct AnaArgs {
 };
 
 template <typename R, int IN, int OUT>
-__global__ void __launch_bounds__(PNT) analysis_pass(Geo g, AnaArgs<R> p) {
+__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) analysis_pass(Geo g, AnaArgs<R> p) {
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* buf = reinterpret_cast<C*>(smem_raw);
@@ -213,21 +213,21 @@ __global__ void __launch_bounds__(PNT) analysis_pass(Geo g, AnaArgs<R> p) {
     const int E = Wa << k;
     const C* src = p.src + (long long)bi * p.src_bs + (long long)st * E;
     if (IN == ANA_IN_PLAIN) {
-        for (int e = tid; e < E; e += PNT) buf[e] = src[e];
+        for (int e = tid; e < E; e += PNT) buf[SP(e)] = src[e];
         __syncthreads();
     } else {
-        C* tws = buf + E;
+        C* tws = buf + SP(E - 1) + 1;
         for (int e = tid; e < g.W; e += PNT) tws[e] = p.tw[e];
-        for (int e = tid; e < E; e += PNT) buf[e] = src[e];
+        for (int e = tid; e < E; e += PNT) buf[SP(e)] = src[e];
         __syncthreads();
-        block_fft<C, true, PNT, PCAP, false>(buf, g.logW, k, Wa, 1, tws);
+        block_fft16<C, true, PNT, PCAP, false, true>(buf, g.logW, k, Wa, 1, tws);
         // unitary scale and the output sign c * (-1)^(n1+n2) of ifft2c
         const R sc = R(1) / sqrt(R(g.W));
         const int rowbase = st << k;
         for (int e = tid; e < E; e += PNT) {
             const int n1 = rowbase + (e >> p.logWa), n2 = e & (Wa - 1);
             const R s = (((n1 + n2) & 1) ? -sc : sc) * (R)g.sign_c;
-            buf[e] = cscale(buf[e], s);
+            buf[SP(e)] = cscale(buf[SP(e)], s);
         }
         __syncthreads();
     }
@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(PNT) analysis_pass(Geo g, AnaArgs<R> p) {
             const int e = tid + i * PNT;
             if (e < P) {
                 const int ii = e >> logCq, jj = e & (Cq - 1);
-                const C* s0 = buf + (2 * ii) * Wa + 2 * jj;
-                C x00 = s0[0], x01 = s0[1], x10 = s0[Wa], x11 = s0[Wa + 1];
+                const int s0 = (2 * ii) * Wa + 2 * jj;
+                C x00 = buf[SP(s0)], x01 = buf[SP(s0 + 1)], x10 = buf[SP(s0 + Wa)], x11 = buf[SP(s0 + Wa + 1)];
                 C lo0 = Haar<R>::sum(x00, x10), hi0 = Haar<R>::dif(x00, x10);
                 C lo1 = Haar<R>::sum(x01, x11), hi1 = Haar<R>::dif(x01, x11);
                 o[i][0] = Haar<R>::sum(lo0, lo1);   // ll
@@ -259,10 +259,10 @@ __global__ void __launch_bounds__(PNT) analysis_pass(Geo g, AnaArgs<R> p) {
             const int e = tid + i * PNT;
             if (e < P) {
                 const int ii = e >> logCq, jj = e & (Cq - 1);
-                buf[ii * Wa + jj] = o[i][0];
-                buf[ii * Wa + Cq + jj] = o[i][1];
-                buf[(Rq + ii) * Wa + jj] = o[i][2];
-                buf[(Rq + ii) * Wa + Cq + jj] = o[i][3];
+                buf[SP(ii * Wa + jj)] = o[i][0];
+                buf[SP(ii * Wa + Cq + jj)] = o[i][1];
+                buf[SP((Rq + ii) * Wa + jj)] = o[i][2];
+                buf[SP((Rq + ii) * Wa + Cq + jj)] = o[i][3];
             }
         }
         __syncthreads();
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(PNT) analysis_pass(Geo g, AnaArgs<R> p) {
             const int f = tid + i * PNT;
             if (f < E) {
                 const StripSlot sl = strip_slot(g, p.a, k, Wa, p.logWa, st, f);
-                C u = buf[sl.smem];
+                C u = buf[SP(sl.smem)];
                 if (sl.approx && p.adst) {
                     p.adst[(long long)bi * p.adst_bs + (long long)st * (Wa >> k) + sl.smem] = u;
                 } else {
@@ -348,8 +348,8 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass(Geo g, C
     for (int e = tid; e < H; e += PNT) tws[e] = p.tw[e];
     for (int e = tid; e < E; e += PNT) buf[e] = p.src[ib + (long long)(e >> lc) * W + c0 + (e & (cw - 1))];
     __syncthreads();
-    if (MODE == COL_INV) block_fft<C, true, PNT, PCAP, true>(buf, g.logH, lc, 1, cw, tws);
-    else                 block_fft<C, false, PNT, PCAP, true>(buf, g.logH, lc, 1, cw, tws);
+    if (MODE == COL_INV) block_fft16<C, true, PNT, PCAP, true, false>(buf, g.logH, lc, 1, cw, tws);
+    else                 block_fft16<C, false, PNT, PCAP, true, false>(buf, g.logH, lc, 1, cw, tws);
     const R sc = R(1) / sqrt(R(H));
     if (MODE == COL_FWD || MODE == COL_INV) {
         // centred output sign c * (-1)^(k1+k2)
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass(Geo g, C
         }
     }
     __syncthreads();
-    block_fft<C, true, PNT, PCAP, true>(buf, g.logH, lc, 1, cw, tws);
+    block_fft16<C, true, PNT, PCAP, true, false>(buf, g.logH, lc, 1, cw, tws);
     for (int e = tid; e < E; e += PNT)
         p.dst[ib + (long long)(e >> lc) * W + c0 + (e & (cw - 1))] = cscale(buf[e], sc);
     if (MODE != COL_VDAMP) return;
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(PNT) row_pass(Geo g, const typename CT<R>::T* 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* buf = reinterpret_cast<C*>(smem_raw);
     const int W = g.W, E = W << logrows;
-    C* tws = buf + E;
+    C* tws = buf + SP(E - 1) + 1;
     const int st = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
     const long long base = (long long)bi * g.N + (long long)st * E;
     const int rowbase = st << logrows;
@@ -462,15 +462,15 @@ __global__ void __launch_bounds__(PNT) row_pass(Geo g, const typename CT<R>::T* 
     for (int e = tid; e < E; e += PNT) {
         C v = src[base + e];
         if (PRE_SIGN && (((rowbase + (e >> g.logW)) + (e & (W - 1))) & 1)) v = mk<C>(-v.x, -v.y);
-        buf[e] = v;
+        buf[SP(e)] = v;
     }
     __syncthreads();
-    block_fft<C, INV, PNT, PCAP, false>(buf, g.logW, logrows, W, 1, tws);
+    block_fft16<C, INV, PNT, PCAP, false, true>(buf, g.logW, logrows, W, 1, tws);
     const R sc = R(1) / sqrt(R(W));
     for (int e = tid; e < E; e += PNT) {
         R s = sc;
         if (POST_SIGN) s = ((((rowbase + (e >> g.logW)) + (e & (W - 1))) & 1) ? -sc : sc) * (R)g.sign_c;
-        dst[base + e] = cscale(buf[e], s);
+        dst[base + e] = cscale(buf[SP(e)], s);
     }
 }
 
