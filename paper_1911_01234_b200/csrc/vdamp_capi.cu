@@ -122,10 +122,18 @@ struct Launch {
     }
 };
 
+// Opt every kernel into the dynamic shared memory it is launched with (static
+// shared memory counts against the default 48 KB too), once per kernel/size.
 template <typename K>
 void set_smem(K kern, size_t bytes) {
-    static_assert(sizeof(K) > 0, "");
-    if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    static thread_local std::vector<std::pair<const void*, size_t>> done;
+    const void* key = reinterpret_cast<const void*>(kern);
+    for (auto& d : done)
+        if (d.first == key && d.second >= bytes) return;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    for (auto& d : done)
+        if (d.first == key) { d.second = bytes; return; }
+    done.push_back({key, bytes});
 }
 
 // ------------------------------------------------------------ sequences --
@@ -447,6 +455,7 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         p->cw = std::max(1, std::min(width, PCAP / height));
         p->logcw = ilog2(p->cw);
         p->ntiles = width / p->cw;
+        if (p->ntiles > MAXCT) throw Err{VDAMP_ERR_UNSUPPORTED, "too many column tiles"};
         p->rowlog = 0;
         while ((2LL << p->rowlog) * width <= PCAP && (2 << p->rowlog) <= height) ++p->rowlog;
         const size_t cs = precision == VDAMP_FP32 ? sizeof(float2) : sizeof(double2);

@@ -28,6 +28,7 @@ constexpr int SMALL_N = 4096;     // subbands up to this size use the small kern
 constexpr int SCAP = 16384;       // fp32 magnitudes sorted in shared memory at once
 template <typename R> struct Scap { static constexpr int v = SCAP; };
 constexpr int MAXTILES = 256;     // SCAP-tiles per subband (n <= 4M)
+constexpr int MAXCT = 1024;       // column tiles per image (H*W/PCAP for 2048^2)
 constexpr double ALPHA_CLAMP = 1.0 - 1e-9;   // src/vdamp.py:25
 constexpr double TAU_FLOOR = 1e-300;         // src/vdamp.py:118
 constexpr int TRACE_F = 8;
@@ -811,6 +812,7 @@ template <int NT>
 struct SelShared {
     double sh[66 + NT / 32 + 2];     // counting-sort min/max words + block scans
     double tsq[MAXTILES], tinv[MAXTILES], tpre[MAXTILES], tsuf[MAXTILES];
+    double tpart[MAXCT];             // tau partials of the column tiles
     double tau, totinv;
     Best best[NT / 32];
 };
@@ -831,11 +833,12 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
 #ifdef VDAMP_PHASE_TIMING
     long long ph0_ = clock64();
 #endif
-    if (tid == 0) {
-        double t = 0.0;
-        if (a.tau_in) t = a.tau_in[(long long)bi * g.S + j];
-        else for (int i = 0; i < a.ntiles; ++i) t += a.taupart[((long long)bi * a.ntiles + i) * g.S + j];
-        s_tau = t;
+    // tau_j: the column-tile partials are loaded in parallel and summed in tile
+    // order by thread 0 after the next barrier (deterministic, no serial loads)
+    if (a.tau_in) {
+        if (tid == 0) s_tau = a.tau_in[(long long)bi * g.S + j];
+    } else {
+        for (int i = tid; i < a.ntiles; i += NT) S_.tpart[i] = a.taupart[((long long)bi * a.ntiles + i) * g.S + j];
     }
     const C* rs = a.r + base;
     const C* w0 = a.w0 ? a.w0 + base : nullptr;
@@ -879,6 +882,11 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             }
         }
         __syncthreads();
+        if (c0 == 0 && !a.tau_in && tid == 0) {
+            double t = 0.0;
+            for (int i = 0; i < a.ntiles; ++i) t += S_.tpart[i];
+            s_tau = t;
+        }
         if constexpr (NT == SNT) {
 #ifdef VDAMP_PHASE_TIMING
             long long* dbg = (bi < 4096) ? &g_csort[bi][j][0] : nullptr;
