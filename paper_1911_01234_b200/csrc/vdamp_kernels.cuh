@@ -90,6 +90,49 @@ struct SynArgs {
     long long asrc_bs, dst_bs;
 };
 
+// Gather the coarse part of a strip (levels a+1..a+k-1 and the approximation
+// row, E/4 coefficients) into the top-left R1 x C1 corner of the mosaic
+// (row stride Wa), Onsager applied.  Uses the flat slot map of the sub-strip.
+template <typename R>
+__device__ __forceinline__ void gather_coarse(const Geo& g, const SynArgs<R>& p, const typename CT<R>::T* coef,
+                                              const R* spar, bool apply, typename CT<R>::T* buf, int st, int bi) {
+    typedef typename CT<R>::T C;
+    const int k = p.k, Wa = p.Wa;
+    const int logC1 = p.logWa - 1, C1 = 1 << logC1;
+    const int E1 = (Wa << k) >> 2;
+    constexpr int PER = PCAP / 4 / PNT;
+    C v[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int f = threadIdx.x + i * PNT;
+        if (f < E1) {
+            if (k > 1) {
+                const StripSlot sl = strip_slot(g, p.a + 1, k - 1, C1, logC1, st, f);
+                v[i] = (sl.approx && p.asrc) ? p.asrc[(long long)bi * p.asrc_bs + (long long)st * (Wa >> k) + sl.smem]
+                                             : coef[sl.gofs];
+            } else {
+                v[i] = p.asrc ? p.asrc[(long long)bi * p.asrc_bs + (long long)st * C1 + f]
+                              : coef[g.off[0] + (long long)st * C1 + f];
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int f = threadIdx.x + i * PNT;
+        if (f < E1) {
+            int j = 0, slot = f;
+            bool from_scratch = (p.asrc != nullptr);
+            if (k > 1) {
+                const StripSlot sl = strip_slot(g, p.a + 1, k - 1, C1, logC1, st, f);
+                j = sl.j; slot = sl.smem; from_scratch = sl.approx && p.asrc;
+            }
+            C x = v[i];
+            if (apply && !from_scratch) x = onsager<R, C>(x, spar[3 * j], spar[3 * j + 1], spar[3 * j + 2]);
+            buf[SP((slot >> logC1) * Wa + (slot & (C1 - 1)))] = x;
+        }
+    }
+}
+
 template <typename R, int MODE>
 __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) synth_pass(Geo g, SynArgs<R> p) {
     typedef typename CT<R>::T C;
@@ -97,54 +140,43 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) synth_pass(Geo g,
     C* buf = reinterpret_cast<C*>(smem_raw);
     const int st = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
     const int k = p.k, Wa = p.Wa;
+    const int E = Wa << k;
     const C* coef = p.coef + (long long)bi * g.N;
     const double* par = p.par ? p.par + (long long)bi * g.S * 3 : nullptr;
-    C* tws = buf + SP((Wa << k) - 1) + 1;
+    C* tws = buf + SP(E - 1) + 1;
+    __shared__ R spar[MAXS * 3];
     if (MODE == SYN_ROWFFT)
         for (int e = tid; e < g.W; e += PNT) tws[e] = p.tw[e];
-
-    // gather the strip's coefficients into the mosaic (Onsager applied); all
-    // loads of a thread are issued before any is used
-    __shared__ R spar[MAXS * 3];
     for (int i = tid; i < g.S * 3; i += PNT) spar[i] = par ? (R)par[i] : ((i % 3) == 2 ? R(1) : R(0));
-    __syncthreads();
-    {
-        constexpr int PER = PCAP / PNT;
-        const int E = Wa << k;
-        C v[PER];
+
+    // level-1 detail coefficients of this strip (3 chunks of R1 x C1): one 2x2
+    // output block per coefficient, loads issued first
+    const int logC1 = p.logWa - 1, C1 = 1 << logC1;
+    const int cnt1 = E >> 2;
+    const int jH = band_of(g.s, p.a, 0);
+    constexpr int MB = PCAP / 4 / PNT;
+    C dH[MB], dV[MB], dD[MB];
 #pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int f = tid + i * PNT;
-            if (f < E) {
-                const StripSlot sl = strip_slot(g, p.a, k, Wa, p.logWa, st, f);
-                if (sl.approx && p.asrc) v[i] = p.asrc[(long long)bi * p.asrc_bs + (long long)st * (Wa >> k) + sl.smem];
-                else v[i] = coef[sl.gofs];
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int f = tid + i * PNT;
-            if (f < E) {
-                const StripSlot sl = strip_slot(g, p.a, k, Wa, p.logWa, st, f);
-                C x = v[i];
-                if (par && !(sl.approx && p.asrc)) {
-                    const int j = sl.j;
-                    x = onsager<R, C>(x, spar[3 * j], spar[3 * j + 1], spar[3 * j + 2]);
-                }
-                buf[SP(sl.smem)] = x;
-            }
+    for (int i = 0; i < MB; ++i) {
+        const int b = tid + i * PNT;
+        if (b < cnt1) {
+            const long long o = (long long)st * cnt1 + b;
+            dH[i] = coef[g.off[jH] + o];
+            dV[i] = coef[g.off[jH + 1] + o];
+            dD[i] = coef[g.off[jH + 2] + o];
         }
     }
+    __syncthreads();                                   // spar, twiddles
+    gather_coarse<R>(g, p, coef, spar, par != nullptr, buf, st, bi);
     __syncthreads();
 
-    // synthesis, coarse to fine (src/wavelet.py:118-129)
-    constexpr int MQ = PCAP / 4 / PNT;
-    for (int q = k; q >= 1; --q) {
+    // coarse synthesis levels k..2 on the top-left corner (src/wavelet.py:118-129)
+    for (int q = k; q >= 2; --q) {
         const int logCq = p.logWa - q, Cq = 1 << logCq, Rq = 1 << (k - q);
         const int P = Rq * Cq;
-        C o[MQ][4];
+        C o[MB][4];
 #pragma unroll
-        for (int i = 0; i < MQ; ++i) {
+        for (int i = 0; i < MB; ++i) {
             const int e = tid + i * PNT;
             if (e < P) {
                 const int ii = e >> logCq, jj = e & (Cq - 1);
@@ -160,7 +192,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) synth_pass(Geo g,
         }
         __syncthreads();
 #pragma unroll
-        for (int i = 0; i < MQ; ++i) {
+        for (int i = 0; i < MB; ++i) {
             const int e = tid + i * PNT;
             if (e < P) {
                 const int ii = e >> logCq, jj = e & (Cq - 1);
@@ -171,22 +203,52 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) synth_pass(Geo g,
         __syncthreads();
     }
 
-    const int E = Wa << k;
+    // level 1 in registers: r~ of the three detail chunks, Haar synthesis of each
+    // 2x2 block; for ROWFFT the (-1)^(n1+n2) modulation (rows of a strip start
+    // at an even index, so the block pattern is +,-,-,+) and the unitary 1/sqrt(W)
+    // are folded in here
+    {
+        R tH = spar[3 * jH], aH = spar[3 * jH + 1], gH = spar[3 * jH + 2];
+        R tV = spar[3 * jH + 3], aV = spar[3 * jH + 4], gV = spar[3 * jH + 5];
+        R tD = spar[3 * jH + 6], aD = spar[3 * jH + 7], gD = spar[3 * jH + 8];
+        const R sc = (MODE == SYN_ROWFFT) ? R(1) / sqrt(R(g.W)) : R(1);
+        C o[MB][4];
+#pragma unroll
+        for (int i = 0; i < MB; ++i) {
+            const int b = tid + i * PNT;
+            if (b < cnt1) {
+                const int ii = b >> logC1, jj = b & (C1 - 1);
+                const C ll = buf[SP(ii * Wa + jj)];
+                C lh = dH[i], hl = dV[i], hh = dD[i];
+                if (par) {
+                    lh = onsager<R, C>(lh, tH, aH, gH);
+                    hl = onsager<R, C>(hl, tV, aV, gV);
+                    hh = onsager<R, C>(hh, tD, aD, gD);
+                }
+                C lo0 = Haar<R>::sum(ll, lh), lo1 = Haar<R>::dif(ll, lh);
+                C hi0 = Haar<R>::sum(hl, hh), hi1 = Haar<R>::dif(hl, hh);
+                o[i][0] = cscale(Haar<R>::sum(lo0, hi0), sc);
+                o[i][1] = cscale(Haar<R>::sum(lo1, hi1), MODE == SYN_ROWFFT ? -sc : sc);
+                o[i][2] = cscale(Haar<R>::dif(lo0, hi0), MODE == SYN_ROWFFT ? -sc : sc);
+                o[i][3] = cscale(Haar<R>::dif(lo1, hi1), sc);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < MB; ++i) {
+            const int b = tid + i * PNT;
+            if (b < cnt1) {
+                const int ii = b >> logC1, jj = b & (C1 - 1);
+                const int d = (2 * ii) * Wa + 2 * jj;
+                buf[SP(d)] = o[i][0]; buf[SP(d + 1)] = o[i][1]; buf[SP(d + Wa)] = o[i][2]; buf[SP(d + Wa + 1)] = o[i][3];
+            }
+        }
+        __syncthreads();
+    }
+
     C* dst = p.dst + (long long)bi * p.dst_bs + (long long)st * E;
-    if (MODE == SYN_PLAIN) {
-        for (int e = tid; e < E; e += PNT) dst[e] = buf[SP(e)];
-        return;
-    }
-    // (-1)^(n1+n2) then row FFT (unitary 1/sqrt(W))
-    const int rowbase = st << k;
-    for (int e = tid; e < E; e += PNT) {
-        const int n1 = rowbase + (e >> p.logWa), n2 = e & (Wa - 1);
-        if ((n1 + n2) & 1) { C v = buf[SP(e)]; buf[SP(e)] = mk<C>(-v.x, -v.y); }
-    }
-    __syncthreads();
-    block_fft16<C, false, PNT, PCAP, false, true>(buf, g.logW, k, Wa, 1, tws);
-    const R sc = R(1) / sqrt(R(g.W));
-    for (int e = tid; e < E; e += PNT) dst[e] = cscale(buf[SP(e)], sc);
+    if (MODE == SYN_ROWFFT) block_fft16<C, false, PNT, PCAP, false, true>(buf, g.logW, k, Wa, 1, tws);
+    for (int e = tid; e < E; e += PNT) dst[e] = buf[SP(e)];
 }
 
 // ------------------------------------------------------------------ K3 ----
@@ -213,34 +275,94 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) analysis_pass(Geo
     const int k = p.k, Wa = p.Wa;
     const int E = Wa << k;
     const C* src = p.src + (long long)bi * p.src_bs + (long long)st * E;
-    if (IN == ANA_IN_PLAIN) {
-        for (int e = tid; e < E; e += PNT) buf[SP(e)] = src[e];
-        __syncthreads();
-    } else {
+    C* coef = p.coef + (long long)bi * g.N;
+    __shared__ R spar[MAXS * 3];
+    if (OUT == ANA_OUT_VDAMP) {
+        const double* par = p.par + (long long)bi * g.S * 3;
+        for (int i = tid; i < g.S * 3; i += PNT) spar[i] = (R)par[i];
+    }
+    if (IN == ANA_IN_ROWIFFT) {
         C* tws = buf + SP(E - 1) + 1;
         for (int e = tid; e < g.W; e += PNT) tws[e] = p.tw[e];
         for (int e = tid; e < E; e += PNT) buf[SP(e)] = src[e];
         __syncthreads();
         block_fft16<C, true, PNT, PCAP, false, true>(buf, g.logW, k, Wa, 1, tws);
-        // unitary scale and the output sign c * (-1)^(n1+n2) of ifft2c
-        const R sc = R(1) / sqrt(R(g.W));
-        const int rowbase = st << k;
-        for (int e = tid; e < E; e += PNT) {
-            const int n1 = rowbase + (e >> p.logWa), n2 = e & (Wa - 1);
-            const R s = (((n1 + n2) & 1) ? -sc : sc) * (R)g.sign_c;
-            buf[SP(e)] = cscale(buf[SP(e)], s);
-        }
+    } else {
+        for (int e = tid; e < E; e += PNT) buf[SP(e)] = src[e];
         __syncthreads();
     }
 
-    // analysis, fine to coarse (src/wavelet.py:107-115)
-    constexpr int MQ = PCAP / 4 / PNT;
-    for (int q = 1; q <= k; ++q) {
+    // level 1 in registers: each thread analyses 2x2 pixel blocks (for ROWIFFT
+    // the ifft2c output sign c * (-1)^(n1+n2) -> +,-,-,+ per block, and the
+    // unitary 1/sqrt(W) are folded in); the three details go straight to
+    // global memory (VDAMP: r_k = Onsager(r_{k-1}) + Psi u), ll to the corner
+    const int logC1 = p.logWa - 1, C1 = 1 << logC1;
+    const int cnt1 = E >> 2;
+    const int jH = band_of(g.s, p.a, 0);
+    constexpr int MB = PCAP / 4 / PNT;
+    C ll[MB];
+    {
+        C oH[MB], oV[MB], oD[MB];
+        if (OUT == ANA_OUT_VDAMP) {
+#pragma unroll
+            for (int i = 0; i < MB; ++i) {
+                const int b = tid + i * PNT;
+                if (b < cnt1) {
+                    const long long o = (long long)st * cnt1 + b;
+                    oH[i] = coef[g.off[jH] + o];
+                    oV[i] = coef[g.off[jH + 1] + o];
+                    oD[i] = coef[g.off[jH + 2] + o];
+                }
+            }
+        }
+        const R sc = (IN == ANA_IN_ROWIFFT) ? (R)g.sign_c / sqrt(R(g.W)) : R(1);
+        const R tH = OUT == ANA_OUT_VDAMP ? spar[3 * jH] : R(0), aH = OUT == ANA_OUT_VDAMP ? spar[3 * jH + 1] : R(0),
+                gH = OUT == ANA_OUT_VDAMP ? spar[3 * jH + 2] : R(1);
+        const R tV = OUT == ANA_OUT_VDAMP ? spar[3 * jH + 3] : R(0), aV = OUT == ANA_OUT_VDAMP ? spar[3 * jH + 4] : R(0),
+                gV = OUT == ANA_OUT_VDAMP ? spar[3 * jH + 5] : R(1);
+        const R tD = OUT == ANA_OUT_VDAMP ? spar[3 * jH + 6] : R(0), aD = OUT == ANA_OUT_VDAMP ? spar[3 * jH + 7] : R(0),
+                gD = OUT == ANA_OUT_VDAMP ? spar[3 * jH + 8] : R(1);
+#pragma unroll
+        for (int i = 0; i < MB; ++i) {
+            const int b = tid + i * PNT;
+            if (b < cnt1) {
+                const int ii = b >> logC1, jj = b & (C1 - 1);
+                const int s0 = (2 * ii) * Wa + 2 * jj;
+                const C x00 = cscale(buf[SP(s0)], sc);
+                const C x01 = cscale(buf[SP(s0 + 1)], IN == ANA_IN_ROWIFFT ? -sc : sc);
+                const C x10 = cscale(buf[SP(s0 + Wa)], IN == ANA_IN_ROWIFFT ? -sc : sc);
+                const C x11 = cscale(buf[SP(s0 + Wa + 1)], sc);
+                const C lo0 = Haar<R>::sum(x00, x10), hi0 = Haar<R>::dif(x00, x10);
+                const C lo1 = Haar<R>::sum(x01, x11), hi1 = Haar<R>::dif(x01, x11);
+                ll[i] = Haar<R>::sum(lo0, lo1);
+                C lh = Haar<R>::dif(lo0, lo1), hl = Haar<R>::sum(hi0, hi1), hh = Haar<R>::dif(hi0, hi1);
+                if (OUT == ANA_OUT_VDAMP) {
+                    lh = cadd(onsager<R, C>(oH[i], tH, aH, gH), lh);
+                    hl = cadd(onsager<R, C>(oV[i], tV, aV, gV), hl);
+                    hh = cadd(onsager<R, C>(oD[i], tD, aD, gD), hh);
+                }
+                const long long o = (long long)st * cnt1 + b;
+                coef[g.off[jH] + o] = lh;
+                coef[g.off[jH + 1] + o] = hl;
+                coef[g.off[jH + 2] + o] = hh;
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < MB; ++i) {
+        const int b = tid + i * PNT;
+        if (b < cnt1) buf[SP((b >> logC1) * Wa + (b & (C1 - 1)))] = ll[i];
+    }
+    __syncthreads();
+
+    // coarse analysis levels 2..k on the corner (src/wavelet.py:107-115)
+    for (int q = 2; q <= k; ++q) {
         const int logCq = p.logWa - q, Cq = 1 << logCq, Rq = 1 << (k - q);
         const int P = Rq * Cq;
-        C o[MQ][4];
+        C o[MB][4];
 #pragma unroll
-        for (int i = 0; i < MQ; ++i) {
+        for (int i = 0; i < MB; ++i) {
             const int e = tid + i * PNT;
             if (e < P) {
                 const int ii = e >> logCq, jj = e & (Cq - 1);
@@ -248,15 +370,15 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) analysis_pass(Geo
                 C x00 = buf[SP(s0)], x01 = buf[SP(s0 + 1)], x10 = buf[SP(s0 + Wa)], x11 = buf[SP(s0 + Wa + 1)];
                 C lo0 = Haar<R>::sum(x00, x10), hi0 = Haar<R>::dif(x00, x10);
                 C lo1 = Haar<R>::sum(x01, x11), hi1 = Haar<R>::dif(x01, x11);
-                o[i][0] = Haar<R>::sum(lo0, lo1);   // ll
-                o[i][1] = Haar<R>::dif(lo0, lo1);   // lh  horizontal
-                o[i][2] = Haar<R>::sum(hi0, hi1);   // hl  vertical
-                o[i][3] = Haar<R>::dif(hi0, hi1);   // hh  diagonal
+                o[i][0] = Haar<R>::sum(lo0, lo1);
+                o[i][1] = Haar<R>::dif(lo0, lo1);
+                o[i][2] = Haar<R>::sum(hi0, hi1);
+                o[i][3] = Haar<R>::dif(hi0, hi1);
             }
         }
         __syncthreads();
 #pragma unroll
-        for (int i = 0; i < MQ; ++i) {
+        for (int i = 0; i < MB; ++i) {
             const int e = tid + i * PNT;
             if (e < P) {
                 const int ii = e >> logCq, jj = e & (Cq - 1);
@@ -269,42 +391,41 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) analysis_pass(Geo
         __syncthreads();
     }
 
-    // scatter the mosaic back to the flat layout (VDAMP: r_new = Onsager(r_old) + u);
-    // all r_old loads of a thread are issued before any is used
-    C* coef = p.coef + (long long)bi * g.N;
-    __shared__ R spar[MAXS * 3];
-    if (OUT == ANA_OUT_VDAMP) {
-        const double* par = p.par + (long long)bi * g.S * 3;
-        for (int i = tid; i < g.S * 3; i += PNT) spar[i] = (R)par[i];
-        __syncthreads();
-    }
+    // scatter the coarse corner (E/4 coefficients: levels 2..k + approximation)
     {
-        constexpr int PER = PCAP / PNT;
-        C old[PER];
+        const int E1 = cnt1;
+        C old[MB];
         if (OUT == ANA_OUT_VDAMP) {
 #pragma unroll
-            for (int i = 0; i < PER; ++i) {
+            for (int i = 0; i < MB; ++i) {
                 const int f = tid + i * PNT;
-                if (f < E) {
-                    const StripSlot sl = strip_slot(g, p.a, k, Wa, p.logWa, st, f);
-                    if (!(sl.approx && p.adst)) old[i] = coef[sl.gofs];
+                if (f < E1) {
+                    if (k > 1) {
+                        const StripSlot sl = strip_slot(g, p.a + 1, k - 1, C1, logC1, st, f);
+                        if (!(sl.approx && p.adst)) old[i] = coef[sl.gofs];
+                    } else if (!p.adst) {
+                        old[i] = coef[g.off[0] + (long long)st * C1 + f];
+                    }
                 }
             }
         }
 #pragma unroll
-        for (int i = 0; i < PER; ++i) {
+        for (int i = 0; i < MB; ++i) {
             const int f = tid + i * PNT;
-            if (f < E) {
-                const StripSlot sl = strip_slot(g, p.a, k, Wa, p.logWa, st, f);
-                C u = buf[SP(sl.smem)];
-                if (sl.approx && p.adst) {
-                    p.adst[(long long)bi * p.adst_bs + (long long)st * (Wa >> k) + sl.smem] = u;
+            if (f < E1) {
+                int j = 0, slot = f;
+                long long gofs = g.off[0] + (long long)st * C1 + f;
+                bool to_scratch = (p.adst != nullptr);
+                if (k > 1) {
+                    const StripSlot sl = strip_slot(g, p.a + 1, k - 1, C1, logC1, st, f);
+                    j = sl.j; slot = sl.smem; gofs = sl.gofs; to_scratch = sl.approx && p.adst;
+                }
+                C u = buf[SP((slot >> logC1) * Wa + (slot & (C1 - 1)))];
+                if (to_scratch) {
+                    p.adst[(long long)bi * p.adst_bs + (long long)st * (Wa >> k) + (k > 1 ? slot : f)] = u;
                 } else {
-                    if (OUT == ANA_OUT_VDAMP) {
-                        const int j = sl.j;
-                        u = cadd(onsager<R, C>(old[i], spar[3 * j], spar[3 * j + 1], spar[3 * j + 2]), u);
-                    }
-                    coef[sl.gofs] = u;
+                    if (OUT == ANA_OUT_VDAMP) u = cadd(onsager<R, C>(old[i], spar[3 * j], spar[3 * j + 1], spar[3 * j + 2]), u);
+                    coef[gofs] = u;
                 }
             }
         }
