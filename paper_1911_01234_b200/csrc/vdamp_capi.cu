@@ -219,7 +219,7 @@ struct Seq {
         const int np = 2 * p->s;
         const size_t E = (size_t)p->H << p->logcw;
         return E * sizeof(C) + (size_t)p->H * sizeof(C) + (size_t)np * PNT * sizeof(double) +
-               (size_t)np * p->cw * sizeof(double) + (size_t)np * p->H * sizeof(double);
+               (size_t)np * p->cw * sizeof(double) + (size_t)np * p->H * sizeof(R);
     }
 
     void col(int mode, const C* src, C* dst, int cls) {

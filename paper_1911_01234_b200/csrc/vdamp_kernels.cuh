@@ -24,7 +24,7 @@ constexpr int PNT = 256;          // threads of strip / column kernels
 constexpr int PCAP = 4096;        // complex elements per strip / column tile
 constexpr int SNT = 1024;         // threads of the SURE kernel (subbands > SMALL_N)
 constexpr int SNT_SMALL = 256;    // threads of the small-subband SURE kernel
-constexpr int SMALL_N = 4096;     // subbands up to this size use the small kernel
+constexpr int SMALL_N = 1024;     // subbands up to this size use the small kernel
 constexpr int SCAP = 16384;       // fp32 magnitudes sorted in shared memory at once
 template <typename R> struct Scap { static constexpr int v = SCAP; };
 constexpr int MAXTILES = 256;     // SCAP-tiles per subband (n <= 4M)
@@ -468,7 +468,20 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass(Geo g, C
     const int c0 = tile << lc;
     const long long ib = (long long)bi * g.N;
     for (int e = tid; e < H; e += PNT) tws[e] = p.tw[e];
-    for (int e = tid; e < E; e += PNT) buf[e] = p.src[ib + (long long)(e >> lc) * W + c0 + (e & (cw - 1))];
+    {
+        constexpr int PER = PCAP / PNT;
+        C v[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = tid + i * PNT;
+            if (e < E) v[i] = p.src[ib + (long long)(e >> lc) * W + c0 + (e & (cw - 1))];
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = tid + i * PNT;
+            if (e < E) buf[e] = v[i];
+        }
+    }
     __syncthreads();
     if (MODE == COL_INV) block_fft16<C, true, PNT, PCAP, true, false>(buf, g.logH, lc, 1, cw, tws);
     else                 block_fft16<C, false, PNT, PCAP, true, false>(buf, g.logH, lc, 1, cw, tws);
@@ -535,18 +548,20 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass(Geo g, C
     // thread tid always sees column c = tid % cw (PNT is a multiple of cw):
     // per row profile q, sum its rows in registers, then combine the threads
     // of each column in a fixed order (deterministic)
+    // per-thread sums over its <= 16 rows in the working precision (float in
+    // fp32 mode: 1e-7 relative), thread and column combination in float64
     double* part = reinterpret_cast<double*>(tws + H);   // [np][PNT] thread partials
-    double* prs = part + np * PNT + np * cw;             // [np][H] row profiles
-    for (int i = tid; i < np * H; i += PNT) prs[i] = p.prow[i];
+    R* prs = reinterpret_cast<R*>(part + np * PNT + np * cw);   // [np][H] row profiles
+    for (int i = tid; i < np * H; i += PNT) prs[i] = (R)p.prow[i];
     __syncthreads();
     for (int q = 0; q < np; ++q) {
-        double a = 0.0;
+        R a = R(0);
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
             const int e = tid + i * PNT;
-            if (e < E) a += prs[q * H + (e >> lc)] * (double)wreg[i];
+            if (e < E) a += prs[q * H + (e >> lc)] * wreg[i];
         }
-        part[q * PNT + tid] = a;
+        part[q * PNT + tid] = (double)a;
     }
     __syncthreads();
     double* psum = part + np * PNT;                       // [np][cw] column partials
@@ -864,10 +879,19 @@ __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, in
     const int E = T >= NT ? T / NT : 1;
     const bool act = tid * E < T;
     const int b0 = tid * E;
+    constexpr int EMAX = 16;
     double ssq = 0.0, sinv = 0.0;
+    double sufl[EMAX];                       // sum of inverses above each owned key, within the segment
     if (act) {
         for (int e = 0; e < E; ++e) { const double m = (double)keys[KI(b0 + e)]; ssq += m * m; }
-        for (int e = E - 1; e >= 0; --e) { const double m = (double)keys[KI(b0 + e)]; if (m > 0) sinv += __drcp_rn(m); }
+#pragma unroll
+        for (int e = EMAX - 1; e >= 0; --e) {
+            if (e < E) {
+                sufl[e] = sinv;
+                const double m = (double)keys[KI(b0 + e)];
+                if (m > 0) sinv += __drcp_rn(m);
+            }
+        }
     }
     const double pre = block_excl_scan<NT, false>(ssq, sh) + pre_tile;
     const double suf = block_excl_scan<NT, true>(sinv, sh) + suf_tile;
@@ -877,19 +901,6 @@ __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, in
     // exact suffix of inverses per owned key (accumulated from the large keys
     // down, no subtraction), then a forward walk for the prefix of squares:
     // both sums are built in the direction that never cancels
-    constexpr int EMAX = 16;
-    double sufv[EMAX];
-    {
-        double acc = suf;
-#pragma unroll
-        for (int e = EMAX - 1; e >= 0; --e) {
-            if (e < E) {
-                sufv[e] = acc;
-                const double m = (double)keys[KI(b0 + e)];
-                if (m > 0) acc += __drcp_rn(m);
-            }
-        }
-    }
     double zacc = pre;
 #pragma unroll
     for (int e = 0; e < EMAX; ++e) {
@@ -900,7 +911,7 @@ __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, in
             const double nxt = (il + 1 < T) ? (double)keys[KI(il + 1)] : next_tile_first;
             if (m != nxt) {
                 const double zeroed = zacc;
-                const double inv_above = sufv[e];
+                const double inv_above = suf + sufl[e];        // both >= 0: no cancellation
                 const double cnt = (double)(n - (tilebase + il + 1));
                 const double risk = zeroed + m * m * cnt - nt + tau * (2.0 * cnt - m * inv_above);
                 consider(best, risk, m, cnt, inv_above);
