@@ -269,8 +269,11 @@ struct Seq {
             if (big) {
                 const int cap = Scap<R>::v;
                 const size_t slots = (size_t)(cap + cap / 32 + 1) + 1;
-                const size_t sm = sizeof(R) == 4 ? 2 * (slots + 1) * sizeof(R) + (CS_BUCKETS / 2) * sizeof(unsigned)
-                                                 : slots * sizeof(R);
+                size_t sm = sizeof(R) == 4 ? 2 * (slots + 1) * sizeof(R) + (CS_BUCKETS / 2) * sizeof(unsigned)
+                                           : slots * sizeof(R);
+                // large subbands: global counting sort counters + ranking tile
+                const size_t gcs = sizeof(R) == 4 ? 32768 * 4 + 16384 * sizeof(R) : 8192 * 4 + 8192 * sizeof(R);
+                if (sm < gcs) sm = gcs;
                 auto k = sure_select<R, SNT>;
                 set_smem(k, sm);
                 k<<<grid, SNT, sm, st_>>>(p->geo, a);

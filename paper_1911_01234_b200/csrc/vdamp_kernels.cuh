@@ -767,7 +767,12 @@ __device__ long long g_csort[4096][64][6];
 #define CS_MARK(i) do { } while (0)
 #endif
 
-__device__ void counting_sort(const float* keys, float* out, unsigned* cnt, int n, double* sh, long long* dbg = nullptr) {
+constexpr int CS_MAXB = 256;      // larger buckets -> comparison-sort fallback (degenerate data)
+
+// Returns false (nothing written to out) when some bucket holds more than
+// CS_MAXB keys: heavy ties / concentrated data (e.g. a diverged run) would make
+// the in-bucket ranking quadratic, the caller then uses the bitonic sort.
+__device__ bool counting_sort(const float* keys, float* out, unsigned* cnt, int n, double* sh, long long* dbg = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 #ifdef VDAMP_PHASE_TIMING
     long long cs0_ = clock64();
@@ -812,6 +817,14 @@ __device__ void counting_sort(const float* keys, float* out, unsigned* cnt, int 
     }
     __syncthreads();
     CS_MARK(1);
+    {
+        unsigned big = 0;
+        for (int i = tid; i < CS_BUCKETS / 2; i += SNT) {
+            const unsigned v = cnt[i];
+            big |= ((v & 0xffffu) > (unsigned)CS_MAXB) | ((v >> 16) > (unsigned)CS_MAXB);
+        }
+        if (__syncthreads_or(big)) return false;
+    }
     // exclusive scan of the CS_BUCKETS 16-bit counts (thread t: buckets [32t, 32t+32))
     {
         constexpr int PER = CS_BUCKETS / 2 / SNT;    // packed words per thread
@@ -866,6 +879,150 @@ __device__ void counting_sort(const float* keys, float* out, unsigned* cnt, int 
     for (int i = tid; i < n; i += SNT) ob[KI(i)] = fb[KI(i)];
     __syncthreads();
     CS_MARK(4);
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// Counting sort of a large subband (n > shared capacity) held in global
+// scratch (L2-resident): 32768 32-bit bucket counters in shared memory, keys
+// in A (input, overwritten by the sorted output) and B (bucket-grouped
+// temporary).  Same bucket map and parallel in-bucket ranking as
+// counting_sort; works on the IEEE bit patterns of float or double keys.
+// ---------------------------------------------------------------------------
+template <typename R> struct KeyU;
+template <> struct KeyU<float> { typedef unsigned int U; };
+template <> struct KeyU<double> { typedef unsigned long long U; };
+
+template <typename R, int NT>
+__device__ bool global_counting_sort(R* A, R* B, unsigned* cnt, int n, double* sh) {
+    typedef typename KeyU<R>::U U;
+    // 32768 buckets (fp32) / 8192 (fp64) 32-bit counters, followed in shared
+    // memory by a ranking tile of GCS_TILE keys
+    constexpr int NB = sizeof(R) == 4 ? 32768 : 8192;
+    constexpr int TILE = sizeof(R) == 4 ? 16384 : 8192;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    U* ka = reinterpret_cast<U*>(A);
+    U* kb = reinterpret_cast<U*>(B);
+    U* tl = reinterpret_cast<U*>(cnt + NB);
+    U mn = ~U(0), mx = 0;
+    for (int i = tid; i < n; i += NT) { const U k = ka[i]; if (k) mn = k < mn ? k : mn; mx = k > mx ? k : mx; }
+    for (int o = 16; o > 0; o >>= 1) {
+        const U a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn; mx = b > mx ? b : mx;
+    }
+    U* red = reinterpret_cast<U*>(sh);
+    __syncthreads();
+    if (lane == 0) { red[w] = mn; red[32 + w] = mx; }
+    for (int i = tid; i < NB; i += NT) cnt[i] = 0;
+    __syncthreads();
+    if (tid == 0) {
+        U a = red[0], b = red[32];
+        for (int i = 1; i < NT / 32; ++i) { a = red[i] < a ? red[i] : a; b = red[32 + i] > b ? red[32 + i] : b; }
+        red[0] = a; red[32] = b;
+    }
+    __syncthreads();
+    mn = red[0]; mx = red[32];
+    __syncthreads();
+    if (mn > mx) mn = mx;
+    int lo = 0;
+    while (((mx >> lo) - (mn >> lo)) >= (U)(NB - 2)) ++lo;
+    const U base = mn >> lo;
+    auto bucket = [&](U k) -> unsigned { return k ? (unsigned)((k >> lo) - base + 1) : 0u; };
+    for (int i = tid; i < n; i += NT) atomicAdd(&cnt[bucket(ka[i])], 1u);
+    __syncthreads();
+    {
+        unsigned big = 0;
+        for (int i = tid; i < NB; i += NT) big |= cnt[i] > (unsigned)CS_MAXB;
+        if (__syncthreads_or(big)) return false;
+    }
+    {
+        constexpr int PER = NB / NT;
+        unsigned tot = 0;
+        for (int i = 0; i < PER; ++i) tot += cnt[tid * PER + i];
+        unsigned run = (unsigned)block_excl_scan<NT, false>((double)tot, sh + 66);
+        for (int i = 0; i < PER; ++i) { const unsigned c = cnt[tid * PER + i]; cnt[tid * PER + i] = run; run += c; }
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += NT) {
+        const U k = ka[i];
+        kb[atomicAdd(&cnt[bucket(k)], 1u)] = k;
+    }
+    __syncthreads();
+    // cnt[b] = end of bucket b.  Rank inside buckets tile by tile in shared
+    // memory; tiles end on bucket boundaries so no bucket is split.
+    int S0 = 0;
+    while (S0 < n) {
+        int E0 = S0 + TILE < n ? S0 + TILE : n;
+        if (E0 < n) {
+            const unsigned bE = bucket(kb[E0]);
+            E0 = bE ? (int)cnt[bE - 1] : 0;            // start of the bucket holding position E0
+        }
+        if (E0 <= S0) {
+            // one bucket larger than a tile: rank it straight from global memory
+            E0 = (int)cnt[bucket(kb[S0])];
+            for (int i = S0 + tid; i < E0; i += NT) {
+                const U x = kb[i];
+                unsigned rank = 0;
+                for (int q = S0; q < E0; ++q) { const U y = kb[q]; rank += (y < x) || (y == x && q < i); }
+                ka[S0 + rank] = x;
+            }
+            __syncthreads();
+            S0 = E0;
+            continue;
+        }
+        for (int i = S0 + tid; i < E0; i += NT) tl[i - S0] = kb[i];
+        __syncthreads();
+        for (int i = S0 + tid; i < E0; i += NT) {
+            const U x = tl[i - S0];
+            const unsigned b = bucket(x);
+            const int e1 = (int)cnt[b], s0 = b ? (int)cnt[b - 1] : 0;
+            unsigned rank = 0;
+            for (int q = s0; q < e1; ++q) { const U y = tl[q - S0]; rank += (y < x) || (y == x && q < i); }
+            ka[s0 + rank] = x;
+        }
+        __syncthreads();
+        S0 = E0;
+    }
+    return true;
+}
+
+// Comparison-sort fallback for a large subband in global scratch: bitonic
+// sort of CAP-key chunks in shared memory, then pairwise merge-path merges in
+// global memory (n and CAP powers of two).  Returns the buffer holding the result.
+template <typename R, int NT>
+__device__ R* global_merge_sort(R* A, R* B, R* smem, int n, int CAP) {
+    const int tid = threadIdx.x;
+    for (int c0 = 0; c0 < n; c0 += CAP) {
+        for (int e = tid; e < CAP; e += NT) smem[KI(e)] = A[c0 + e];
+        __syncthreads();
+        block_sort<R, NT>(smem, CAP);
+        for (int e = tid; e < CAP; e += NT) A[c0 + e] = smem[KI(e)];
+        __syncthreads();
+    }
+    R* srcb = A;
+    R* dstb = B;
+    const int per = n / NT;
+    for (int w = CAP; w < n; w <<= 1) {
+        const int o0 = tid * per;
+        const int pb = o0 / (2 * w) * (2 * w);
+        const R* X = srcb + pb;
+        const R* Y = srcb + pb + w;
+        const int d = o0 - pb;
+        int lo = d > w ? d - w : 0, hi = d < w ? d : w;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (X[mid] <= Y[d - 1 - mid]) lo = mid + 1; else hi = mid;
+        }
+        int ia = lo, ib = d - lo;
+        for (int e = 0; e < per; ++e) {
+            R v;
+            if (ib >= w || (ia < w && X[ia] <= Y[ib])) v = X[ia++]; else v = Y[ib++];
+            dstb[o0 + e] = v;
+        }
+        __syncthreads();
+        R* t = srcb; srcb = dstb; dstb = t;
+    }
+    return srcb;
 }
 
 // Evaluate the candidates owned by this thread on one tile of sorted
@@ -984,7 +1141,7 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
     R* stage = keys + KI(CAPK) + 2;
     unsigned* ccnt = reinterpret_cast<unsigned*>(stage + KI(CAPK) + 2);
     const bool csort = NT == SNT && sizeof(R) == 4 && T >= 4096;
-    for (int c0 = 0; c0 < n; c0 += T) {
+    if (!large) {
         R* dstk = csort ? stage : keys;
         // issue 8 independent loads per thread before using any (memory-level parallelism)
         constexpr int LB = 8;
@@ -993,7 +1150,7 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
 #pragma unroll
             for (int u = 0; u < LB; ++u) {
                 const int e = e0 + u * NT;
-                if (e < T) v[u] = rs[c0 + e];
+                if (e < T) v[u] = rs[e];
             }
 #pragma unroll
             for (int u = 0; u < LB; ++u) {
@@ -1005,7 +1162,7 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
                 for (int u = 0; u < LB; ++u) {
                     const int e = e0 + u * NT;
                     if (e < T) {
-                        const C w = w0[c0 + e];
+                        const C w = w0[e];
                         const double dx = (double)v[u].x - (double)w.x, dy = (double)v[u].y - (double)w.y;
                         err += dx * dx + dy * dy;
                         ref += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
@@ -1014,7 +1171,7 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             }
         }
         __syncthreads();
-        if (c0 == 0 && !a.tau_in && tid == 0) {
+        if (!a.tau_in && tid == 0) {
             double t = 0.0;
             for (int i = 0; i < a.ntiles; ++i) t += S_.tpart[i];
             s_tau = t;
@@ -1025,54 +1182,49 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
 #else
             long long* dbg = nullptr;
 #endif
-            if (csort) counting_sort(reinterpret_cast<const float*>(stage), reinterpret_cast<float*>(keys), ccnt, T, sh, dbg);
-            else block_sort<R, NT>(keys, T);
+            bool done = false;
+            if (csort) done = counting_sort(reinterpret_cast<const float*>(stage), reinterpret_cast<float*>(keys), ccnt, T, sh, dbg);
+            if (csort && !done) {
+                for (int e = tid; e < T; e += NT) keys[KI(e)] = stage[KI(e)];
+                __syncthreads();
+            }
+            if (!done) block_sort<R, NT>(keys, T);
         } else {
             block_sort<R, NT>(keys, T);
         }
-        if (large) {
-            for (int e = tid; e < T; e += NT) a.kA[base + c0 + e] = keys[KI(e)];
-            __syncthreads();
-        }
-    }
-    if (large) {
-        // merge sorted runs pairwise in global memory (merge path per thread)
-        R* srcb = a.kA + base;
-        R* dstb = a.kB + base;
-        const int per = n / NT;
-        for (int w = CAPK; w < n; w <<= 1) {
-            const int o0 = tid * per;
-            const int pb = o0 / (2 * w) * (2 * w);
-            const R* A = srcb + pb;
-            const R* Bv = srcb + pb + w;
-            const int d = o0 - pb;
-            int lo = d > w ? d - w : 0, hi = d < w ? d : w;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (A[mid] <= Bv[d - 1 - mid]) lo = mid + 1; else hi = mid;
+    } else {
+        // whole subband -> global scratch keys, counting sort there (L2-resident)
+        R* ka = a.kA + base;
+        for (int e = tid; e < n; e += NT) {
+            const C v = rs[e];
+            ka[e] = cmag(v);
+            if (w0) {
+                const C w = w0[e];
+                const double dx = (double)v.x - (double)w.x, dy = (double)v.y - (double)w.y;
+                err += dx * dx + dy * dy;
+                ref += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
             }
-            int ia = lo, ib = d - lo;
-            for (int e = 0; e < per; ++e) {
-                R v;
-                if (ib >= w || (ia < w && A[ia] <= Bv[ib])) v = A[ia++]; else v = Bv[ib++];
-                dstb[o0 + e] = v;
-            }
-            __syncthreads();
-            R* t = srcb; srcb = dstb; dstb = t;
         }
-        sorted = srcb;
+        __syncthreads();
+        if (!a.tau_in && tid == 0) {
+            double t = 0.0;
+            for (int i = 0; i < a.ntiles; ++i) t += S_.tpart[i];
+            s_tau = t;
+        }
+        sorted = ka;
+        if constexpr (NT == SNT) {
+            if (!global_counting_sort<R, NT>(ka, a.kB + base, reinterpret_cast<unsigned*>(keys), n, sh))
+                sorted = global_merge_sort<R, NT>(ka, a.kB + base, keys, n, CAPK);
+        }
         // tile totals (ascending squares, descending inverses)
         for (int t = 0; t < ntl; ++t) {
             double q = 0.0, v = 0.0;
             for (int e = tid; e < CAPK; e += NT) {
                 const double m = (double)sorted[t * CAPK + e];
                 q += m * m;
+                if (m > 0) v += __drcp_rn(m);
             }
             q = block_sum<NT>(q, sh);
-            for (int e = tid; e < CAPK; e += NT) {
-                const double m = (double)sorted[t * CAPK + e];
-                if (m > 0) v += 1.0 / m;
-            }
             v = block_sum<NT>(v, sh);
             if (tid == 0) { tsq[t] = q; tinv[t] = v; }
         }

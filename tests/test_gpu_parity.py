@@ -76,6 +76,10 @@ def _tricky_coeffs(rng, n, kind):
         r = np.round(r, 1)
     elif kind == "zeros":
         r[rng.random(n) < 0.3] = 0
+    elif kind == "diverged":
+        # a blown-up run (cf. reference VDAMP on cfg2 slice 20): huge, nearly equal
+        # magnitudes with few distinct values -> crowded buckets, sort fallback
+        r = 7.7e12 * (1 + 1e-7 * rng.integers(0, 15, n)) * np.exp(1j * rng.uniform(0, 6.28, n))
     elif kind == "sparse":
         r = r * 0.05
         idx = rng.choice(n, n // 20, replace=False)
@@ -84,7 +88,7 @@ def _tricky_coeffs(rng, n, kind):
 
 
 @pytest.mark.parametrize("shape", [(64, 64, 3), (256, 256, 4), (512, 512, 2)])
-@pytest.mark.parametrize("kind", ["gauss", "ties", "zeros", "sparse"])
+@pytest.mark.parametrize("kind", ["gauss", "ties", "zeros", "sparse", "diverged"])
 def test_sure_select_vs_oracle(oracle, shape, kind):
     """Exact SURE argmin incl. ties, zeros, interior points; 512x512 s=2 has 65,536-entry
     subbands (multi-tile merge path)."""

@@ -5,20 +5,24 @@ sys.path.insert(0, ROOT)
 os.environ["VDAMP_LIB"] = os.path.join(ROOT, "paper_1911_01234_b200", "libvdamp_b200_phase.so")
 import numpy as np
 from paper_1911_01234_b200 import _lib, vdamp, workload
-w = workload.make_workload("cfg1", batch=64)
-vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, 4, 3, precision="fp32")
+cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg1"
+nb = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+w = workload.make_workload(cfg, batch=nb)
+vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, w.config.scales, 3, precision="fp32")
 buf = (ctypes.c_longlong * (64 * 64 * 4))()
 lib = _lib.load()
 lib.vdamp_debug_phase_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
 _lib.check(lib.vdamp_debug_phase_times(buf, 64))
-a = np.frombuffer(buf, dtype=np.int64).reshape(64, 64, 4)[:, :13, :3]
-lens = [256] * 4 + [1024] * 3 + [4096] * 3 + [16384] * 3
-for j in range(13):
+S = 1 + 3 * w.config.scales
+a = np.frombuffer(buf, dtype=np.int64).reshape(64, 64, 4)[:nb, :S, :3]
+from paper_1911_01234_b200.wavelet import SubbandLayout
+lens = [b.length for b in SubbandLayout.create(w.config.size, w.config.size, w.config.scales).subbands]
+for j in range(S):
     m = a[:, j, :].mean(0)
-    print(f"subband {j:2d} n={lens[j]:5d}  load+sort {m[0]:9.0f}  scan {m[1]:9.0f}  argmin {m[2]:7.0f} cycles")
+    print(f"subband {j:2d} n={lens[j]:6d}  load+sort {m[0]:9.0f}  scan {m[1]:9.0f}  argmin {m[2]:7.0f} cycles")
 
 buf2 = (ctypes.c_longlong * (64 * 64 * 6))()
 lib.vdamp_debug_csort_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
 _lib.check(lib.vdamp_debug_csort_times(buf2, 64))
-c = np.frombuffer(buf2, dtype=np.int64).reshape(64, 64, 6)[:, 10:13, :5].mean((0, 1))
+c = np.frombuffer(buf2, dtype=np.int64).reshape(64, 64, 6)[:nb, S - 3:S, :5].mean((0, 1))
 print("counting sort (n=16384) cycles: minmax %.0f  hist %.0f  scan %.0f  scatter %.0f  fixup %.0f" % tuple(c))
