@@ -218,11 +218,11 @@ def main():
     w = workload.make_workload(cfg, batch=B, first=rank * B)
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ns = max(4, min(cores, 32))
+        ns = max(8, min(2 * cores, B))                     # ~0.55 s of CPU per slice: 10-30 s of work
         rate, ts = cpu_oracle_rate(w, ns, cores, repeats=1)
         cpu_base = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                     "sample": f"{ns} of the {B} slices x {cfg.n_iters} iterations, one slice per process, "
-                              f"{cores} processes (oracle/vdamp_oracle.py, numpy float64), {ts[0]:.1f} s"}
+                              f"{cores} processes (oracle/vdamp_oracle.py, numpy float64), {ts[0]:.1f} s wall"}
 
     import torch
     import torch.distributed as dist
