@@ -72,6 +72,8 @@ struct Plan {
     void* w0 = nullptr;             // dwt(x0)
     void* xtmp = nullptr;           // per-iteration finalize image (NMSE)
     double* trtmp = nullptr;        // [B][S][TRACE_F]
+    cudaStream_t side = nullptr;    // fork/join stream for the small-subband SURE kernel
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool have_meas = false;
     bool have_gt = false;
     size_t bytes = 0;
@@ -257,15 +259,28 @@ struct Seq {
         a.kA = (R*)p->kA; a.kB = (R*)p->kB;
         // big subbands: 1024-thread CTAs with the full sort workspace; small ones:
         // 256-thread CTAs with little shared memory, many per SM
+        // the small-subband kernel runs on a side stream, concurrently with the
+        // big one (its CTAs fill the SMs the big kernel's tail leaves idle)
+        bool forked = false;
         for (int big = 1; big >= 0; --big) {
             std::vector<int> st{0}, li;
             for (int j = 0; j < p->S; ++j)
-                if ((p->geo.len[j] > SMALL_N) == (big == 1)) { li.push_back(j); st.push_back((int)li.size()); }
+                if ((p->geo.len[j] > SMALL_N) == (big == 1)) li.push_back(j);
+            // longest items first (grid is image-fastest, so they are all scheduled first)
+            std::stable_sort(li.begin(), li.end(), [&](int x, int y) { return p->geo.len[x] > p->geo.len[y]; });
+            for (size_t i = 0; i < li.size(); ++i) st.push_back((int)i + 1);
             if (li.empty()) continue;
             for (size_t i = 0; i < st.size(); ++i) a.item_start[i] = st[i];
             for (size_t i = 0; i < li.size(); ++i) a.item_list[i] = li[i];
-            dim3 grid((unsigned)li.size(), p->B);
-            Launch L(p, 3, st_);
+            dim3 grid(p->B, (unsigned)li.size());
+            cudaStream_t ls = st_;
+            if (!big && p->side && p->B * li.size() >= 64) {
+                CK(cudaEventRecord(p->ev_fork, st_));
+                CK(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+                ls = p->side;
+                forked = true;
+            }
+            Launch L(p, 3, ls);
             if (big) {
                 const int cap = Scap<R>::v;
                 const size_t slots = (size_t)(cap + cap / 32 + 1) + 1;
@@ -276,13 +291,17 @@ struct Seq {
                 if (sm < gcs) sm = gcs;
                 auto k = sure_select<R, SNT>;
                 set_smem(k, sm);
-                k<<<grid, SNT, sm, st_>>>(p->geo, a);
+                k<<<grid, SNT, sm, ls>>>(p->geo, a);
             } else {
                 const size_t sm = (size_t)(SMALL_N + SMALL_N / 32 + 2) * sizeof(R);
                 auto k = sure_select<R, SNT_SMALL>;
                 set_smem(k, sm);
-                k<<<grid, SNT_SMALL, sm, st_>>>(p->geo, a);
+                k<<<grid, SNT_SMALL, sm, ls>>>(p->geo, a);
             }
+        }
+        if (forked) {
+            CK(cudaEventRecord(p->ev_join, p->side));
+            CK(cudaStreamWaitEvent(st_, p->ev_join, 0));
         }
     }
 
@@ -373,6 +392,9 @@ void free_plan(Plan* p) {
     for (void* b : bufs) if (b) cudaFree(b);
     for (void* b : p->scratch) if (b) cudaFree(b);
     for (auto& e : p->ev) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
+    if (p->side) cudaStreamDestroy(p->side);
+    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+    if (p->ev_join) cudaEventDestroy(p->ev_join);
     delete p;
 }
 
@@ -490,6 +512,9 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
             p->kA = dalloc(p, img * rs);
             p->kB = dalloc(p, img * rs);
         }
+        CK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
         CK(cudaMemset(p->yg, 0, img * cs));
         CK(cudaMemset(p->pinv, 0, img * rs));
         if (precision == VDAMP_FP32) {

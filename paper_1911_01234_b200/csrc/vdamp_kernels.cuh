@@ -1302,7 +1302,7 @@ __global__ void __launch_bounds__(NT, NT == SNT ? 1 : 4) sure_select(Geo g, SelA
     extern __shared__ __align__(16) unsigned char smem_raw[];
     R* keys = reinterpret_cast<R*>(smem_raw);
     __shared__ SelShared<NT> S_;
-    const int it = blockIdx.x, bi = blockIdx.y;
+    const int bi = blockIdx.x, it = blockIdx.y;     // images fastest: long items of all images start first
     // one work item = one large subband, or several small ones packed to ~SCAP keys
     for (int q = a.item_start[it]; q < a.item_start[it + 1]; ++q) {
         select_band<R, NT>(g, a, a.item_list[q], bi, keys, S_);
