@@ -135,6 +135,12 @@ VDAMP_API int vdamp_denoise_colored(vdamp_plan_t plan, const void* r, const doub
 VDAMP_API int vdamp_set_timing(vdamp_plan_t plan, int enable);
 /* Synchronises the recorded events; ms[c] = summed device time, launches[c] = count. */
 VDAMP_API int vdamp_kernel_times(vdamp_plan_t plan, double* ms, int64_t* launches);
+/* vdamp_run captures its whole launch sequence as a CUDA graph (default: on for
+ * plans of at most 8 x 256^2 pixels, where launches are short; env VDAMP_GRAPHS=0/1
+ * overrides) and replays it while the outputs, iteration count,
+ * stream and flags are unchanged.  With timing enabled each graph run synchronises
+ * once to accumulate the kernel times. */
+VDAMP_API int vdamp_set_graphs(vdamp_plan_t plan, int enable);
 /* total kernel launches issued by this plan since creation or the last reset */
 VDAMP_API int vdamp_launch_count(vdamp_plan_t plan, int64_t* count, int reset);
 

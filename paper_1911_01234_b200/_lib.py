@@ -52,6 +52,7 @@ SIGNATURES = {
     "vdamp_denoise_colored": (_I, [_P, _P, _P, _P, _P, _P]),
     "vdamp_set_timing": (_I, [_P, _I]),
     "vdamp_kernel_times": (_I, [_P, _DP, _I64P]),
+    "vdamp_set_graphs": (_I, [_P, _I]),
     "vdamp_launch_count": (_I, [_P, _I64P, _I]),
 }
 

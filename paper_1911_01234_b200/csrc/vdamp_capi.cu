@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -73,6 +74,15 @@ struct Plan {
     void* xtmp = nullptr;           // per-iteration finalize image (NMSE)
     double* trtmp = nullptr;        // [B][S][TRACE_F]
     cudaStream_t side = nullptr;    // fork/join stream for the small-subband SURE kernel
+    // CUDA graph of the whole vdamp_run sequence, re-captured when its key changes
+    bool graphs = true;
+    cudaGraphExec_t gexec = nullptr;
+    std::vector<const void*> gkey;
+    long long g_launches = 0;
+    long long g_cls[VDAMP_KERNEL_CLASSES] = {0};
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> gev;   // timing events inside the graph
+    cudaStream_t gstream = nullptr; // capture/launch stream when the caller passes the legacy default stream
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool have_meas = false;
     bool have_gt = false;
@@ -101,6 +111,14 @@ int ilog2(long long v) { int l = 0; while ((1LL << l) < v) ++l; return l; }
 bool pow2(long long v) { return v > 0 && (v & (v - 1)) == 0; }
 
 // ---------------------------------------------------------------- launch --
+// event record that also works inside stream capture (a real record node)
+inline cudaError_t record(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                                               : cudaEventRecord(e, s);
+}
+
 struct Launch {
     Plan* p;
     int cls;
@@ -111,14 +129,14 @@ struct Launch {
             cudaEvent_t e1;
             CK(cudaEventCreate(&e0));
             CK(cudaEventCreate(&e1));
-            CK(cudaEventRecord(e0, st));
+            CK(record(e0, st));
             p->ev.push_back({cls, {e0, e1}});
         }
     }
     ~Launch() {
         p->launches++;
         p->cls_launches[cls]++;
-        if (p->timing) cudaEventRecord(p->ev.back().second.second, st);
+        if (p->timing) record(p->ev.back().second.second, st);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess && p->pend == cudaSuccess) p->pend = e;
     }
@@ -126,6 +144,26 @@ struct Launch {
 
 // Opt every kernel into the dynamic shared memory it is launched with (static
 // shared memory counts against the default 48 KB too), once per kernel/size.
+// add the elapsed times of recorded event pairs to the per-class totals
+void accumulate(Plan* p, std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>& ev, bool destroy) {
+    for (auto& e : ev) {
+        CK(cudaEventSynchronize(e.second.second));
+        float t = 0;
+        CK(cudaEventElapsedTime(&t, e.second.first, e.second.second));
+        p->ms[e.first] += t;
+        if (destroy) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
+    }
+    if (destroy) ev.clear();
+}
+
+void drop_graph(Plan* p) {
+    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    p->gexec = nullptr;
+    p->gkey.clear();
+    for (auto& e : p->gev) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
+    p->gev.clear();
+}
+
 template <typename K>
 void set_smem(K kern, size_t bytes) {
     static thread_local std::vector<std::pair<const void*, size_t>> done;
@@ -392,7 +430,11 @@ void free_plan(Plan* p) {
     for (void* b : bufs) if (b) cudaFree(b);
     for (void* b : p->scratch) if (b) cudaFree(b);
     for (auto& e : p->ev) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
+    drop_graph(p);
     if (p->side) cudaStreamDestroy(p->side);
+    if (p->gstream) cudaStreamDestroy(p->gstream);
+    if (p->ev_in) cudaEventDestroy(p->ev_in);
+    if (p->ev_out) cudaEventDestroy(p->ev_out);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);
     delete p;
@@ -513,6 +555,13 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
             p->kB = dalloc(p, img * rs);
         }
         CK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&p->gstream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
+        // graphs pay off when launches are short (small batches); large batches are
+        // GPU-bound and measured slightly faster with direct launches (round 1, cfg1)
+        p->graphs = (long long)batch * p->N <= 8LL * 65536;
+        if (const char* ge = getenv("VDAMP_GRAPHS")) p->graphs = atoi(ge) != 0;
         CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
         CK(cudaMemset(p->yg, 0, img * cs));
@@ -621,10 +670,81 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
         if (!p->have_meas) throw Err{VDAMP_ERR_STATE, "vdamp_set_measurements must be called first"};
         if (nmse && !p->have_gt) throw Err{VDAMP_ERR_STATE, "NMSE trace requested without ground truth"};
         if (!x_hat) throw Err{VDAMP_ERR_ARG, "null x_hat"};
-        dispatch(p, stream, [&](auto& s) {
-            typedef typename std::remove_reference<decltype(s)>::type S_;
-            s.run(n_iters, (typename S_::C*)x_hat, trace, nmse, snapshots);
-        });
+        cudaStream_t caller = (cudaStream_t)stream;
+        cudaStream_t st = caller;
+        if (!p->graphs) {
+            dispatch(p, stream, [&](auto& s) {
+                typedef typename std::remove_reference<decltype(s)>::type S_;
+                s.run(n_iters, (typename S_::C*)x_hat, trace, nmse, snapshots);
+            });
+            return;
+        }
+        // the legacy default stream cannot be captured: run on the plan's stream,
+        // ordered after / before the caller's work by events
+        const bool hop = (caller == nullptr || caller == cudaStreamLegacy || caller == cudaStreamPerThread);
+        if (hop) {
+            st = p->gstream;
+            CK(cudaEventRecord(p->ev_in, caller));
+            CK(cudaStreamWaitEvent(st, p->ev_in, 0));
+        }
+        void* sarg = (void*)st;
+        // key: everything baked into the captured launches
+        std::vector<const void*> key{(const void*)(intptr_t)n_iters, x_hat, trace, nmse, (const void*)(intptr_t)p->have_gt,
+                                     (const void*)(intptr_t)p->timing, (const void*)st};
+        if (snapshots) for (int k = 0; k < n_iters; ++k) key.push_back(snapshots[k]);
+        else key.push_back(nullptr);
+        if (!p->gexec || key != p->gkey) {
+            drop_graph(p);
+            CK(cudaSetDevice(p->dev));
+            // capture: launches and timing events recorded during capture belong to the graph
+            const long long l0 = p->launches;
+            long long c0[VDAMP_KERNEL_CLASSES];
+            for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) c0[c] = p->cls_launches[c];
+            std::swap(p->ev, p->gev);          // Launch appends to p->ev: collect the graph's events
+            p->ev.clear();
+            CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            bool ok = true;
+            try {
+                dispatch(p, sarg, [&](auto& s) {
+                    typedef typename std::remove_reference<decltype(s)>::type S_;
+                    s.run(n_iters, (typename S_::C*)x_hat, trace, nmse, snapshots);
+                });
+            } catch (...) { ok = false; }
+            cudaGraph_t graph = nullptr;
+            cudaError_t ec = cudaStreamEndCapture(st, &graph);
+            std::swap(p->ev, p->gev);          // p->gev = graph events, p->ev = previous one-shot events
+            if (!ok || ec != cudaSuccess) {
+                if (graph) cudaGraphDestroy(graph);
+                p->graphs = false;             // fall back to direct launches for this plan
+                drop_graph(p);
+                p->launches = l0;
+                for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) p->cls_launches[c] = c0[c];
+                cudaGetLastError();
+                dispatch(p, sarg, [&](auto& s) {
+                    typedef typename std::remove_reference<decltype(s)>::type S_;
+                    s.run(n_iters, (typename S_::C*)x_hat, trace, nmse, snapshots);
+                });
+                if (hop) {
+                    CK(cudaEventRecord(p->ev_out, st));
+                    CK(cudaStreamWaitEvent(caller, p->ev_out, 0));
+                }
+                return;
+            }
+            CK(cudaGraphInstantiate(&p->gexec, graph, 0));
+            cudaGraphDestroy(graph);
+            p->gkey = key;
+            p->g_launches = p->launches - l0;
+            for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) { p->g_cls[c] = p->cls_launches[c] - c0[c]; p->cls_launches[c] = c0[c]; }
+            p->launches = l0;
+        }
+        CK(cudaGraphLaunch(p->gexec, st));
+        if (hop) {
+            CK(cudaEventRecord(p->ev_out, st));
+            CK(cudaStreamWaitEvent(caller, p->ev_out, 0));
+        }
+        p->launches += p->g_launches;
+        for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) p->cls_launches[c] += p->g_cls[c];
+        if (p->timing && !p->gev.empty()) accumulate(p, p->gev, false);   // graph events are reused per replay
     });
 }
 
@@ -721,6 +841,7 @@ int vdamp_set_timing(vdamp_plan_t plan, int enable) {
         p->timing = enable != 0;
         for (auto& e : p->ev) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
         p->ev.clear();
+        drop_graph(p);
         for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) { p->ms[c] = 0; p->cls_launches[c] = 0; }
     });
 }
@@ -728,15 +849,7 @@ int vdamp_set_timing(vdamp_plan_t plan, int enable) {
 int vdamp_kernel_times(vdamp_plan_t plan, double* ms, int64_t* launches) {
     return guard([&] {
         Plan* p = P(plan);
-        for (auto& e : p->ev) {
-            CK(cudaEventSynchronize(e.second.second));
-            float t = 0;
-            CK(cudaEventElapsedTime(&t, e.second.first, e.second.second));
-            p->ms[e.first] += t;
-            cudaEventDestroy(e.second.first);
-            cudaEventDestroy(e.second.second);
-        }
-        p->ev.clear();
+        accumulate(p, p->ev, true);
         for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) {
             if (ms) ms[c] = p->ms[c];
             if (launches) launches[c] = p->cls_launches[c];
@@ -753,6 +866,14 @@ extern "C" VDAMP_API int vdamp_debug_csort_times(long long* out, int images) {
     return guard([&] { CK(cudaMemcpyFromSymbol(out, g_csort, (size_t)images * 64 * 6 * sizeof(long long))); });
 }
 #endif
+
+int vdamp_set_graphs(vdamp_plan_t plan, int enable) {
+    return guard([&] {
+        Plan* p = P(plan);
+        p->graphs = enable != 0;
+        drop_graph(p);
+    });
+}
 
 int vdamp_launch_count(vdamp_plan_t plan, int64_t* count, int reset) {
     return guard([&] {

@@ -184,6 +184,9 @@ class Plan:
         _lib.check(_lib.load().vdamp_kernel_times(self.handle, ms, n))
         return {name: (float(ms[i]), int(n[i])) for i, name in enumerate(_lib.KERNEL_CLASS_NAMES)}
 
+    def set_graphs(self, enable: bool):
+        _lib.check(_lib.load().vdamp_set_graphs(self.handle, int(bool(enable))))
+
     def launch_count(self, reset=False) -> int:
         v = ctypes.c_int64()
         _lib.check(_lib.load().vdamp_launch_count(self.handle, ctypes.byref(v), int(bool(reset))))
