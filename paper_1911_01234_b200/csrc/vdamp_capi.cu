@@ -71,7 +71,11 @@ struct Plan {
     void* kB = nullptr;
     void* x0 = nullptr;             // ground truth image (owned copy)
     void* w0 = nullptr;             // dwt(x0)
-    void* xtmp = nullptr;           // per-iteration finalize image (NMSE)
+    void* xtmp = nullptr;           // per-iteration finalize image (NMSE, direct path)
+    void* x0r = nullptr;            // raw unitary FFT2 of s_in * x0 (Parseval NMSE)
+    double* nmconst = nullptr;      // [B][2]: mask error constant, |x0|^2
+    double* nmpart = nullptr;       // [B][ntiles]
+    bool parseval = true;           // per-iteration NMSE by Parseval (one forward FFT)
     double* trtmp = nullptr;        // [B][S][TRACE_F]
     cudaStream_t side = nullptr;    // fork/join stream for the small-subband SURE kernel
     // CUDA graph of the whole vdamp_run sequence, re-captured when its key changes
@@ -180,6 +184,7 @@ void set_smem(K kern, size_t bytes) {
 template <typename R>
 struct Seq {
     typedef typename CT<R>::T C;
+    typedef R Rt;
     Plan* p;
     cudaStream_t st;
     cudaStream_t& st_ = st;
@@ -268,6 +273,7 @@ struct Seq {
         a.yg = (const C*)p->yg; a.pinv = (const R*)p->pinv; a.noise_var = p->nvar;
         a.prow = p->prow; a.pcol = p->pcol; a.taupart = p->taupart;
         a.tw = (const C*)p->twH; a.cw = p->cw; a.logcw = p->logcw; a.ntiles = p->ntiles;
+        a.x0r = (const C*)p->x0r; a.nmsepart = p->nmpart;
         dim3 grid(p->ntiles, p->B);
         const size_t sm = col_smem();
         Launch L(p, cls, st);
@@ -275,6 +281,8 @@ struct Seq {
             case COL_FWD:   { auto k = col_pass<R, COL_FWD>;   set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
             case COL_INV:   { auto k = col_pass<R, COL_INV>;   set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
             case COL_VDAMP: { auto k = col_pass<R, COL_VDAMP>; set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
+            case COL_RAW:   { auto k = col_pass<R, COL_RAW>;   set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
+            case COL_NMSE:  { auto k = col_pass<R, COL_NMSE>;  set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
             default:        { auto k = col_pass<R, COL_FINAL>; set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
         }
     }
@@ -380,11 +388,27 @@ struct Seq {
         CK(cudaMemsetAsync(p->r, 0, (size_t)p->B * p->N * sizeof(C), st));   // r~_0 = 0
         identity_params();
         const long long tstride = (long long)p->B * p->S * TRACE_F;
+        if (nmse_out && p->parseval) {
+            // per-run Parseval constants: sum_mask |y - F x0|^2 and |x0|^2
+            Launch L(p, 5, st);
+            nmse_setup<R><<<p->B, SNT, 0, st>>>(p->geo, (const C*)p->yg, (const R*)p->pinv, (const C*)p->x0r,
+                                                (const C*)p->x0, p->nmconst);
+        }
         for (int it = 0; it < n_iters; ++it) {
             iteration(trace ? trace + it * tstride : nullptr, snaps ? snaps[it] : nullptr);
             if (nmse_out) {
-                finalize_from_r(p->parf, (C*)p->xtmp);
-                nmse((const C*)p->xtmp, nmse_out + (long long)it * p->B * VDAMP_NMSE_FIELDS);
+                double* rec = nmse_out + (long long)it * p->B * VDAMP_NMSE_FIELDS;
+                if (p->parseval) {
+                    // x_hat_k = finalize(soft(r_k)): F x_hat is y on the mask and
+                    // F Psi^H w_hat elsewhere, so one forward FFT suffices
+                    synth(r(), p->parf, true, nullptr, 4);
+                    col(COL_NMSE, (const C*)p->T1, nullptr, 4);
+                    Launch L(p, 5, st);
+                    nmse_finish<<<(p->B + 127) / 128, 128, 0, st>>>(p->nmpart, p->ntiles, p->nmconst, rec, p->B);
+                } else {
+                    finalize_from_r(p->parf, (C*)p->xtmp);
+                    nmse((const C*)p->xtmp, rec);
+                }
             }
         }
         finalize_from_r(p->parf, xhat);
@@ -425,7 +449,7 @@ void dispatch(Plan* p, void* stream, F&& f) {
 void free_plan(Plan* p) {
     if (!p) return;
     cudaSetDevice(p->dev);
-    void* bufs[] = {p->r, p->T1, p->T2, p->yg, p->pinv, p->par, p->parf, p->taupart, p->prow, p->pcol,
+    void* bufs[] = {p->x0r, p->nmconst, p->nmpart, p->r, p->T1, p->T2, p->yg, p->pinv, p->par, p->parf, p->taupart, p->prow, p->pcol,
                     p->nvar, p->offs, p->twH, p->twW, p->kA, p->kB, p->x0, p->w0, p->xtmp, p->trtmp};
     for (void* b : bufs) if (b) cudaFree(b);
     for (void* b : p->scratch) if (b) cudaFree(b);
@@ -561,6 +585,7 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         // graphs pay off when launches are short (small batches); large batches are
         // GPU-bound and measured slightly faster with direct launches (round 1, cfg1)
         p->graphs = (long long)batch * p->N <= 8LL * 65536;
+        if (const char* pe = getenv("VDAMP_PARSEVAL")) p->parseval = atoi(pe) != 0;
         if (const char* ge = getenv("VDAMP_GRAPHS")) p->graphs = atoi(ge) != 0;
         CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
@@ -651,12 +676,20 @@ int vdamp_set_ground_truth(vdamp_plan_t plan, const void* x0, void* stream) {
         if (!x0) { p->have_gt = false; return; }
         CK(cudaSetDevice(p->dev));
         const size_t bytes = (size_t)p->B * p->N * p->csz;
-        if (!p->x0) { p->x0 = dalloc(p, bytes); p->w0 = dalloc(p, bytes); p->xtmp = dalloc(p, bytes); }
+        if (!p->x0) {
+            p->x0 = dalloc(p, bytes); p->w0 = dalloc(p, bytes); p->xtmp = dalloc(p, bytes); p->x0r = dalloc(p, bytes);
+            p->nmconst = (double*)dalloc(p, (size_t)p->B * 2 * sizeof(double));
+            p->nmpart = (double*)dalloc(p, (size_t)p->B * p->ntiles * sizeof(double));
+        }
         CK(cudaMemcpyAsync(p->x0, x0, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
         dispatch(p, stream, [&](auto& s) {
             typedef typename std::remove_reference<decltype(s)>::type S_;
             typedef typename S_::C C;
+            typedef typename S_::Rt R;
             s.analysis((const C*)p->x0, false, (C*)p->w0, nullptr, false, 5);
+            // X0r = FFT2u(s_in x0) and the per-run Parseval constants (needs measurements)
+            s.template rows<false, true, false>((const C*)p->x0, (C*)p->T1, 5);
+            s.col(COL_RAW, (const C*)p->T1, (C*)p->x0r, 5);
         });
         p->have_gt = true;
     });

@@ -433,7 +433,9 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) analysis_pass(Geo
 }
 
 // ------------------------------------------------------------------ K2 ----
-enum { COL_FWD = 0, COL_INV = 1, COL_VDAMP = 2, COL_FINAL = 3 };
+// COL_RAW: forward column FFT without the centring sign (X0 setup);
+// COL_NMSE: forward column FFT + Parseval error vs X0 off the mask (no IFFT)
+enum { COL_FWD = 0, COL_INV = 1, COL_VDAMP = 2, COL_FINAL = 3, COL_RAW = 4, COL_NMSE = 5 };
 
 template <typename R>
 struct ColArgs {
@@ -447,6 +449,8 @@ struct ColArgs {
     double* taupart;                 // [B][ntiles][S]
     const typename CT<R>::T* tw;     // length H
     int cw, logcw, ntiles;
+    const typename CT<R>::T* x0r;    // COL_NMSE: raw unitary FFT2 of s_in * x0
+    double* nmsepart;                // COL_NMSE: [B][ntiles] error partials
 };
 
 __device__ __forceinline__ void band_profiles(int s, int j, int& prow, int& pcol) {
@@ -493,6 +497,27 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass(Geo g, C
             const R s = (((n + col) & 1) ? -sc : sc) * (R)g.sign_c;
             p.dst[ib + (long long)n * W + col] = cscale(buf[e], s);
         }
+        return;
+    }
+    if (MODE == COL_RAW) {
+        for (int e = tid; e < E; e += PNT)
+            p.dst[ib + (long long)(e >> lc) * W + c0 + (e & (cw - 1))] = cscale(buf[e], sc);
+        return;
+    }
+    if (MODE == COL_NMSE) {
+        // ||x_hat - x0||^2 off the mask = sum |F Psi^H w - F x0|^2 (Parseval; on the
+        // mask x_hat has exactly y, that part is a per-run constant)
+        double e2 = 0.0;
+        for (int e = tid; e < E; e += PNT) {
+            const long long gi = ib + (long long)(e >> lc) * W + c0 + (e & (cw - 1));
+            if (p.pinv[gi] == R(0)) {
+                const C d = csub(cscale(buf[e], sc), p.x0r[gi]);
+                e2 += (double)d.x * (double)d.x + (double)d.y * (double)d.y;
+            }
+        }
+        double* sh = reinterpret_cast<double*>(tws + H);
+        e2 = block_sum<PNT>(e2, sh);
+        if (tid == 0) p.nmsepart[(long long)bi * p.ntiles + tile] = e2;
         return;
     }
     const R cs = (R)g.sign_c;
@@ -1373,6 +1398,41 @@ __global__ void make_profiles(double* prof, int L, int s) {
         }
         prof[(long long)pidx * L + w] = (re * re + im * im) / (double)L;
     }
+}
+
+// Parseval NMSE constants per image: E_mask = sum over the mask of |y - F x0|^2
+// (= |y' - c X0r|^2 in the sign-folded convention) and |x0|^2.
+template <typename R>
+__global__ void __launch_bounds__(SNT) nmse_setup(Geo g, const typename CT<R>::T* yg, const R* pinv,
+                                                  const typename CT<R>::T* x0r, const typename CT<R>::T* x0,
+                                                  double* consts) {
+    __shared__ double sh[SNT / 32 + 2];
+    const int bi = blockIdx.x;
+    const long long base = (long long)bi * g.N;
+    const double c = (double)g.sign_c;
+    double e = 0.0, r = 0.0;
+    for (long long i = threadIdx.x; i < g.N; i += SNT) {
+        if (pinv[base + i] != R(0)) {
+            const typename CT<R>::T a = yg[base + i], b = x0r[base + i];
+            const double dx = (double)a.x - c * (double)b.x, dy = (double)a.y - c * (double)b.y;
+            e += dx * dx + dy * dy;
+        }
+        const typename CT<R>::T v = x0[base + i];
+        r += (double)v.x * (double)v.x + (double)v.y * (double)v.y;
+    }
+    e = block_sum<SNT>(e, sh);
+    r = block_sum<SNT>(r, sh);
+    if (threadIdx.x == 0) { consts[2 * bi] = e; consts[2 * bi + 1] = r; }
+}
+
+// per-iteration NMSE record from the column-tile partials (fixed order)
+__global__ void nmse_finish(const double* part, int ntiles, const double* consts, double* out, int B) {
+    const int bi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (bi >= B) return;
+    double e = consts[2 * bi];
+    for (int t = 0; t < ntiles; ++t) e += part[(long long)bi * ntiles + t];
+    out[2 * bi] = e;
+    out[2 * bi + 1] = consts[2 * bi + 1];
 }
 
 // per-image |x - x0|^2 and |x0|^2 (src/diagnostics.py:21-34), deterministic

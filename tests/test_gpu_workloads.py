@@ -167,3 +167,21 @@ def test_graph_replay_matches_direct(cfg0_small):
     captured = run()                              # capture + first launch
     replayed = run()                              # replay of the cached graph
     assert np.array_equal(direct, captured) and np.array_equal(captured, replayed)
+
+
+def test_parseval_nmse_matches_finalize_path(cfg0_small):
+    """Per-iteration NMSE by Parseval (one forward FFT) equals the
+    finalize-then-compare path of src/vdamp.py:189-192 to round-off."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); "
+            "from paper_1911_01234_b200 import vdamp, workload; w = workload.make_workload('cfg1', batch=2); "
+            "_, tr = vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, 4, 8, ground_truths=w.x0, precision='fp64'); "
+            "print(repr([list(t.nmse_curve()) for t in tr]))") % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for v in ("1", "0"):
+        env = dict(os.environ, VDAMP_PARSEVAL=v)
+        res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True)
+        out[v] = np.array(eval(res.stdout.strip().splitlines()[-1]))
+    assert np.abs(out["1"] - out["0"]).max() <= 1e-8
