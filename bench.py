@@ -176,6 +176,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="print a short human summary instead of JSON")
+    ap.add_argument("--with-trace", action="store_true",
+                    help="time the production trace path: ground truth set, per-iteration NMSE + trace records")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -252,7 +254,18 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    trace_buf = nmse_buf = None
+    if args.with_trace:
+        plan.set_measurements(dev_in["y"], dev_in["indices"], dev_in["counts"], dev_in["probs"], dev_in["noise_var"], True)
+        plan.set_ground_truth(torch.from_numpy(w.x0).to(dev, cd))
+        trace_buf = plan.new_trace(cfg.n_iters)
+        nmse_buf = torch.zeros((cfg.n_iters, B, 2), dtype=torch.float64, device=dev)
+
     def step():
+        if args.with_trace:
+            plan.set_measurements(dev_in["y"], dev_in["indices"], dev_in["counts"], dev_in["probs"],
+                                  dev_in["noise_var"], True)
+            return plan.run(cfg.n_iters, x_hat=rec._x, trace=trace_buf, nmse=nmse_buf)
         return rec(dev_in["y"], dev_in["indices"], dev_in["counts"], dev_in["probs"], dev_in["noise_var"],
                    cfg.n_iters, shared_probs=True, sync=False)
 
@@ -333,6 +346,7 @@ def main():
                                f"R={cfg.undersampling:g}, {cfg.snr_db:g} dB, {cfg.n_iters} iterations",
                    "images_per_gpu": B, "n_iters": cfg.n_iters, "precision": args.precision,
                    "l2": "flushed between timed steps (256 MiB write, untimed)",
+                   "trace": "ground truth + per-iteration NMSE/trace records" if args.with_trace else "off (as the CPU timing)",
                    "parallelism": f"images sharded, {world} process(es), 1 GPU each, no collective"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
