@@ -330,7 +330,8 @@ struct Seq {
             if (big) {
                 const int cap = Scap<R>::v;
                 const size_t slots = (size_t)(cap + cap / 32 + 1) + 1;
-                size_t sm = sizeof(R) == 4 ? 2 * (slots + 1) * sizeof(R) + (CS_BUCKETS / 2) * sizeof(unsigned)
+                const size_t slot16 = ((size_t)cap + cap / 32 + 2 + 3) & ~(size_t)3;   // kernel's SLOT
+                size_t sm = sizeof(R) == 4 ? 2 * slot16 * sizeof(R) + (CS_BUCKETS / 2) * sizeof(unsigned)
                                            : slots * sizeof(R);
                 // large subbands: global counting sort counters + ranking tile
                 const size_t gcs = sizeof(R) == 4 ? 32768 * 4 + 16384 * sizeof(R) : 8192 * 4 + 8192 * sizeof(R);

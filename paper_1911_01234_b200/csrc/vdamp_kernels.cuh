@@ -1124,6 +1124,8 @@ __device__ long long g_phase[4096][64][4];
 
 template <int NT>
 struct SelShared {
+    unsigned long long mbar;         // TMA completion barrier (fp32 big-subband path)
+    unsigned mphase;
     double sh[66 + NT / 32 + 2];     // counting-sort min/max words + block scans
     double tsq[MAXTILES], tinv[MAXTILES], tpre[MAXTILES], tsuf[MAXTILES];
     double tpart[MAXCT];             // tau partials of the column tiles
@@ -1163,11 +1165,55 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
     const int ntl = large ? n / CAPK : 1;
     const R* sorted = keys;
     // fp32: counting sort from the staging buffer `stage` into `keys`
-    R* stage = keys + KI(CAPK) + 2;
-    unsigned* ccnt = reinterpret_cast<unsigned*>(stage + KI(CAPK) + 2);
+    constexpr int SLOT = (CAPK + CAPK / 32 + 2 + 3) & ~3;          // padded keys, 16-byte aligned stride
+    R* stage = keys + SLOT;
+    unsigned* ccnt = reinterpret_cast<unsigned*>(stage + SLOT);
     const bool csort = NT == SNT && sizeof(R) == 4 && T >= 4096;
-    if (!large) {
-        R* dstk = csort ? stage : keys;
+    R* skeys = keys;                                               // where the sorted keys end up
+    if (!large && csort) {
+        // TMA: the subband is one contiguous segment of r; bulk-copy it into the
+        // stage+counter region (free at this point), then build the keys from smem
+        C* cz = reinterpret_cast<C*>(stage);
+        const unsigned bytes = (unsigned)T * (unsigned)sizeof(C);
+        __syncthreads();                                           // previous users of the region are done
+        if (tid == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(&S_.mbar, bytes);
+            for (unsigned o = 0; o < bytes; o += 32768u)
+                bulk_g2s(reinterpret_cast<char*>(cz) + o, reinterpret_cast<const char*>(rs) + o,
+                         bytes - o < 32768u ? bytes - o : 32768u, &S_.mbar);
+        }
+        mbar_wait(&S_.mbar, S_.mphase);
+        for (int e = tid; e < T; e += NT) {
+            const C v = cz[e];
+            keys[KI(e)] = cmag(v);
+            if (w0) {
+                const C w = w0[e];
+                const double dx = (double)v.x - (double)w.x, dy = (double)v.y - (double)w.y;
+                err += dx * dx + dy * dy;
+                ref += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) S_.mphase ^= 1u;
+        if (!a.tau_in && tid == 0) {
+            double t = 0.0;
+            for (int i = 0; i < a.ntiles; ++i) t += S_.tpart[i];
+            s_tau = t;
+        }
+        if constexpr (NT == SNT) {
+#ifdef VDAMP_PHASE_TIMING
+            long long* dbg = (bi < 4096) ? &g_csort[bi][j][0] : nullptr;
+#else
+            long long* dbg = nullptr;
+#endif
+            if (counting_sort(reinterpret_cast<const float*>(keys), reinterpret_cast<float*>(stage), ccnt, T, sh, dbg))
+                skeys = stage;
+            else
+                block_sort<R, NT>(keys, T);
+        }
+    } else if (!large) {
+        R* dstk = keys;
         // issue 8 independent loads per thread before using any (memory-level parallelism)
         constexpr int LB = 8;
         for (int e0 = tid; e0 < T; e0 += LB * NT) {
@@ -1201,22 +1247,7 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             for (int i = 0; i < a.ntiles; ++i) t += S_.tpart[i];
             s_tau = t;
         }
-        if constexpr (NT == SNT) {
-#ifdef VDAMP_PHASE_TIMING
-            long long* dbg = (bi < 4096) ? &g_csort[bi][j][0] : nullptr;
-#else
-            long long* dbg = nullptr;
-#endif
-            bool done = false;
-            if (csort) done = counting_sort(reinterpret_cast<const float*>(stage), reinterpret_cast<float*>(keys), ccnt, T, sh, dbg);
-            if (csort && !done) {
-                for (int e = tid; e < T; e += NT) keys[KI(e)] = stage[KI(e)];
-                __syncthreads();
-            }
-            if (!done) block_sort<R, NT>(keys, T);
-        } else {
-            block_sort<R, NT>(keys, T);
-        }
+        block_sort<R, NT>(keys, T);
     } else {
         // whole subband -> global scratch keys, counting sort there (L2-resident)
         R* ka = a.kA + base;
@@ -1274,13 +1305,13 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             __syncthreads();
         }
         const double nf = (t + 1 < ntl) ? (double)sorted[(t + 1) * CAPK] : INFINITY;
-        scan_tile<R, NT>(keys, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, best, &s_totinv);
+        scan_tile<R, NT>(large ? keys : skeys, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, best, &s_totinv);
     }
     // candidate t = 0 when no magnitude is zero (src/denoise.py:84)
     __syncthreads();
     __syncthreads();
     if (tid == 0) {
-        const double m0 = large ? (double)sorted[0] : (double)keys[0];
+        const double m0 = large ? (double)sorted[0] : (double)skeys[0];
         if (m0 > 0) {
             const double totinv = s_totinv;
             const double nn = (double)n;
@@ -1328,6 +1359,8 @@ __global__ void __launch_bounds__(NT, NT == SNT ? 1 : 4) sure_select(Geo g, SelA
     R* keys = reinterpret_cast<R*>(smem_raw);
     __shared__ SelShared<NT> S_;
     const int bi = blockIdx.x, it = blockIdx.y;     // images fastest: long items of all images start first
+    if (threadIdx.x == 0) { mbar_init(&S_.mbar, 1); S_.mphase = 0; }
+    __syncthreads();
     // one work item = one large subband, or several small ones packed to ~SCAP keys
     for (int q = a.item_start[it]; q < a.item_start[it + 1]; ++q) {
         select_band<R, NT>(g, a, a.item_list[q], bi, keys, S_);
