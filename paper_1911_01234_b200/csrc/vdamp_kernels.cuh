@@ -781,7 +781,8 @@ __device__ void block_sort(R* s, int n) {
 // zeros go to bucket 0.  Histogram and scatter use packed 16-bit shared
 // counters; the scatter order inside a bucket is arbitrary, so every bucket
 // is finished by an insertion sort on the full key.  The sorted sequence is
-// unique, so the result is deterministic.  out must not alias keys.
+// unique, so the result is deterministic.  `out` is scratch (must not alias
+// keys); on success the sorted keys are back in `keys`.
 // ---------------------------------------------------------------------------
 constexpr int CS_BUCKETS = 32768;
 
@@ -884,8 +885,8 @@ __device__ bool counting_sort(const float* keys, float* out, unsigned* cnt, int 
     // finish every bucket in parallel: the final slot of key x at grouped position
     // i is start(b) + #{y in b : y < x} + #{y in b : y == x, pos(y) < i}.  Threads
     // of a warp mostly share a bucket, so the smem reads broadcast.  The grouped
-    // keys live in `ob`; the ranked result is written back into the staging
-    // buffer (free by now) and copied to `out`.
+    // keys live in `ob`; the sorted result is written into the input buffer
+    // (consumed by now): on success the keys come back sorted IN PLACE.
     unsigned* fb = const_cast<unsigned*>(kb);
     for (int i = tid; i < n; i += SNT) {
         const unsigned x = ob[KI(i)];
@@ -900,8 +901,6 @@ __device__ bool counting_sort(const float* keys, float* out, unsigned* cnt, int 
         }
         fb[KI(s0 + rank)] = x;
     }
-    __syncthreads();
-    for (int i = tid; i < n; i += SNT) ob[KI(i)] = fb[KI(i)];
     __syncthreads();
     CS_MARK(4);
     return true;
@@ -1207,9 +1206,7 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
 #else
             long long* dbg = nullptr;
 #endif
-            if (counting_sort(reinterpret_cast<const float*>(keys), reinterpret_cast<float*>(stage), ccnt, T, sh, dbg))
-                skeys = stage;
-            else
+            if (!counting_sort(reinterpret_cast<const float*>(keys), reinterpret_cast<float*>(stage), ccnt, T, sh, dbg))
                 block_sort<R, NT>(keys, T);
         }
     } else if (!large) {
