@@ -129,6 +129,15 @@ VDAMP_API int vdamp_finalize(vdamp_plan_t plan, const void* w_hat, void* x_hat, 
 VDAMP_API int vdamp_denoise_colored(vdamp_plan_t plan, const void* r, const double* tau, void* w_hat,
                           double* trace, void* stream);
 
+/* Monte Carlo accumulation over the batch (reference tests/conftest.py:41-81):
+ *   r       batch x N complex iterates r_k of one iteration k, one per draw
+ *   w0      N complex reference coefficients dwt(x0)
+ *   sum_r   N complex128 (float64 pairs), += sum over draws of r_b
+ *   sum_sq  S float64, += per-subband mean over entries of sum over draws |r_b - w0|^2
+ *   scratch N float64 workspace */
+VDAMP_API int vdamp_mc_accumulate(vdamp_plan_t plan, const void* r, const void* w0, double* sum_r,
+                                  double* sum_sq, double* scratch, void* stream);
+
 /* Instrumentation.  Kernel classes: 0 synthesis+row FFT, 1 column FFT/residual,
  * 2 row IFFT+analysis, 3 SURE select, 4 finalize, 5 other. */
 #define VDAMP_KERNEL_CLASSES 6

@@ -901,6 +901,35 @@ extern "C" VDAMP_API int vdamp_debug_csort_times(long long* out, int images) {
 }
 #endif
 
+int vdamp_mc_accumulate(vdamp_plan_t plan, const void* r, const void* w0, double* sum_r, double* sum_sq,
+                        double* scratch, void* stream) {
+    return guard([&] {
+        Plan* p = P(plan);
+        if (!r || !w0 || !sum_r || !sum_sq || !scratch) throw Err{VDAMP_ERR_ARG, "null Monte Carlo buffer"};
+        CK(cudaSetDevice(p->dev));
+        cudaStream_t st = (cudaStream_t)stream;
+        const unsigned grid = (unsigned)std::min<long long>((p->N + 255) / 256, 4096);
+        {
+            Launch L(p, 5, st);
+            if (p->prec == VDAMP_FP32)
+                mc_accumulate<float><<<grid, 256, 0, st>>>(p->geo, p->B, (const float2*)r, (const float2*)w0,
+                                                           (double2*)sum_r, scratch);
+            else
+                mc_accumulate<double><<<grid, 256, 0, st>>>(p->geo, p->B, (const double2*)r, (const double2*)w0,
+                                                            (double2*)sum_r, scratch);
+        }
+        {
+            Launch L(p, 5, st);
+            mc_band_sums<<<p->S, SNT, 0, st>>>(p->geo, scratch, sum_sq);
+        }
+        if (p->pend != cudaSuccess) {
+            cudaError_t e = p->pend;
+            p->pend = cudaSuccess;
+            throw Err{VDAMP_ERR_CUDA, std::string("mc_accumulate: ") + cudaGetErrorString(e)};
+        }
+    });
+}
+
 int vdamp_set_graphs(vdamp_plan_t plan, int enable) {
     return guard([&] {
         Plan* p = P(plan);

@@ -1465,6 +1465,36 @@ __global__ void nmse_finish(const double* part, int ntiles, const double* consts
     out[2 * bi + 1] = consts[2 * bi + 1];
 }
 
+// Monte Carlo accumulation over a batch of draws (tests/conftest.py:41-81 of the
+// reference): sum_r[i] += sum_b r_b[i]; err[i] = sum_b |r_b[i] - w0[i]|^2 (fixed
+// image order, deterministic).  Per-subband means are formed by mc_band_sums.
+template <typename R>
+__global__ void mc_accumulate(Geo g, int B, const typename CT<R>::T* r, const typename CT<R>::T* w0,
+                              double2* sum_r, double* err) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.N; i += (long long)gridDim.x * blockDim.x) {
+        const typename CT<R>::T w = w0[i];
+        double sx = 0.0, sy = 0.0, e = 0.0;
+        for (int b = 0; b < B; ++b) {
+            const typename CT<R>::T v = r[(long long)b * g.N + i];
+            sx += (double)v.x; sy += (double)v.y;
+            const double dx = (double)v.x - (double)w.x, dy = (double)v.y - (double)w.y;
+            e += dx * dx + dy * dy;
+        }
+        sum_r[i].x += sx; sum_r[i].y += sy;
+        err[i] = e;
+    }
+}
+
+// sum_sq[j] += (sum over subband j of err) / len_j   (one CTA per subband)
+__global__ void __launch_bounds__(SNT) mc_band_sums(Geo g, const double* err, double* sum_sq) {
+    __shared__ double sh[SNT / 32 + 2];
+    const int j = blockIdx.x;
+    double e = 0.0;
+    for (int i = threadIdx.x; i < g.len[j]; i += SNT) e += err[g.off[j] + i];
+    e = block_sum<SNT>(e, sh);
+    if (threadIdx.x == 0) sum_sq[j] += e / (double)g.len[j];
+}
+
 // per-image |x - x0|^2 and |x0|^2 (src/diagnostics.py:21-34), deterministic
 template <typename R>
 __global__ void __launch_bounds__(SNT) nmse_sums(Geo g, const typename CT<R>::T* x, const typename CT<R>::T* x0, double* out) {

@@ -126,10 +126,12 @@ def _records(trace_np, nmse_np, b, n_iters, wall):
 
 
 def run_batch(ys, masks, pmaps, noise_vars, scales, n_iters, ground_truths=None, keep_r_iters=(),
-              *, precision="fp64", device=None, return_tensor=False):
+              *, precision="fp64", device=None, return_tensor=False, keep_device=False):
     """VDAMP on a batch of independent images (one launch sequence for all).
 
-    Returns (x_hat (B, H, W) complex ndarray, [RunTrace per image]).
+    Returns (x_hat (B, H, W) complex ndarray, [RunTrace per image]).  With
+    ``keep_device`` the r snapshots stay on the device: ``traces[0].device_snapshots[k]``
+    is the (B, N) tensor of r_k (no per-image host copies).
     """
     import torch
     from .plan import get_plan
@@ -168,10 +170,12 @@ def run_batch(ys, masks, pmaps, noise_vars, scales, n_iters, ground_truths=None,
     traces = []
     for b in range(B):
         rt = RunTrace("vdamp", _records(trace_np, nmse_np, b, n_iters, wall), precompute)
-        if snaps:
+        if snaps and not keep_device:
             for k, t in snaps.items():
                 rt.r_snapshots[k] = WaveletCoeffs(t[b].cpu().numpy().astype(np.complex128), layout)
         traces.append(rt)
+    if keep_device and traces:
+        traces[0].device_snapshots = snaps or {}
     if return_tensor:
         return x, traces
     return x.cpu().numpy().astype(np.complex128), traces
