@@ -129,6 +129,16 @@ VDAMP_API int vdamp_finalize(vdamp_plan_t plan, const void* w_hat, void* x_hat, 
 VDAMP_API int vdamp_denoise_colored(vdamp_plan_t plan, const void* r, const double* tau, void* w_hat,
                           double* trace, void* stream);
 
+/* Baselines on the same kernels (src/baselines.py): algorithm 0 = FISTA with the
+ * global threshold lam[b] (device float64 [batch]); 1 = SURE-IT with the oracle
+ * tau_k = |r_k - w0|^2 / N (needs vdamp_set_ground_truth).  Set measurements with
+ * p = 1 (no density compensation).  x_hat = idwt(w_hat); trace (SURE-IT: tau, t,
+ * lambda, alpha per subband; FISTA: fields 6/7 = |w_hat - w0|^2, |w0|^2 per
+ * subband) and nmse ([n_iters][batch][2] of w_hat vs w0, = image NMSE since Psi
+ * is orthonormal) are optional. */
+VDAMP_API int vdamp_baseline_run(vdamp_plan_t plan, int algorithm, int n_iters, const double* lam, void* x_hat,
+                                 double* trace, double* nmse, void* stream);
+
 /* Monte Carlo accumulation over the batch (reference tests/conftest.py:41-81):
  *   r       batch x N complex iterates r_k of one iteration k, one per draw
  *   w0      N complex reference coefficients dwt(x0)

@@ -434,3 +434,82 @@ def run(y, idx, probs, noise_var, scales, n_iters, ground_truth=None,
         rt = st.r_tilde
     res.x_hat = finalize(st.w_hat, p)
     return res
+
+
+# --------------------------------------------------------------------------
+# Baselines on the same operators (src/baselines.py) -- SURVEY §8f row 3
+# --------------------------------------------------------------------------
+SURE_IT_TAU_FLOOR = 1e-30         # src/baselines.py:23
+
+
+def gradient_step(r_tilde, y, idx, shape, scales):
+    """r~ + Psi F^H M^T (y - M F Psi^H r~), unit step (src/baselines.py:41-43)."""
+    resid = y - forward(idwt(r_tilde, shape[0], shape[1], scales), idx)
+    return r_tilde + dwt(adjoint(resid, idx, shape), scales)
+
+
+def _momentum(t_m):
+    t_next = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * t_m * t_m))
+    return t_next, (t_m - 1.0) / t_next
+
+
+def fista(y, idx, shape, lam, n_iters, scales=4, ground_truth=None):
+    """Accelerated soft thresholding, one global threshold (src/baselines.py:54-91).
+    Returns (x_hat, nmse_curve or None)."""
+    if lam <= 0:
+        raise ValueError("lam must be > 0")
+    if n_iters < 1:
+        raise ValueError("need at least one iteration")
+    w_hat = np.zeros(shape[0] * shape[1], dtype=np.complex128)
+    rt = w_hat
+    t_m = 1.0
+    nm = []
+    for _ in range(n_iters):
+        g = gradient_step(rt, y, idx, shape, scales)
+        w_new = soft(g, lam)
+        t_m, beta = _momentum(t_m)
+        rt = w_new + beta * (w_new - w_hat)
+        w_hat = w_new
+        if ground_truth is not None:
+            nm.append(nmse_db(idwt(w_hat, shape[0], shape[1], scales), ground_truth))
+    return idwt(w_hat, shape[0], shape[1], scales), (nm if ground_truth is not None else None)
+
+
+def sure_it(y, idx, shape, w0, n_iters, scales=4, ground_truth=None):
+    """SURE-tuned thresholding with the oracle scalar error level (src/baselines.py:115-164).
+    Returns (x_hat, taus, thresholds, nmse_curve or None)."""
+    bands = band_table(shape[0], shape[1], scales)
+    N = shape[0] * shape[1]
+    w_hat = np.zeros(N, dtype=np.complex128)
+    rt = w_hat
+    t_m = 1.0
+    taus, thr, nm = [], [], []
+    for _ in range(n_iters):
+        r = gradient_step(rt, y, idx, shape, scales)
+        e = r - w0
+        tau_k = max(float(np.vdot(e, e).real) / N, SURE_IT_TAU_FLOOR)
+        tau = np.full(len(bands), tau_k)
+        w_new, _, lam, _ = denoise_colored(r, tau, bands)
+        t_m, beta = _momentum(t_m)
+        rt = w_new + beta * (w_new - w_hat)
+        w_hat = w_new
+        taus.append(tau)
+        thr.append(lam * tau)
+        if ground_truth is not None:
+            nm.append(nmse_db(idwt(w_hat, shape[0], shape[1], scales), ground_truth))
+    return (idwt(w_hat, shape[0], shape[1], scales), np.array(taus), np.array(thr),
+            nm if ground_truth is not None else None)
+
+
+def tune_lambda(y, idx, shape, x0, budget_iters, grid, scales=4):
+    """Smallest-NMSE threshold on a grid, ties keep the smaller (src/baselines.py:94-112)."""
+    grid = np.sort(np.asarray(grid, dtype=float))
+    if grid.size == 0:
+        raise ValueError("empty lambda grid")
+    best, best_nm = None, np.inf
+    for lam in grid:
+        x, _ = fista(y, idx, shape, float(lam), budget_iters, scales)
+        s = nmse_db(x, x0)
+        if s < best_nm:
+            best, best_nm = float(lam), s
+    return best

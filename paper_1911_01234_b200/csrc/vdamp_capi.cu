@@ -76,6 +76,9 @@ struct Plan {
     double* nmconst = nullptr;      // [B][2]: mask error constant, |x0|^2
     double* nmpart = nullptr;       // [B][ntiles]
     bool parseval = true;           // per-iteration NMSE by Parseval (one forward FFT)
+    void* what = nullptr;           // baselines: w_hat state [B][N]
+    double* btau = nullptr;         // baselines: [B][S] oracle tau
+    double* berr = nullptr;         // baselines: [B][S][2] coefficient errors
     double* trtmp = nullptr;        // [B][S][TRACE_F]
     cudaStream_t side = nullptr;    // fork/join stream for the small-subband SURE kernel
     // CUDA graph of the whole vdamp_run sequence, re-captured when its key changes
@@ -385,6 +388,49 @@ struct Seq {
         nmse_sums<R><<<p->B, SNT, 0, st>>>(p->geo, x, (const C*)p->x0, out);
     }
 
+    // FISTA (alg 0) / SURE-IT (alg 1) on the same kernels (src/baselines.py:54-164).
+    // The gradient step r~ + Psi F^H M^T (y - M F Psi^H r~) is K1/K2/K3 with identity
+    // Onsager parameters and unit weights on the mask (measurements set with p = 1).
+    void baseline(int alg, int n_iters, const double* lam, C* xhat, double* trace, double* nmse_out) {
+        const size_t cb = (size_t)p->B * p->N * sizeof(C);
+        CK(cudaMemsetAsync(p->r, 0, cb, st));
+        CK(cudaMemsetAsync(p->what, 0, cb, st));
+        identity_params();
+        if (alg == 0) {
+            Launch L(p, 5, st);
+            fill_threshold_params<<<(p->B * p->S + 255) / 256, 256, 0, st>>>(p->parf, lam, p->S, p->B);
+        }
+        const long long tstride = (long long)p->B * p->S * TRACE_F;
+        double t_m = 1.0;
+        const int mx = *std::max_element(p->geo.len, p->geo.len + p->S);
+        dim3 ugrid((unsigned)std::max(1, std::min(mx / 256, 64)), p->S, p->B);
+        for (int it = 0; it < n_iters; ++it) {
+            synth(r(), p->par, true, nullptr, 0);
+            col(COL_VDAMP, (const C*)p->T1, (C*)p->T2, 1);
+            analysis(nullptr, true, r(), p->par, true, 2);          // r <- g (gradient step)
+            if (alg == 1) {
+                { Launch L(p, 5, st); oracle_tau<R><<<p->B, SNT, 0, st>>>(p->geo, r(), (const C*)p->w0, p->btau); }
+                select(r(), p->btau, trace ? trace + it * tstride : nullptr, true);   // -> parf = (t_j, 0, 1)
+            }
+            const double t_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t_m * t_m));
+            const double beta = (t_m - 1.0) / t_next;
+            t_m = t_next;
+            { Launch L(p, 5, st); momentum_update<R><<<ugrid, 256, 0, st>>>(p->geo, r(), (C*)p->what, p->parf, beta); }
+            if (nmse_out || (alg == 0 && trace)) {
+                { Launch L(p, 5, st); coef_err<R><<<dim3(p->S, p->B), 256, 0, st>>>(p->geo, (const C*)p->what, (const C*)p->w0, p->berr); }
+                if (nmse_out) {
+                    Launch L(p, 5, st);
+                    err_totals<<<(p->B + 127) / 128, 128, 0, st>>>(p->berr, p->S, p->B,
+                                                                   nmse_out + (long long)it * p->B * VDAMP_NMSE_FIELDS);
+                }
+                if (alg == 0 && trace)            // FISTA records subband NMSE of w_hat in fields 6/7
+                    CK(cudaMemcpy2DAsync(trace + it * tstride + 6, TRACE_F * sizeof(double), p->berr, 2 * sizeof(double),
+                                         2 * sizeof(double), (size_t)p->B * p->S, cudaMemcpyDeviceToDevice, st));
+            }
+        }
+        synth((const C*)p->what, nullptr, false, xhat, 4);                  // x_hat = idwt(w_hat)
+    }
+
     void run(int n_iters, C* xhat, double* trace, double* nmse_out, void* const* snaps) {
         CK(cudaMemsetAsync(p->r, 0, (size_t)p->B * p->N * sizeof(C), st));   // r~_0 = 0
         identity_params();
@@ -450,7 +496,7 @@ void dispatch(Plan* p, void* stream, F&& f) {
 void free_plan(Plan* p) {
     if (!p) return;
     cudaSetDevice(p->dev);
-    void* bufs[] = {p->x0r, p->nmconst, p->nmpart, p->r, p->T1, p->T2, p->yg, p->pinv, p->par, p->parf, p->taupart, p->prow, p->pcol,
+    void* bufs[] = {p->what, p->btau, p->berr, p->x0r, p->nmconst, p->nmpart, p->r, p->T1, p->T2, p->yg, p->pinv, p->par, p->parf, p->taupart, p->prow, p->pcol,
                     p->nvar, p->offs, p->twH, p->twW, p->kA, p->kB, p->x0, p->w0, p->xtmp, p->trtmp};
     for (void* b : bufs) if (b) cudaFree(b);
     for (void* b : p->scratch) if (b) cudaFree(b);
@@ -900,6 +946,31 @@ extern "C" VDAMP_API int vdamp_debug_csort_times(long long* out, int images) {
     return guard([&] { CK(cudaMemcpyFromSymbol(out, g_csort, (size_t)images * 64 * 6 * sizeof(long long))); });
 }
 #endif
+
+int vdamp_baseline_run(vdamp_plan_t plan, int algorithm, int n_iters, const double* lam, void* x_hat, double* trace,
+                       double* nmse, void* stream) {
+    return guard([&] {
+        Plan* p = P(plan);
+        if (algorithm != 0 && algorithm != 1) throw Err{VDAMP_ERR_ARG, "algorithm must be 0 (fista) or 1 (sure_it)"};
+        if (n_iters < 1) throw Err{VDAMP_ERR_ARG, "need at least one iteration"};
+        if (!p->have_meas) throw Err{VDAMP_ERR_STATE, "vdamp_set_measurements must be called first"};
+        if (algorithm == 0 && !lam) throw Err{VDAMP_ERR_ARG, "fista requires lam"};
+        if ((algorithm == 1 || nmse || trace) && !p->have_gt)
+            throw Err{VDAMP_ERR_STATE, algorithm == 1 ? "sure_it needs the ground truth (oracle tau)"
+                                                      : "trace/NMSE need the ground truth"};
+        if (!x_hat) throw Err{VDAMP_ERR_ARG, "null x_hat"};
+        CK(cudaSetDevice(p->dev));
+        if (!p->what) {
+            p->what = dalloc(p, (size_t)p->B * p->N * p->csz);
+            p->btau = (double*)dalloc(p, (size_t)p->B * p->S * sizeof(double));
+            p->berr = (double*)dalloc(p, (size_t)p->B * p->S * 2 * sizeof(double));
+        }
+        dispatch(p, stream, [&](auto& s) {
+            typedef typename std::remove_reference<decltype(s)>::type S_;
+            s.baseline(algorithm, n_iters, lam, (typename S_::C*)x_hat, trace, nmse);
+        });
+    });
+}
 
 int vdamp_mc_accumulate(vdamp_plan_t plan, const void* r, const void* w0, double* sum_r, double* sum_sq,
                         double* scratch, void* stream) {

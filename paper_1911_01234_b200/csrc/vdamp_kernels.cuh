@@ -1495,6 +1495,78 @@ __global__ void __launch_bounds__(SNT) mc_band_sums(Geo g, const double* err, do
     if (threadIdx.x == 0) sum_sq[j] += e / (double)g.len[j];
 }
 
+// ---- baselines on the same operators (src/baselines.py) -----------------
+// FISTA / SURE-IT update: w = soft(g; t_j), r~ = w + beta (w - w_prev), in place
+// (src/baselines.py:77-83, 143-148).  par = (t, 0, 1) per (image, subband).
+template <typename R>
+__global__ void momentum_update(Geo g, typename CT<R>::T* coef, typename CT<R>::T* what, const double* par,
+                                double beta) {
+    typedef typename CT<R>::T C;
+    const int j = blockIdx.y, bi = blockIdx.z;
+    const R t = (R)par[((long long)bi * g.S + j) * 3];
+    const R be = (R)beta;
+    const long long base = (long long)bi * g.N + g.off[j];
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < g.len[j]; e += gridDim.x * blockDim.x) {
+        const C w = onsager<R, C>(coef[base + e], t, R(0), R(1));
+        const C wp = what[base + e];
+        coef[base + e] = mk<C>(w.x + be * (w.x - wp.x), w.y + be * (w.y - wp.y));
+        what[base + e] = w;
+    }
+}
+
+// per (image, subband): |a - w0|^2 and |w0|^2 (src/diagnostics.py:37-51)
+template <typename R>
+__global__ void __launch_bounds__(256) coef_err(Geo g, const typename CT<R>::T* a, const typename CT<R>::T* w0,
+                                                double* out) {
+    __shared__ double sh[256 / 32 + 2];
+    const int j = blockIdx.x, bi = blockIdx.y;
+    const long long base = (long long)bi * g.N + g.off[j];
+    double e = 0.0, r = 0.0;
+    for (int i = threadIdx.x; i < g.len[j]; i += 256) {
+        const typename CT<R>::T u = a[base + i], w = w0[base + i];
+        const double dx = (double)u.x - (double)w.x, dy = (double)u.y - (double)w.y;
+        e += dx * dx + dy * dy;
+        r += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
+    }
+    e = block_sum<256>(e, sh);
+    r = block_sum<256>(r, sh);
+    if (threadIdx.x == 0) { out[((long long)bi * g.S + j) * 2] = e; out[((long long)bi * g.S + j) * 2 + 1] = r; }
+}
+
+// per image: NMSE record {sum_j err, sum_j ref} of coef_err output (fixed order)
+__global__ void err_totals(const double* e, int S, int B, double* out) {
+    const int bi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (bi >= B) return;
+    double a = 0.0, b = 0.0;
+    for (int j = 0; j < S; ++j) { a += e[((long long)bi * S + j) * 2]; b += e[((long long)bi * S + j) * 2 + 1]; }
+    out[2 * bi] = a; out[2 * bi + 1] = b;
+}
+
+// SURE-IT oracle error level tau_k = |r - w0|^2 / N, floored, same for every
+// subband (src/baselines.py:140-142)
+template <typename R>
+__global__ void __launch_bounds__(SNT) oracle_tau(Geo g, const typename CT<R>::T* r, const typename CT<R>::T* w0,
+                                                  double* tau) {
+    __shared__ double sh[SNT / 32 + 2];
+    const int bi = blockIdx.x;
+    const long long base = (long long)bi * g.N;
+    double e = 0.0;
+    for (long long i = threadIdx.x; i < g.N; i += SNT) {
+        const typename CT<R>::T u = r[base + i], w = w0[base + i];
+        const double dx = (double)u.x - (double)w.x, dy = (double)u.y - (double)w.y;
+        e += dx * dx + dy * dy;
+    }
+    e = block_sum<SNT>(e, sh);
+    const double t = fmax(e / (double)g.N, 1e-30);
+    for (int j = threadIdx.x; j < g.S; j += SNT) tau[(long long)bi * g.S + j] = t;
+}
+
+__global__ void fill_threshold_params(double* par, const double* lam, int S, int B) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * S) return;
+    par[3 * i] = lam[i / S]; par[3 * i + 1] = 0.0; par[3 * i + 2] = 1.0;
+}
+
 // per-image |x - x0|^2 and |x0|^2 (src/diagnostics.py:21-34), deterministic
 template <typename R>
 __global__ void __launch_bounds__(SNT) nmse_sums(Geo g, const typename CT<R>::T* x, const typename CT<R>::T* x0, double* out) {

@@ -161,6 +161,27 @@ def main():
     mask = draw_mask(pmap, 0)
     record_run("full64", x0, pmap, mask, synthesize(x0, mask, None), 4, 1)
 
+    # baselines on the same operators (src/baselines.py)
+    from csmri import baselines
+    x0 = shepp_logan(64, 64)
+    pmap = polynomial_pmap(64, 64, 8, 0.02, 4.0)
+    mask = draw_mask(pmap, 5)
+    kd = synthesize(x0, mask, 40.0, 6)
+    xf, trf = baselines.fista(kd.values, mask, 0.01, 12, 4, ground_truth=x0)
+    w0 = dwt(x0, 4)
+    xs, trs = baselines.sure_it(kd.values, mask, w0, 10, 4, ground_truth=x0)
+    grid = np.geomspace(1e-4, 1e-1, 6)
+    lam = baselines.tune_lambda(kd.values, mask, x0, 8, grid, 4)
+    np.savez_compressed(
+        os.path.join(OUT, "baselines.npz"),
+        x0=x0, sampled=mask.sampled, y=kd.values, noise_var=np.array(kd.noise_var),
+        fista_x=xf, fista_nmse=trf.nmse_curve(), fista_sbn=np.array([r.subband_nmse_db for r in trf.records]),
+        sure_x=xs, sure_nmse=trs.nmse_curve(), sure_tau=np.array([r.tau for r in trs.records]),
+        sure_thr=np.array([r.thresholds for r in trs.records]),
+        sure_sbn=np.array([r.subband_nmse_db for r in trs.records]),
+        grid=grid, lam=np.array(lam),
+    )
+
     # density + mask pin for the workload generator (reference disc centre)
     pm = polynomial_pmap(64, 48, 8, 0.02, 4.0)
     pm6 = polynomial_pmap(96, 96, 6, 0.1, 5.0)
