@@ -300,10 +300,10 @@ struct Seq {
         k<<<grid, PNT, sm, st>>>(p->geo, src, dst, (const C*)p->twW, p->rowlog);
     }
 
-    void select(const C* rr, const double* tau_in, double* trace, bool use_w0) {
+    void select(const C* rr, const double* tau_in, double* trace, bool use_w0, bool onsager_par = true) {
         SelArgs<R> a;
         a.r = rr; a.taupart = p->taupart; a.tau_in = tau_in; a.ntiles = p->ntiles;
-        a.par = p->par; a.parf = p->parf; a.trace = trace;
+        a.par = onsager_par ? p->par : nullptr; a.parf = p->parf; a.trace = trace;
         a.w0 = use_w0 ? (const C*)p->w0 : nullptr;
         a.kA = (R*)p->kA; a.kB = (R*)p->kB;
         // big subbands: 1024-thread CTAs with the full sort workspace; small ones:
@@ -410,7 +410,8 @@ struct Seq {
             analysis(nullptr, true, r(), p->par, true, 2);          // r <- g (gradient step)
             if (alg == 1) {
                 { Launch L(p, 5, st); oracle_tau<R><<<p->B, SNT, 0, st>>>(p->geo, r(), (const C*)p->w0, p->btau); }
-                select(r(), p->btau, trace ? trace + it * tstride : nullptr, true);   // -> parf = (t_j, 0, 1)
+                // par keeps the identity of the gradient step; parf = (t_j, 0, 1)
+                select(r(), p->btau, trace ? trace + it * tstride : nullptr, true, false);
             }
             const double t_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t_m * t_m));
             const double beta = (t_m - 1.0) / t_next;
