@@ -101,10 +101,11 @@ def sure_it(y, mask: SamplingMask, w0: WaveletCoeffs, n_iters: int, scales: int 
             *, precision="fp64", device=None):
     """SURE-tuned thresholding with the oracle scalar error level (src/baselines.py:115-164)."""
     lay = SubbandLayout.create(mask.shape[0], mask.shape[1], scales)
-    if w0.layout != lay:
+    wl = w0.layout
+    if (wl.image_height, wl.image_width, wl.scales) != (lay.image_height, lay.image_width, lay.scales):
         raise ValueError("ground-truth coefficients use a different layout")
     from .wavelet import idwt
-    x0 = idwt(w0, precision="fp64")            # the device keeps w0 = dwt(x0)
+    x0 = idwt(WaveletCoeffs(np.asarray(w0.values), lay), precision="fp64")   # the device keeps w0 = dwt(x0)
     x, tr, nm, wall = _run(1, [y], mask, None, n_iters, scales, [x0], precision, device, True)
     trace = RunTrace("sure_it")
     for k in range(n_iters):

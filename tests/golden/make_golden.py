@@ -190,10 +190,48 @@ def main():
         probs_64x48=pm.probs, mask_64x48_seed7=draw_mask(pm, 7).sampled,
         probs_96_d6=pm6.probs,
     )
+    cli_golden()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))
 
 
+CLI_CONFIG = {
+    "phantom_size": 32, "scales": 3, "snr_db": 40.0, "undersampling": [3.0, 5.0],
+    "density": {"degree": 8, "center_radius": 0.02, "p_min": 1e-3},
+    "algorithms": {"vdamp": {"n_iters": 8},
+                   "fista": {"n_iters": 6, "lambda_grid": [1e-3, 1e-2, 1e-1], "tune_budget": 4},
+                   "sure_it": {"n_iters": 6}},
+    "seed": 11,
+}
+
+
+def cli_golden():
+    """Every artifact of one reference ``run_experiment`` (src/cli.py:104-164),
+    packed as text (CSV/JSON) and arrays (.bin) into cli.npz."""
+    import json
+    import tempfile
+    sys.path.insert(0, REF)
+    from csmri import cli, io
+    from csmri.config import config_from_dict
+    d = {"config_json": np.array(json.dumps(CLI_CONFIG))}
+    with tempfile.TemporaryDirectory() as tmp:
+        cli.run_experiment(config_from_dict(json.loads(json.dumps(CLI_CONFIG))), tmp)
+        names = sorted(os.listdir(tmp))
+        d["files"] = np.array(names)
+        for f in names:
+            path = os.path.join(tmp, f)
+            if f.endswith(".bin"):
+                arr, _ = io.load_array(path)
+                d["bin:" + f] = arr
+            else:
+                with open(path) as fh:
+                    d["txt:" + f] = np.array(fh.read())
+    np.savez_compressed(os.path.join(OUT, "cli.npz"), **d)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["cli"]:
+        cli_golden()
+    else:
+        main()
