@@ -334,14 +334,15 @@ struct Seq {
                 const int cap = Scap<R>::v;
                 const size_t slots = (size_t)(cap + cap / 32 + 1) + 1;
                 const size_t slot16 = ((size_t)cap + cap / 32 + 2 + 3) & ~(size_t)3;   // kernel's SLOT
-                size_t sm = sizeof(R) == 4 ? 2 * slot16 * sizeof(R) + (CS_BUCKETS / 2) * sizeof(unsigned)
+                size_t sm = sizeof(R) == 4 ? 2 * slot16 * sizeof(R) + CS_WORDS * sizeof(unsigned)
                                            : slots * sizeof(R);
                 // large subbands: global counting sort counters + ranking tile
                 const size_t gcs = sizeof(R) == 4 ? 32768 * 4 + 16384 * sizeof(R) : 8192 * 4 + 8192 * sizeof(R);
                 if (sm < gcs) sm = gcs;
-                auto k = sure_select<R, SNT>;
+                constexpr int BNT = sizeof(R) == 4 ? BNT32 : BNT64;
+                auto k = sure_select<R, BNT>;
                 set_smem(k, sm);
-                k<<<grid, SNT, sm, ls>>>(p->geo, a);
+                k<<<grid, BNT, sm, ls>>>(p->geo, a);
             } else {
                 const size_t sm = (size_t)(SMALL_N + SMALL_N / 32 + 2) * sizeof(R);
                 auto k = sure_select<R, SNT_SMALL>;
@@ -942,6 +943,9 @@ int vdamp_kernel_times(vdamp_plan_t plan, double* ms, int64_t* launches) {
 // debug build only: copy the per-(image, subband) phase clocks of the last select launch
 extern "C" VDAMP_API int vdamp_debug_phase_times(long long* out, int images) {
     return guard([&] { CK(cudaMemcpyFromSymbol(out, g_phase, (size_t)images * 64 * 4 * sizeof(long long))); });
+}
+extern "C" VDAMP_API int vdamp_debug_scan_times(long long* out, int images) {
+    return guard([&] { CK(cudaMemcpyFromSymbol(out, g_scan, (size_t)images * 64 * 5 * sizeof(long long))); });
 }
 extern "C" VDAMP_API int vdamp_debug_csort_times(long long* out, int images) {
     return guard([&] { CK(cudaMemcpyFromSymbol(out, g_csort, (size_t)images * 64 * 6 * sizeof(long long))); });

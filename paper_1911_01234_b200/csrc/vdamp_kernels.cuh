@@ -22,7 +22,12 @@ namespace vdamp {
 constexpr int MAXS = 64;          // subbands supported (scales <= 21)
 constexpr int PNT = 256;          // threads of strip / column kernels
 constexpr int PCAP = 4096;        // complex elements per strip / column tile
-constexpr int SNT = 1024;         // threads of the SURE kernel (subbands > SMALL_N)
+constexpr int SNT = 1024;         // threads of the per-image reduction kernels
+// threads of the big SURE-select kernel (subbands > SMALL_N): 512 for fp32
+// (128 registers per thread: the sort and scan loops run spill-free; local
+// memory would miss the ~30 KB of L1 left beside 200 KB of shared memory),
+// 1024 for fp64
+constexpr int BNT32 = 1024, BNT64 = 1024;
 constexpr int SNT_SMALL = 256;    // threads of the small-subband SURE kernel
 constexpr int SMALL_N = 1024;     // subbands up to this size use the small kernel
 constexpr int SCAP = 16384;       // fp32 magnitudes sorted in shared memory at once
@@ -655,6 +660,21 @@ struct SelArgs {
 
 struct Best { double risk, t, cnt, inv; };
 
+// 1/m for m > 0 without the library reciprocal's out-of-line slow path (whose
+// call forces register spills in the select kernels): hardware approximation
+// plus two FMA Newton steps (within 1 ulp); extreme magnitudes are
+// rescaled by an exact power of two first.
+__device__ __forceinline__ double rcp_pos(double m) {
+    double sc = 1.0;
+    if (m < 1e-300) { m *= 0x1p600; sc = 0x1p600; }           // exact power-of-two rescaling
+    else if (m > 1e300) { m *= 0x1p-600; sc = 0x1p-600; }
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(m));
+    double e = fma(-m, r, 1.0); r = fma(r, e, r);
+    e = fma(-m, r, 1.0); r = fma(r, e, r);
+    return r * sc;
+}
+
 __device__ __forceinline__ bool better(const Best& a, const Best& b) {
     return a.risk < b.risk || (a.risk == b.risk && a.t < b.t);
 }
@@ -770,21 +790,32 @@ __device__ void block_sort(R* s, int n) {
         case 2: block_sort_e<R, 2>(s, n); break;
         case 4: block_sort_e<R, 4>(s, n); break;
         case 8: block_sort_e<R, 8>(s, n); break;
-        default: block_sort_e<R, 16>(s, n); break;
+        default:
+            if constexpr (SCAP / NT > 16) { if (E > 16) { block_sort_e<R, 32>(s, n); break; } }
+            block_sort_e<R, 16>(s, n);
+            break;
     }
 }
 
 // ---------------------------------------------------------------------------
-// Counting sort of n <= SCAP float magnitudes (fp32 path).  Bucket = the key's
-// IEEE bits (monotone for x >= 0) shifted so that the nonzero range fits
-// CS_BUCKETS-1 buckets (float bits are logarithmic: ~1000 buckets per octave);
-// zeros go to bucket 0.  Histogram and scatter use packed 16-bit shared
-// counters; the scatter order inside a bucket is arbitrary, so every bucket
-// is finished by an insertion sort on the full key.  The sorted sequence is
-// unique, so the result is deterministic.  `out` is scratch (must not alias
-// keys); on success the sorted keys are back in `keys`.
+// Counting sort of 4096 <= n <= SCAP float magnitudes (fp32 path), with a
+// data-equalised bucket map.  Keys are IEEE bits (monotone for x >= 0); zeros
+// go to bucket 0.  A coarse pass histograms the nonzero bit range into
+// CS_COARSE equal-width coarse buckets; each coarse bucket c then receives a
+// run of fine buckets proportional to its population (fs_c, w_c), and a key
+// maps linearly into its coarse bucket's run.  The map is monotone in the
+// key, and on the magnitudes VDAMP produces it leaves ~1 key per fine bucket
+// (plain float-bit buckets crowd 10+ keys into the buckets of the Rayleigh
+// bulk), so the buckets are finished by two passes of 16-key register
+// bitonic sorts over overlapping windows; data with a bucket of more than 8
+// keys takes an in-bucket ranking pass instead.  Histogram and scatter use
+// packed 16-bit shared counters.  The sorted sequence is unique, so the
+// result is deterministic.  `out` must not alias `keys`.
 // ---------------------------------------------------------------------------
-constexpr int CS_BUCKETS = 32768;
+constexpr int CS_WORDS = 16384;   // 64 KB counter region (also the TMA landing zone's tail)
+constexpr int CS_FINE = 16384;    // fine buckets (packed 16-bit: CS_FINE / 2 words)
+constexpr int CS_COARSE = 1024;   // coarse buckets (one per thread of the 1024-thread CTA)
+static_assert(CS_FINE / 2 + 2 * CS_COARSE <= CS_WORDS, "counting-sort tables exceed the counter region");
 
 #ifdef VDAMP_PHASE_TIMING
 __device__ long long g_csort[4096][64][6];
@@ -793,20 +824,52 @@ __device__ long long g_csort[4096][64][6];
 #define CS_MARK(i) do { } while (0)
 #endif
 
-constexpr int CS_MAXB = 256;      // larger buckets -> comparison-sort fallback (degenerate data)
+constexpr int CS_MAXB = 256;      // larger fine buckets -> comparison-sort fallback (heavy ties)
 
-// Returns false (nothing written to out) when some bucket holds more than
-// CS_MAXB keys: heavy ties / concentrated data (e.g. a diverged run) would make
-// the in-bucket ranking quadratic, the caller then uses the bitonic sort.
-__device__ bool counting_sort(const float* keys, float* out, unsigned* cnt, int n, double* sh, long long* dbg = nullptr) {
+__device__ __forceinline__ unsigned cs_fine(unsigned k, int lc, unsigned cb, const unsigned* tab) {
+    if (!k) return 0u;
+    const unsigned c = (k >> lc) - cb;
+    const unsigned t = tab[c];
+    const unsigned long long off = (unsigned long long)(k - ((cb + c) << lc)) * (t >> 16);
+    return 1u + (t & 0xffffu) + (unsigned)(off >> lc);
+}
+
+__device__ __forceinline__ void sort16(unsigned (&v)[16]) {
+#pragma unroll
+    for (int k = 2; k <= 16; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const unsigned x = v[i], y = v[l];
+                    const bool up = (i & k) == 0;
+                    v[i] = up ? min(x, y) : max(x, y);
+                    v[l] = up ? max(x, y) : min(x, y);
+                }
+            }
+        }
+    }
+}
+
+// 0: some bucket holds more than CS_MAXB keys (nothing usable; the caller
+// bitonic-sorts `keys`); 1: sorted keys in `out`; 2: sorted keys in `keys`.
+template <int NT>
+__device__ int counting_sort(const float* keys, float* out, unsigned* cnt, int n, double* sh, long long* dbg = nullptr) {
+    static_assert(CS_COARSE % NT == 0 && NT <= CS_COARSE, "coarse scan: whole coarse buckets per thread");
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 #ifdef VDAMP_PHASE_TIMING
     long long cs0_ = clock64();
 #endif
     const unsigned* kb = reinterpret_cast<const unsigned*>(keys);
     unsigned* ob = reinterpret_cast<unsigned*>(out);
+    unsigned* hc = cnt + CS_FINE / 2;                // coarse histogram
+    unsigned* tab = hc + CS_COARSE;                  // coarse bucket -> fine start | width << 16
+    const int nbf = n >= CS_FINE ? CS_FINE : (int)(1u << (32 - __clz((unsigned)n - 1u)));
+    const int words = nbf >> 1;
     unsigned mn = 0xffffffffu, mx = 0;
-    for (int i = tid; i < n; i += SNT) {
+    for (int i = tid; i < n; i += NT) {
         const unsigned k = kb[KI(i)];
         if (k) mn = min(mn, k);
         mx = max(mx, k);
@@ -818,7 +881,8 @@ __device__ bool counting_sort(const float* keys, float* out, unsigned* cnt, int 
     unsigned* red = reinterpret_cast<unsigned*>(sh);
     __syncthreads();
     if (lane == 0) { red[w] = mn; red[32 + w] = mx; }
-    for (int i = tid; i < CS_BUCKETS / 2; i += SNT) cnt[i] = 0;
+    for (int i = tid; i < words; i += NT) cnt[i] = 0;
+    for (int i = tid; i < CS_COARSE; i += NT) hc[i] = 0;
     __syncthreads();
     if (tid < 32) {
         unsigned a = red[tid], b = red[32 + tid];
@@ -830,68 +894,121 @@ __device__ bool counting_sort(const float* keys, float* out, unsigned* cnt, int 
     }
     __syncthreads();
     mn = red[64]; mx = red[65];
-    CS_MARK(0);
     if (mn > mx) mn = mx;                            // all zeros
-    int lo = 0;
-    while (((mx >> lo) - (mn >> lo)) >= (unsigned)(CS_BUCKETS - 2)) ++lo;
-    const unsigned base = mn >> lo;
-    // histogram
-    for (int i = tid; i < n; i += SNT) {
+    int lc = 0;
+    while (((mx >> lc) - (mn >> lc)) >= (unsigned)CS_COARSE) ++lc;
+    const unsigned cb = mn >> lc;
+    // coarse histogram of the nonzero keys
+    for (int i = tid; i < n; i += NT) {
         const unsigned k = kb[KI(i)];
-        const unsigned b = k ? (k >> lo) - base + 1u : 0u;
+        if (k) atomicAdd(&hc[(k >> lc) - cb], 1u);
+    }
+    __syncthreads();
+    CS_MARK(0);
+    // coarse bucket t -> fine run [fs, fs + w) of the nbf - 1 nonzero buckets,
+    // proportional to its population (integer arithmetic: exact, deterministic)
+    {
+        constexpr int CPT = CS_COARSE / NT;          // coarse buckets per thread
+        unsigned h[CPT], hs = 0;
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) { h[q] = hc[tid * CPT + q]; hs += h[q]; }
+        unsigned P = (unsigned)block_excl_scan<NT, false>((double)hs, sh + 66);
+        if (tid == NT - 1) red[66] = P + hs;
+        __syncthreads();
+        const unsigned tot = red[66];
+        const unsigned F = (unsigned)nbf - 1u;
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+            unsigned fs = 0, fe = 0;
+            if (tot) {
+                fs = (unsigned)(((unsigned long long)P * F) / tot);
+                fe = (unsigned)(((unsigned long long)(P + h[q]) * F) / tot);
+            }
+            tab[tid * CPT + q] = fs | ((fe - fs) << 16);
+            P += h[q];
+        }
+    }
+    __syncthreads();
+    // fine histogram
+    for (int i = tid; i < n; i += NT) {
+        const unsigned b = cs_fine(kb[KI(i)], lc, cb, tab);
         atomicAdd(&cnt[b >> 1], 1u << ((b & 1u) * 16));
     }
     __syncthreads();
     CS_MARK(1);
+    bool crowd8;
     {
-        unsigned big = 0;
-        for (int i = tid; i < CS_BUCKETS / 2; i += SNT) {
+        unsigned big = 0, c8 = 0;
+        for (int i = tid; i < words; i += NT) {
             const unsigned v = cnt[i];
-            big |= ((v & 0xffffu) > (unsigned)CS_MAXB) | ((v >> 16) > (unsigned)CS_MAXB);
+            const unsigned lo16 = i ? (v & 0xffffu) : 0u;            // bucket 0: zeros, always in order
+            big |= (lo16 > (unsigned)CS_MAXB) | ((v >> 16) > (unsigned)CS_MAXB);
+            c8 |= (lo16 > 8u) | ((v >> 16) > 8u);
         }
-        if (__syncthreads_or(big)) return false;
+        if (__syncthreads_or(big)) return 0;
+        crowd8 = __syncthreads_or(c8) != 0;
     }
-    // exclusive scan of the CS_BUCKETS 16-bit counts (thread t: buckets [32t, 32t+32))
+    // exclusive scan of the fine counts (thread t: words [t*per, t*per + per))
     {
-        constexpr int PER = CS_BUCKETS / 2 / SNT;    // packed words per thread
-        unsigned v[PER];
+        constexpr int PMAX = CS_FINE / 2 / NT;
+        const int per = words / NT;
+        unsigned v[PMAX];
         unsigned tot = 0;
 #pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            v[i] = cnt[tid * PER + i];
+        for (int i = 0; i < PMAX; ++i) {
+            v[i] = i < per ? cnt[tid * per + i] : 0u;
             tot += (v[i] & 0xffffu) + (v[i] >> 16);
         }
-        // block exclusive scan of integer totals (exact in double)
-        unsigned run = (unsigned)block_excl_scan<SNT, false>((double)tot, sh + 66);
+        unsigned run = (unsigned)block_excl_scan<NT, false>((double)tot, sh + 66);
 #pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const unsigned c0 = v[i] & 0xffffu, c1 = v[i] >> 16;
-            cnt[tid * PER + i] = run | ((run + c0) << 16);
-            run += c0 + c1;
+        for (int i = 0; i < PMAX; ++i) {
+            if (i < per) {
+                const unsigned c0 = v[i] & 0xffffu, c1 = v[i] >> 16;
+                cnt[tid * per + i] = run | ((run + c0) << 16);
+                run += c0 + c1;
+            }
         }
     }
     __syncthreads();
     CS_MARK(2);
     // scatter (cursor = packed 16-bit half, never carries: offsets + counts <= n <= 16384)
-    for (int i = tid; i < n; i += SNT) {
+    for (int i = tid; i < n; i += NT) {
         const unsigned k = kb[KI(i)];
-        const unsigned b = k ? (k >> lo) - base + 1u : 0u;
+        const unsigned b = cs_fine(k, lc, cb, tab);
         const unsigned sft = (b & 1u) * 16;
         const unsigned old = atomicAdd(&cnt[b >> 1], 1u << sft);
         ob[KI((old >> sft) & 0xffffu)] = k;
     }
     __syncthreads();
     CS_MARK(3);
-    // finish every bucket in parallel: the final slot of key x at grouped position
-    // i is start(b) + #{y in b : y < x} + #{y in b : y == x, pos(y) < i}.  Threads
-    // of a warp mostly share a bucket, so the smem reads broadcast.  The grouped
-    // keys live in `ob`; the sorted result is written into the input buffer
-    // (consumed by now): on success the keys come back sorted IN PLACE.
+    // every cursor now holds its bucket's end.  Fast path (all buckets <= 8
+    // keys, the normal case with ~1 key per bucket): bitonic-sort the aligned
+    // 16-key windows in registers, then the windows shifted by 8.  Sorting a
+    // window only permutes keys of the same bucket (the bucket order is
+    // already right), and every bucket of <= 8 keys lies inside one window of
+    // one of the two passes, so both passes together sort every bucket.
+    if (!crowd8) {
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int p0 = tid * 16 + pass * 8; p0 + 16 <= n; p0 += NT * 16) {
+                unsigned v[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] = ob[KI(p0 + e)];
+                sort16(v);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) ob[KI(p0 + e)] = v[e];
+            }
+            __syncthreads();
+        }
+        CS_MARK(4);
+        return 1;
+    }
+    // slow path: rank every key inside its bucket (ties by grouped position),
+    // writing the sorted sequence back into `keys` (consumed by now)
     unsigned* fb = const_cast<unsigned*>(kb);
-    for (int i = tid; i < n; i += SNT) {
+    for (int i = tid; i < n; i += NT) {
         const unsigned x = ob[KI(i)];
-        const unsigned bk = x ? (x >> lo) - base + 1u : 0u;
-        const unsigned e1 = cnt[bk >> 1] >> ((bk & 1u) * 16) & 0xffffu;          // end of bucket bk
+        const unsigned bk = cs_fine(x, lc, cb, tab);
+        const unsigned e1 = cnt[bk >> 1] >> ((bk & 1u) * 16) & 0xffffu;
         unsigned s0 = 0;
         if (bk > 0) { const unsigned bp = bk - 1u; s0 = cnt[bp >> 1] >> ((bp & 1u) * 16) & 0xffffu; }
         unsigned rank = 0;
@@ -903,7 +1020,7 @@ __device__ bool counting_sort(const float* keys, float* out, unsigned* cnt, int 
     }
     __syncthreads();
     CS_MARK(4);
-    return true;
+    return 2;
 }
 
 // ---------------------------------------------------------------------------
@@ -1052,48 +1169,107 @@ __device__ R* global_merge_sort(R* A, R* B, R* smem, int n, int CAP) {
 // Evaluate the candidates owned by this thread on one tile of sorted
 // magnitudes (src/denoise.py:62-118):  candidate t = m_i at the end of each
 // tie run, plus the stationary point of the quadratic piece that starts there.
-template <typename R, int NT>
+template <typename R, int NT, int EMAX, bool SMEM>
+__device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, int n, double tau, int b0, int E,
+                                          double pre, double suf, double next_tile_first, Best& best,
+                                          const double* sreg, const double* slo, const double* shi);
+
+// One tile of the exact SURE scan.  Thread t owns the E consecutive sorted keys
+// [t*E, t*E + E).  The suffix of inverses is accumulated from the large keys
+// down and the prefix of squares from the small keys up, so neither sum ever
+// cancels.  The per-key suffixes go to shared scratch (slo/shi, key e of thread
+// t at [e * NT + t], conflict-free; keys e >= EMAX/2 in shi) when SMEM, to
+// registers otherwise (small E only: a register array of 16 doubles spills).
+template <typename R, int NT, int EMAX, bool SMEM>
 __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, int n, double tau,
                                           double pre_tile, double suf_tile, double next_tile_first,
-                                          double* sh, Best& best, double* totinv) {
+                                          double* sh, Best* wbest, Best* run, double* totinv, double* slo,
+                                          double* shi, long long* dbg = nullptr) {
     const int tid = threadIdx.x;
+    Best best{INFINITY, INFINITY, 0.0, 0.0};
+#ifdef VDAMP_PHASE_TIMING
+    long long c0_ = clock64();
+#define SC_MARK(i) do { if (tid == 0 && dbg) { long long c_ = clock64(); dbg[i] = c_ - c0_; c0_ = c_; } } while (0)
+#else
+#define SC_MARK(i) do { } while (0)
+#endif
     const int E = T >= NT ? T / NT : 1;
     const bool act = tid * E < T;
     const int b0 = tid * E;
-    constexpr int EMAX = 16;
+    constexpr int HALF = EMAX / 2 > 0 ? EMAX / 2 : 1;
     double ssq = 0.0, sinv = 0.0;
-    double sufl[EMAX];                       // sum of inverses above each owned key, within the segment
+    double sreg[SMEM ? 1 : EMAX];
     if (act) {
-        for (int e = 0; e < E; ++e) { const double m = (double)keys[KI(b0 + e)]; ssq += m * m; }
-#pragma unroll
+        // one conversion per key (F2F/I2F/MUFU issue at 1/4 of the DFMA rate)
+#pragma unroll (SMEM ? 4 : EMAX)
         for (int e = EMAX - 1; e >= 0; --e) {
             if (e < E) {
-                sufl[e] = sinv;
+                if constexpr (SMEM) (e < HALF ? slo : shi)[(e % HALF) * NT + tid] = sinv;
+                else sreg[e] = sinv;
                 const double m = (double)keys[KI(b0 + e)];
-                if (m > 0) sinv += __drcp_rn(m);
+                ssq = fma(m, m, ssq);
+                if (m > 0) sinv += rcp_pos(m);
             }
         }
     }
+    SC_MARK(0);
     const double pre = block_excl_scan<NT, false>(ssq, sh) + pre_tile;
     const double suf = block_excl_scan<NT, true>(sinv, sh) + suf_tile;
     if (tid == 0 && tilebase == 0) *totinv = suf + sinv;     // sum of all inverses
-    if (!act) return;
+    SC_MARK(1);
+    if (act) scan_keys<R, NT, EMAX, SMEM>(keys, T, tilebase, n, tau, b0, E, pre, suf, next_tile_first, best,
+                                          sreg, slo, shi);
+    // tile argmin (ties -> smaller t) merged into the running best by thread 0
+    for (int o = 16; o > 0; o >>= 1) {
+        Best c;
+        c.risk = __shfl_xor_sync(0xffffffffu, best.risk, o);
+        c.t = __shfl_xor_sync(0xffffffffu, best.t, o);
+        c.cnt = __shfl_xor_sync(0xffffffffu, best.cnt, o);
+        c.inv = __shfl_xor_sync(0xffffffffu, best.inv, o);
+        if (better(c, best)) best = c;
+    }
+    SC_MARK(2);
+    if ((tid & 31) == 0) wbest[tid >> 5] = best;
+    __syncthreads();
+    SC_MARK(3);
+    if (tid < 32) {                                  // warp 0: argmin over the warp winners
+        Best c = tid < NT / 32 ? wbest[tid] : Best{INFINITY, INFINITY, 0.0, 0.0};
+        for (int o = 16; o > 0; o >>= 1) {
+            Best d;
+            d.risk = __shfl_xor_sync(0xffffffffu, c.risk, o);
+            d.t = __shfl_xor_sync(0xffffffffu, c.t, o);
+            d.cnt = __shfl_xor_sync(0xffffffffu, c.cnt, o);
+            d.inv = __shfl_xor_sync(0xffffffffu, c.inv, o);
+            if (better(d, c)) c = d;
+        }
+        if (tid == 0 && better(c, *run)) *run = c;
+    }
+    SC_MARK(4);
+}
+
+template <typename R, int NT, int EMAX, bool SMEM>
+__device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, int n, double tau, int b0, int E,
+                                          double pre, double suf, double next_tile_first, Best& best,
+                                          const double* sreg, const double* slo, const double* shi) {
+    const int tid = threadIdx.x;
+    constexpr int HALF = EMAX / 2 > 0 ? EMAX / 2 : 1;
     const double nt = (double)n * tau;
-    // exact suffix of inverses per owned key (accumulated from the large keys
-    // down, no subtraction), then a forward walk for the prefix of squares:
-    // both sums are built in the direction that never cancels
     double zacc = pre;
-#pragma unroll
+    double m = (double)keys[KI(b0)];
+    double cnt = (double)(n - (tilebase + b0));                // keys above, counted down exactly
+#pragma unroll (SMEM ? 4 : EMAX)
     for (int e = 0; e < EMAX; ++e) {
         if (e < E) {
             const int il = b0 + e;
-            const double m = (double)keys[KI(il)];
             zacc += m * m;                                     // sum_{j <= i} m_j^2
+            cnt -= 1.0;
             const double nxt = (il + 1 < T) ? (double)keys[KI(il + 1)] : next_tile_first;
             if (m != nxt) {
+                double sl;
+                if constexpr (SMEM) sl = (e < HALF ? slo : shi)[(e % HALF) * NT + tid];
+                else sl = sreg[e];
                 const double zeroed = zacc;
-                const double inv_above = suf + sufl[e];        // both >= 0: no cancellation
-                const double cnt = (double)(n - (tilebase + il + 1));
+                const double inv_above = suf + sl;             // both >= 0: no cancellation
                 const double risk = zeroed + m * m * cnt - nt + tau * (2.0 * cnt - m * inv_above);
                 consider(best, risk, m, cnt, inv_above);
                 if (cnt > 0) {
@@ -1109,6 +1285,7 @@ __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, in
                     }
                 }
             }
+            m = nxt;
         }
     }
 }
@@ -1116,6 +1293,7 @@ __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, in
 #ifdef VDAMP_PHASE_TIMING
 // [image][subband][phase]: clock64 deltas of thread 0 (debug builds only)
 __device__ long long g_phase[4096][64][4];
+__device__ long long g_scan[4096][64][5];
 #define PHASE_MARK(i) do { if (threadIdx.x == 0 && bi < 4096) { long long c_ = clock64(); g_phase[bi][j][i] = c_ - ph0_; ph0_ = c_; } } while (0)
 #else
 #define PHASE_MARK(i) do { } while (0)
@@ -1130,6 +1308,8 @@ struct SelShared {
     double tpart[MAXCT];             // tau partials of the column tiles
     double tau, totinv;
     Best best[NT / 32];
+    Best run;                        // running argmin over the tiles
+    double err, ref;                 // subband |r - w0|^2, |w0|^2 (trace)
 };
 
 // Exact SURE selection for subband j of image bi (src/denoise.py:62-118,
@@ -1158,6 +1338,13 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
     const C* rs = a.r + base;
     const C* w0 = a.w0 ? a.w0 + base : nullptr;
     double err = 0.0, ref = 0.0;
+    // reduced right after the loads, so the sums are not live across the sort and scan
+    auto flush_err = [&]() {
+        if (w0) {
+            const double e2 = block_sum<NT>(err, sh), r2 = block_sum<NT>(ref, sh);
+            if (tid == 0) { S_.err = e2; S_.ref = r2; }
+        }
+    };
     constexpr int CAPK = Scap<R>::v;
     const bool large = n > CAPK;
     const int T = large ? CAPK : n;
@@ -1167,7 +1354,7 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
     constexpr int SLOT = (CAPK + CAPK / 32 + 2 + 3) & ~3;          // padded keys, 16-byte aligned stride
     R* stage = keys + SLOT;
     unsigned* ccnt = reinterpret_cast<unsigned*>(stage + SLOT);
-    const bool csort = NT == SNT && sizeof(R) == 4 && T >= 4096;
+    const bool csort = NT >= BNT32 && sizeof(R) == 4 && T >= 4096;
     R* skeys = keys;                                               // where the sorted keys end up
     if (!large && csort) {
         // TMA: the subband is one contiguous segment of r; bulk-copy it into the
@@ -1200,14 +1387,16 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             for (int i = 0; i < a.ntiles; ++i) t += S_.tpart[i];
             s_tau = t;
         }
-        if constexpr (NT == SNT) {
+        flush_err();
+        if constexpr (NT >= BNT32) {
 #ifdef VDAMP_PHASE_TIMING
             long long* dbg = (bi < 4096) ? &g_csort[bi][j][0] : nullptr;
 #else
             long long* dbg = nullptr;
 #endif
-            if (!counting_sort(reinterpret_cast<const float*>(keys), reinterpret_cast<float*>(stage), ccnt, T, sh, dbg))
-                block_sort<R, NT>(keys, T);
+            const int cs = counting_sort<NT>(reinterpret_cast<const float*>(keys), reinterpret_cast<float*>(stage), ccnt, T, sh, dbg);
+            if (cs == 1) skeys = stage;
+            else if (cs == 0) block_sort<R, NT>(keys, T);
         }
     } else if (!large) {
         R* dstk = keys;
@@ -1244,6 +1433,7 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             for (int i = 0; i < a.ntiles; ++i) t += S_.tpart[i];
             s_tau = t;
         }
+        flush_err();
         block_sort<R, NT>(keys, T);
     } else {
         // whole subband -> global scratch keys, counting sort there (L2-resident)
@@ -1264,8 +1454,9 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             for (int i = 0; i < a.ntiles; ++i) t += S_.tpart[i];
             s_tau = t;
         }
+        flush_err();
         sorted = ka;
-        if constexpr (NT == SNT) {
+        if constexpr (NT >= BNT32) {
             if (!global_counting_sort<R, NT>(ka, a.kB + base, reinterpret_cast<unsigned*>(keys), n, sh))
                 sorted = global_merge_sort<R, NT>(ka, a.kB + base, keys, n, CAPK);
         }
@@ -1275,7 +1466,7 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             for (int e = tid; e < CAPK; e += NT) {
                 const double m = (double)sorted[t * CAPK + e];
                 q += m * m;
-                if (m > 0) v += __drcp_rn(m);
+                if (m > 0) v += rcp_pos(m);
             }
             q = block_sum<NT>(q, sh);
             v = block_sum<NT>(v, sh);
@@ -1283,7 +1474,6 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
         }
         __syncthreads();
     }
-    if (w0) { err = block_sum<NT>(err, sh); ref = block_sum<NT>(ref, sh); }
     if (tid == 0) {
         double acc = 0.0;
         for (int t = 0; t < ntl; ++t) { tpre[t] = acc; acc += large ? tsq[t] : 0.0; }
@@ -1294,7 +1484,22 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
     PHASE_MARK(0);                                   // load + sort (+ merges)
     const double tau = fmax(s_tau, TAU_FLOOR);
 
-    Best best{INFINITY, INFINITY, 0.0, 0.0};
+    if (tid == 0) S_.run = Best{INFINITY, INFINITY, 0.0, 0.0};     // scan_tile's barriers order this
+    // fp32 big kernel: per-key suffix scratch in the shared regions the sorted
+    // keys do not occupy (2 x 64 KB)
+    constexpr bool SMEMSUF = NT >= BNT32 && sizeof(R) == 4;
+    constexpr int EMAXS = NT >= BNT32 ? CAPK / NT : SMALL_N / NT;
+    double* slo = nullptr;
+    double* shi = nullptr;
+    if constexpr (SMEMSUF) {
+        if (!large && skeys == stage) {
+            slo = reinterpret_cast<double*>(keys);
+            shi = reinterpret_cast<double*>(ccnt);
+        } else {
+            slo = reinterpret_cast<double*>(stage);
+            shi = slo + (EMAXS / 2) * NT;
+        }
+    }
     for (int t = 0; t < ntl; ++t) {
         if (large) {
             __syncthreads();
@@ -1302,7 +1507,14 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             __syncthreads();
         }
         const double nf = (t + 1 < ntl) ? (double)sorted[(t + 1) * CAPK] : INFINITY;
-        scan_tile<R, NT>(large ? keys : skeys, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, best, &s_totinv);
+        scan_tile<R, NT, EMAXS, SMEMSUF>(large ? keys : skeys, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, s_best,
+                                          &S_.run, &s_totinv, slo, shi,
+#ifdef VDAMP_PHASE_TIMING
+                                          bi < 4096 ? &g_scan[bi][j][0] : nullptr
+#else
+                                          nullptr
+#endif
+                                          );
     }
     // candidate t = 0 when no magnitude is zero (src/denoise.py:84)
     __syncthreads();
@@ -1312,29 +1524,20 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
         if (m0 > 0) {
             const double totinv = s_totinv;
             const double nn = (double)n;
-            consider(best, 0.0 + 0.0 * nn - nn * tau + tau * (2.0 * nn - 0.0 * totinv), 0.0, nn, totinv);
+            Best bb = S_.run;
+            consider(bb, 0.0 + 0.0 * nn - nn * tau + tau * (2.0 * nn - 0.0 * totinv), 0.0, nn, totinv);
             const double ts = tau * totinv / (2.0 * nn);
             if (ts > 0.0 && ts < m0) {
                 const double rsk = 0.0 + ts * ts * nn - nn * tau + tau * (2.0 * nn - ts * totinv);
-                consider(best, rsk, ts, nn, totinv);
+                consider(bb, rsk, ts, nn, totinv);
             }
+            S_.run = bb;
         }
     }
     PHASE_MARK(1);                                   // scans + candidates
-    // block argmin, ties -> smaller t
-    for (int o = 16; o > 0; o >>= 1) {
-        Best c;
-        c.risk = __shfl_xor_sync(0xffffffffu, best.risk, o);
-        c.t = __shfl_xor_sync(0xffffffffu, best.t, o);
-        c.cnt = __shfl_xor_sync(0xffffffffu, best.cnt, o);
-        c.inv = __shfl_xor_sync(0xffffffffu, best.inv, o);
-        if (better(c, best)) best = c;
-    }
-    if ((tid & 31) == 0) s_best[tid >> 5] = best;
-    __syncthreads();
+    // the argmin over all tiles and candidates (ties -> smaller t) is S_.run
     if (tid == 0) {
-        Best bb = s_best[0];
-        for (int w = 1; w < NT / 32; ++w) if (better(s_best[w], bb)) bb = s_best[w];
+        const Best bb = S_.run;
         const double alpha = (bb.cnt - 0.5 * bb.t * bb.inv) / (double)n;   // src/denoise.py:169
         const bool clamped = alpha >= ALPHA_CLAMP;                         // src/vdamp.py:121-124
         const double ac = clamped ? ALPHA_CLAMP : alpha;
@@ -1344,14 +1547,14 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
         if (a.trace) {
             double* tr = a.trace + pj * TRACE_F;
             tr[0] = s_tau; tr[1] = bb.t; tr[2] = bb.t / tau; tr[3] = ac; tr[4] = alpha;
-            tr[5] = clamped ? 1.0 : 0.0; tr[6] = err; tr[7] = ref;
+            tr[5] = clamped ? 1.0 : 0.0; tr[6] = w0 ? S_.err : 0.0; tr[7] = w0 ? S_.ref : 0.0;
         }
     }
     PHASE_MARK(2);                                   // argmin + outputs
 }
 
 template <typename R, int NT>
-__global__ void __launch_bounds__(NT, NT == SNT ? 1 : 4) sure_select(Geo g, SelArgs<R> a) {
+__global__ void __launch_bounds__(NT, NT >= BNT32 ? 1 : 4) sure_select(Geo g, SelArgs<R> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     R* keys = reinterpret_cast<R*>(smem_raw);
     __shared__ SelShared<NT> S_;

@@ -25,4 +25,12 @@ buf2 = (ctypes.c_longlong * (64 * 64 * 6))()
 lib.vdamp_debug_csort_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
 _lib.check(lib.vdamp_debug_csort_times(buf2, 64))
 c = np.frombuffer(buf2, dtype=np.int64).reshape(64, 64, 6)[:nb, S - 3:S, :5].mean((0, 1))
-print("counting sort (n=16384) cycles: minmax %.0f  hist %.0f  scan %.0f  scatter %.0f  fixup %.0f" % tuple(c))
+print("counting sort (n=16384) cycles: minmax+coarse %.0f  table+fine hist %.0f  check+scan %.0f  scatter %.0f  bucket sort %.0f" % tuple(c))
+
+buf3 = (ctypes.c_longlong * (64 * 64 * 5))()
+lib.vdamp_debug_scan_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
+_lib.check(lib.vdamp_debug_scan_times(buf3, 64))
+c3 = np.frombuffer(buf3, dtype=np.int64).reshape(64, 64, 5)[:nb, :S, :]
+for j in range(S):
+    m = c3[:, j, :].mean(0)
+    print(f"scan subband {j:2d}: pass1 {m[0]:7.0f}  block scans {m[1]:7.0f}  keys {m[2]:7.0f}  barrier {m[3]:7.0f}  merge {m[4]:7.0f}")
