@@ -1247,6 +1247,20 @@ __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, in
     SC_MARK(4);
 }
 
+// q = a / b for b > 0 without the library division's out-of-line slow path
+// (FMA residual correction of a ~1-ulp reciprocal: correctly rounded for the
+// magnitudes the SURE scan produces)
+__device__ __forceinline__ double div_pos(double a, double b) {
+    const double r = rcp_pos(b);
+    const double q = a * r;
+    return fma(fma(-b, q, a), r, q);
+}
+
+// Candidate walk over the keys one thread owns.  Only the best risk and a
+// 32-bit candidate code (key index * 2 + interior flag) are carried through
+// the loop; the winner's (t, count, inverse sum) are rebuilt afterwards.
+// Candidates arrive in increasing t, so a strict '<' keeps the smaller t of
+// a tie.
 template <typename R, int NT, int EMAX, bool SMEM>
 __device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, int n, double tau, int b0, int E,
                                           double pre, double suf, double next_tile_first, Best& best,
@@ -1257,6 +1271,8 @@ __device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, in
     double zacc = pre;
     double m = (double)keys[KI(b0)];
     double cnt = (double)(n - (tilebase + b0));                // keys above, counted down exactly
+    double brisk = INFINITY;
+    int bcode = -1;
 #pragma unroll (SMEM ? 4 : EMAX)
     for (int e = 0; e < EMAX; ++e) {
         if (e < E) {
@@ -1268,25 +1284,37 @@ __device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, in
                 double sl;
                 if constexpr (SMEM) sl = (e < HALF ? slo : shi)[(e % HALF) * NT + tid];
                 else sl = sreg[e];
-                const double zeroed = zacc;
                 const double inv_above = suf + sl;             // both >= 0: no cancellation
-                const double risk = zeroed + m * m * cnt - nt + tau * (2.0 * cnt - m * inv_above);
-                consider(best, risk, m, cnt, inv_above);
-                if (cnt > 0) {
-                    // stationary point ts = tau*inv/(2 cnt) inside (m, nxt)?  Pre-test by
-                    // multiplication with a relative guard, divide only for survivors.
-                    const double ti = tau * inv_above, c2 = 2.0 * cnt;
-                    if (ti > c2 * m * (1.0 - 1e-12) && ti < c2 * nxt * (1.0 + 1e-12)) {
-                        const double ts = ti / c2;
-                        if (ts > m && ts < nxt) {
-                            const double rs = zeroed + ts * ts * cnt - nt + tau * (2.0 * cnt - ts * inv_above);
-                            consider(best, rs, ts, cnt, inv_above);
-                        }
+                const double risk = zacc + m * m * cnt - nt + tau * (2.0 * cnt - m * inv_above);
+                if (risk < brisk) { brisk = risk; bcode = 2 * e; }
+                // stationary point ts = tau*inv/(2 cnt) inside (m, nxt)?  Pre-test by
+                // multiplication with a relative guard, divide only for survivors.
+                const double ti = tau * inv_above, c2 = 2.0 * cnt;
+                if (cnt > 0 && ti > c2 * m * (1.0 - 1e-12) && ti < c2 * nxt * (1.0 + 1e-12)) {
+                    const double ts = div_pos(ti, c2);
+                    if (ts > m && ts < nxt) {
+                        const double rs = zacc + ts * ts * cnt - nt + tau * (2.0 * cnt - ts * inv_above);
+                        if (rs < brisk) { brisk = rs; bcode = 2 * e + 1; }
                     }
                 }
             }
             m = nxt;
         }
+    }
+    if (bcode >= 0) {
+        const int e = bcode >> 1, il = b0 + e;
+        double sl;
+        if constexpr (SMEM) sl = (e < HALF ? slo : shi)[(e % HALF) * NT + tid];
+        else {
+            sl = 0.0;
+#pragma unroll
+            for (int q = 0; q < EMAX; ++q) if (q == e) sl = sreg[q];
+        }
+        const double inv_above = suf + sl;
+        const double c = (double)(n - (tilebase + il + 1));
+        const double mk = (double)keys[KI(il)];
+        const double t = (bcode & 1) ? div_pos(tau * inv_above, 2.0 * c) : mk;
+        best = Best{brisk, t, c, inv_above};
     }
 }
 
