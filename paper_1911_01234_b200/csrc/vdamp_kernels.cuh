@@ -664,6 +664,15 @@ struct Best { double risk, t, cnt, inv; };
 // call forces register spills in the select kernels): hardware approximation
 // plus two FMA Newton steps (within 1 ulp); extreme magnitudes are
 // rescaled by an exact power of two first.
+// m holds a float value (any positive float, denormals included, is a normal
+// double whose reciprocal is a normal double): no rescaling needed
+__device__ __forceinline__ double rcp_posf(double m) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(m));
+    double e = fma(-m, r, 1.0); r = fma(r, e, r);
+    e = fma(-m, r, 1.0); return fma(r, e, r);
+}
+
 __device__ __forceinline__ double rcp_pos(double m) {
     double sc = 1.0;
     if (m < 1e-300) { m *= 0x1p600; sc = 0x1p600; }           // exact power-of-two rescaling
@@ -1169,7 +1178,7 @@ __device__ R* global_merge_sort(R* A, R* B, R* smem, int n, int CAP) {
 // Evaluate the candidates owned by this thread on one tile of sorted
 // magnitudes (src/denoise.py:62-118):  candidate t = m_i at the end of each
 // tie run, plus the stationary point of the quadratic piece that starts there.
-template <typename R, int NT, int EMAX, bool SMEM>
+template <typename R, int NT, int EMAX, bool SMEM, int EFIX>
 __device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, int n, double tau, int b0, int E,
                                           double pre, double suf, double next_tile_first, Best& best,
                                           const double* sreg, const double* slo, const double* shi);
@@ -1180,7 +1189,7 @@ __device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, in
 // cancels.  The per-key suffixes go to shared scratch (slo/shi, key e of thread
 // t at [e * NT + t], conflict-free; keys e >= EMAX/2 in shi) when SMEM, to
 // registers otherwise (small E only: a register array of 16 doubles spills).
-template <typename R, int NT, int EMAX, bool SMEM>
+template <typename R, int NT, int EMAX, bool SMEM, int EFIX = 0>
 __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, int n, double tau,
                                           double pre_tile, double suf_tile, double next_tile_first,
                                           double* sh, Best* wbest, Best* run, double* totinv, double* slo,
@@ -1193,22 +1202,24 @@ __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, in
 #else
 #define SC_MARK(i) do { } while (0)
 #endif
-    const int E = T >= NT ? T / NT : 1;
-    const bool act = tid * E < T;
+    // EFIX > 0: T == NT * EFIX known at compile time (fully unrolled, unguarded)
+    const int E = EFIX ? EFIX : (T >= NT ? T / NT : 1);
+    const bool act = EFIX ? true : tid * E < T;
     const int b0 = tid * E;
     constexpr int HALF = EMAX / 2 > 0 ? EMAX / 2 : 1;
+    constexpr bool FKEY = sizeof(R) == 4;
     double ssq = 0.0, sinv = 0.0;
     double sreg[SMEM ? 1 : EMAX];
     if (act) {
         // one conversion per key (F2F/I2F/MUFU issue at 1/4 of the DFMA rate)
-#pragma unroll (SMEM ? 4 : EMAX)
+#pragma unroll ((SMEM && !EFIX) ? 4 : EMAX)
         for (int e = EMAX - 1; e >= 0; --e) {
             if (e < E) {
                 if constexpr (SMEM) (e < HALF ? slo : shi)[(e % HALF) * NT + tid] = sinv;
                 else sreg[e] = sinv;
                 const double m = (double)keys[KI(b0 + e)];
                 ssq = fma(m, m, ssq);
-                if (m > 0) sinv += rcp_pos(m);
+                if (m > 0) sinv += FKEY ? rcp_posf(m) : rcp_pos(m);
             }
         }
     }
@@ -1217,7 +1228,7 @@ __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, in
     const double suf = block_excl_scan<NT, true>(sinv, sh) + suf_tile;
     if (tid == 0 && tilebase == 0) *totinv = suf + sinv;     // sum of all inverses
     SC_MARK(1);
-    if (act) scan_keys<R, NT, EMAX, SMEM>(keys, T, tilebase, n, tau, b0, E, pre, suf, next_tile_first, best,
+    if (act) scan_keys<R, NT, EMAX, SMEM, EFIX>(keys, T, tilebase, n, tau, b0, E, pre, suf, next_tile_first, best,
                                           sreg, slo, shi);
     // tile argmin (ties -> smaller t) merged into the running best by thread 0
     for (int o = 16; o > 0; o >>= 1) {
@@ -1261,7 +1272,7 @@ __device__ __forceinline__ double div_pos(double a, double b) {
 // the loop; the winner's (t, count, inverse sum) are rebuilt afterwards.
 // Candidates arrive in increasing t, so a strict '<' keeps the smaller t of
 // a tie.
-template <typename R, int NT, int EMAX, bool SMEM>
+template <typename R, int NT, int EMAX, bool SMEM, int EFIX>
 __device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, int n, double tau, int b0, int E,
                                           double pre, double suf, double next_tile_first, Best& best,
                                           const double* sreg, const double* slo, const double* shi) {
@@ -1535,14 +1546,21 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             __syncthreads();
         }
         const double nf = (t + 1 < ntl) ? (double)sorted[(t + 1) * CAPK] : INFINITY;
-        scan_tile<R, NT, EMAXS, SMEMSUF>(large ? keys : skeys, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, s_best,
-                                          &S_.run, &s_totinv, slo, shi,
 #ifdef VDAMP_PHASE_TIMING
-                                          bi < 4096 ? &g_scan[bi][j][0] : nullptr
+        long long* sdbg = bi < 4096 ? &g_scan[bi][j][0] : nullptr;
 #else
-                                          nullptr
+        long long* sdbg = nullptr;
 #endif
-                                          );
+        const R* tk = large ? keys : skeys;
+        if (SMEMSUF && T == NT * 16)
+            scan_tile<R, NT, EMAXS, SMEMSUF, SMEMSUF ? 16 : 0>(tk, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, s_best,
+                                                               &S_.run, &s_totinv, slo, shi, sdbg);
+        else if (SMEMSUF && T == NT * 4)
+            scan_tile<R, NT, EMAXS, SMEMSUF, SMEMSUF ? 4 : 0>(tk, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, s_best,
+                                                              &S_.run, &s_totinv, slo, shi, sdbg);
+        else
+            scan_tile<R, NT, EMAXS, SMEMSUF>(tk, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, s_best, &S_.run,
+                                             &s_totinv, slo, shi, sdbg);
     }
     // candidate t = 0 when no magnitude is zero (src/denoise.py:84)
     __syncthreads();
