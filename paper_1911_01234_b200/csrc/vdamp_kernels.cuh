@@ -16,6 +16,7 @@
 // modulation; the output sign is folded into y at setup.
 #pragma once
 #include "vdamp_device.cuh"
+#include <type_traits>
 
 namespace vdamp {
 
@@ -835,12 +836,14 @@ __device__ long long g_csort[4096][64][6];
 
 constexpr int CS_MAXB = 256;      // larger fine buckets -> comparison-sort fallback (heavy ties)
 
-__device__ __forceinline__ unsigned cs_fine(unsigned k, int lc, unsigned cb, const unsigned* tab) {
+// fine bucket of key k (a coarse bucket with an empty run, w = 0, sends its keys
+// to the next run's first bucket: still monotone; clamped to the last bucket)
+__device__ __forceinline__ unsigned cs_fine(unsigned k, int lc, unsigned cb, const unsigned* tab, unsigned last) {
     if (!k) return 0u;
     const unsigned c = (k >> lc) - cb;
     const unsigned t = tab[c];
     const unsigned long long off = (unsigned long long)(k - ((cb + c) << lc)) * (t >> 16);
-    return 1u + (t & 0xffffu) + (unsigned)(off >> lc);
+    return min(1u + (t & 0xffffu) + (unsigned)(off >> lc), last);
 }
 
 __device__ __forceinline__ void sort16(unsigned (&v)[16]) {
@@ -864,8 +867,11 @@ __device__ __forceinline__ void sort16(unsigned (&v)[16]) {
 
 // 0: some bucket holds more than CS_MAXB keys (nothing usable; the caller
 // bitonic-sorts `keys`); 1: sorted keys in `out`; 2: sorted keys in `keys`.
-template <int NT>
-__device__ int counting_sort(const float* keys, float* out, unsigned* cnt, int n, double* sh, long long* dbg = nullptr) {
+// n == EF * NT (EF keys per thread, compile time); mn / mx: this thread's
+// min nonzero / max key bits (from the key-building loop)
+template <int NT, int EF>
+__device__ int counting_sort(const float* keys, float* out, unsigned* cnt, int n, unsigned mn, unsigned mx,
+                             double* sh, long long* dbg = nullptr) {
     static_assert(CS_COARSE % NT == 0 && NT <= CS_COARSE, "coarse scan: whole coarse buckets per thread");
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 #ifdef VDAMP_PHASE_TIMING
@@ -877,12 +883,6 @@ __device__ int counting_sort(const float* keys, float* out, unsigned* cnt, int n
     unsigned* tab = hc + CS_COARSE;                  // coarse bucket -> fine start | width << 16
     const int nbf = n >= CS_FINE ? CS_FINE : (int)(1u << (32 - __clz((unsigned)n - 1u)));
     const int words = nbf >> 1;
-    unsigned mn = 0xffffffffu, mx = 0;
-    for (int i = tid; i < n; i += NT) {
-        const unsigned k = kb[KI(i)];
-        if (k) mn = min(mn, k);
-        mx = max(mx, k);
-    }
     for (int o = 16; o > 0; o >>= 1) {
         mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
         mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -904,14 +904,20 @@ __device__ int counting_sort(const float* keys, float* out, unsigned* cnt, int n
     __syncthreads();
     mn = red[64]; mx = red[65];
     if (mn > mx) mn = mx;                            // all zeros
-    int lc = 0;
-    while (((mx >> lc) - (mn >> lc)) >= (unsigned)CS_COARSE) ++lc;
+    // smallest shift lc with (mx >> lc) - (mn >> lc) < CS_COARSE (= 2^10)
+    const unsigned dd = mx - mn;
+    int lc = dd < (unsigned)CS_COARSE ? 0 : (32 - __clz(dd)) - 10;
+    if (((mx >> lc) - (mn >> lc)) >= (unsigned)CS_COARSE) ++lc;
     const unsigned cb = mn >> lc;
     // coarse histogram of the nonzero keys
-    for (int i = tid; i < n; i += NT) {
-        const unsigned k = kb[KI(i)];
-        if (k) atomicAdd(&hc[(k >> lc) - cb], 1u);
-    }
+    unsigned kr[EF];
+#pragma unroll
+    for (int e = 0; e < EF; ++e) kr[e] = kb[KI(tid + e * NT)];
+    // (a 1-in-4 sample would save atomics, but its noisier map pushes buckets
+    // past 8 keys and into the slow ranking pass: measured slower)
+#pragma unroll
+    for (int e = 0; e < EF; ++e)
+        if (kr[e]) atomicAdd(&hc[(kr[e] >> lc) - cb], 1u);
     __syncthreads();
     CS_MARK(0);
     // coarse bucket t -> fine run [fs, fs + w) of the nbf - 1 nonzero buckets,
@@ -925,49 +931,44 @@ __device__ int counting_sort(const float* keys, float* out, unsigned* cnt, int n
         if (tid == NT - 1) red[66] = P + hs;
         __syncthreads();
         const unsigned tot = red[66];
-        const unsigned F = (unsigned)nbf - 1u;
+        // fine start = floor(P * F / tot) through one double scale factor: monotone
+        // in P and within [0, F], so runs never overlap (no 64-bit integer division)
+        const double scl = tot ? (double)(nbf - 1) / (double)tot : 0.0;
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
-            unsigned fs = 0, fe = 0;
-            if (tot) {
-                fs = (unsigned)(((unsigned long long)P * F) / tot);
-                fe = (unsigned)(((unsigned long long)(P + h[q]) * F) / tot);
-            }
+            const unsigned fs = __double2uint_rz((double)P * scl);
+            const unsigned fe = __double2uint_rz((double)(P + h[q]) * scl);
             tab[tid * CPT + q] = fs | ((fe - fs) << 16);
             P += h[q];
         }
     }
     __syncthreads();
     // fine histogram
-    for (int i = tid; i < n; i += NT) {
-        const unsigned b = cs_fine(kb[KI(i)], lc, cb, tab);
+#pragma unroll
+    for (int e = 0; e < EF; ++e) {
+        const unsigned b = cs_fine(kr[e], lc, cb, tab, (unsigned)nbf - 1u);
         atomicAdd(&cnt[b >> 1], 1u << ((b & 1u) * 16));
     }
     __syncthreads();
     CS_MARK(1);
+    // exclusive scan of the fine counts (thread t: words [t*per, t*per + per)),
+    // with the crowded-bucket flags folded into the same pass
     bool crowd8;
-    {
-        unsigned big = 0, c8 = 0;
-        for (int i = tid; i < words; i += NT) {
-            const unsigned v = cnt[i];
-            const unsigned lo16 = i ? (v & 0xffffu) : 0u;            // bucket 0: zeros, always in order
-            big |= (lo16 > (unsigned)CS_MAXB) | ((v >> 16) > (unsigned)CS_MAXB);
-            c8 |= (lo16 > 8u) | ((v >> 16) > 8u);
-        }
-        if (__syncthreads_or(big)) return 0;
-        crowd8 = __syncthreads_or(c8) != 0;
-    }
-    // exclusive scan of the fine counts (thread t: words [t*per, t*per + per))
     {
         constexpr int PMAX = CS_FINE / 2 / NT;
         const int per = words / NT;
         unsigned v[PMAX];
-        unsigned tot = 0;
+        unsigned tot = 0, big = 0, c8 = 0;
 #pragma unroll
         for (int i = 0; i < PMAX; ++i) {
             v[i] = i < per ? cnt[tid * per + i] : 0u;
             tot += (v[i] & 0xffffu) + (v[i] >> 16);
+            const unsigned lo16 = (tid * per + i) ? (v[i] & 0xffffu) : 0u;   // bucket 0: zeros, in order
+            big |= (lo16 > (unsigned)CS_MAXB) | ((v[i] >> 16) > (unsigned)CS_MAXB);
+            c8 |= (lo16 > 8u) | ((v[i] >> 16) > 8u);
         }
+        if (__syncthreads_or(big)) return 0;
+        crowd8 = __syncthreads_or(c8) != 0;
         unsigned run = (unsigned)block_excl_scan<NT, false>((double)tot, sh + 66);
 #pragma unroll
         for (int i = 0; i < PMAX; ++i) {
@@ -981,9 +982,10 @@ __device__ int counting_sort(const float* keys, float* out, unsigned* cnt, int n
     __syncthreads();
     CS_MARK(2);
     // scatter (cursor = packed 16-bit half, never carries: offsets + counts <= n <= 16384)
-    for (int i = tid; i < n; i += NT) {
-        const unsigned k = kb[KI(i)];
-        const unsigned b = cs_fine(k, lc, cb, tab);
+#pragma unroll
+    for (int e = 0; e < EF; ++e) {
+        const unsigned k = kr[e];
+        const unsigned b = cs_fine(k, lc, cb, tab, (unsigned)nbf - 1u);
         const unsigned sft = (b & 1u) * 16;
         const unsigned old = atomicAdd(&cnt[b >> 1], 1u << sft);
         ob[KI((old >> sft) & 0xffffu)] = k;
@@ -1016,7 +1018,7 @@ __device__ int counting_sort(const float* keys, float* out, unsigned* cnt, int n
     unsigned* fb = const_cast<unsigned*>(kb);
     for (int i = tid; i < n; i += NT) {
         const unsigned x = ob[KI(i)];
-        const unsigned bk = cs_fine(x, lc, cb, tab);
+        const unsigned bk = cs_fine(x, lc, cb, tab, (unsigned)nbf - 1u);
         const unsigned e1 = cnt[bk >> 1] >> ((bk & 1u) * 16) & 0xffffu;
         unsigned s0 = 0;
         if (bk > 0) { const unsigned bp = bk - 1u; s0 = cnt[bp >> 1] >> ((bp & 1u) * 16) & 0xffffu; }
@@ -1409,16 +1411,30 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
                          bytes - o < 32768u ? bytes - o : 32768u, &S_.mbar);
         }
         mbar_wait(&S_.mbar, S_.mphase);
-        for (int e = tid; e < T; e += NT) {
-            const C v = cz[e];
-            keys[KI(e)] = cmag(v);
-            if (w0) {
-                const C w = w0[e];
-                const double dx = (double)v.x - (double)w.x, dy = (double)v.y - (double)w.y;
-                err += dx * dx + dy * dy;
-                ref += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
+        unsigned kmn = 0xffffffffu, kmx = 0;                      // key-bit range for the counting sort
+        auto build = [&](auto efc) {
+            constexpr int EF = decltype(efc)::value;
+#pragma unroll
+            for (int q = 0; q < EF; ++q) {
+                const int e = tid + q * NT;
+                const C v = cz[e];
+                const float kf = (float)cmag(v);
+                keys[KI(e)] = (R)kf;
+                const unsigned u = __float_as_uint(kf);
+                if (u) kmn = min(kmn, u);
+                kmx = max(kmx, u);
+                if (w0) {
+                    const C w = w0[e];
+                    const double dx = (double)v.x - (double)w.x, dy = (double)v.y - (double)w.y;
+                    err += dx * dx + dy * dy;
+                    ref += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
+                }
             }
-        }
+        };
+        const int ef = T / NT;
+        if (ef == 16) build(std::integral_constant<int, 16>{});
+        else if (ef == 8) build(std::integral_constant<int, 8>{});
+        else build(std::integral_constant<int, 4>{});
         __syncthreads();
         if (tid == 0) S_.mphase ^= 1u;
         if (!a.tau_in && tid == 0) {
@@ -1433,7 +1449,11 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
 #else
             long long* dbg = nullptr;
 #endif
-            const int cs = counting_sort<NT>(reinterpret_cast<const float*>(keys), reinterpret_cast<float*>(stage), ccnt, T, sh, dbg);
+            const float* kf = reinterpret_cast<const float*>(keys);
+            float* of = reinterpret_cast<float*>(stage);
+            const int cs = ef == 16 ? counting_sort<NT, SCAP / NT>(kf, of, ccnt, T, kmn, kmx, sh, dbg)
+                         : ef == 8  ? counting_sort<NT, (SCAP / NT) / 2>(kf, of, ccnt, T, kmn, kmx, sh, dbg)
+                                    : counting_sort<NT, (SCAP / NT) / 4>(kf, of, ccnt, T, kmn, kmx, sh, dbg);
             if (cs == 1) skeys = stage;
             else if (cs == 0) block_sort<R, NT>(keys, T);
         }
