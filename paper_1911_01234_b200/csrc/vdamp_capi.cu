@@ -149,6 +149,30 @@ struct Launch {
     }
 };
 
+// Launch with programmatic dependent launch (PDL): the kernel may start while
+// the previous kernel in the stream drains; every PDL kernel executes
+// griddepcontrol.wait before its first global memory access, so ordering and
+// visibility are those of a plain stream launch.  Off via VDAMP_PDL=0.
+static bool pdl_enabled() {
+    static const bool on = [] { const char* e = getenv("VDAMP_PDL"); return !(e && atoi(e) == 0); }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t sm, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+}
+
 // Opt every kernel into the dynamic shared memory it is launched with (static
 // shared memory counts against the default 48 KB too), once per kernel/size.
 // add the elapsed times of recorded event pairs to the per-class totals
@@ -215,11 +239,11 @@ struct Seq {
                 auto k = synth_pass<R, SYN_ROWFFT>;
                 const size_t smf = sm + (size_t)p->W * sizeof(C);
                 set_smem(k, smf);
-                k<<<grid, PNT, smf, st>>>(p->geo, a);
+                launch(k, grid, PNT, smf, st, p->geo, a);
             } else {
                 auto k = synth_pass<R, SYN_PLAIN>;
                 set_smem(k, sm);
-                k<<<grid, PNT, sm, st>>>(p->geo, a);
+                launch(k, grid, PNT, sm, st, p->geo, a);
             }
         }
     }
@@ -246,18 +270,18 @@ struct Seq {
                 sm += (size_t)p->W * sizeof(C);
                 if (vdamp_mode) {
                     auto k = analysis_pass<R, ANA_IN_ROWIFFT, ANA_OUT_VDAMP>; set_smem(k, sm);
-                    k<<<grid, PNT, sm, st>>>(p->geo, a);
+                    launch(k, grid, PNT, sm, st, p->geo, a);
                 } else {
                     auto k = analysis_pass<R, ANA_IN_ROWIFFT, ANA_OUT_COEF>; set_smem(k, sm);
-                    k<<<grid, PNT, sm, st>>>(p->geo, a);
+                    launch(k, grid, PNT, sm, st, p->geo, a);
                 }
             } else {
                 if (vdamp_mode) {
                     auto k = analysis_pass<R, ANA_IN_PLAIN, ANA_OUT_VDAMP>; set_smem(k, sm);
-                    k<<<grid, PNT, sm, st>>>(p->geo, a);
+                    launch(k, grid, PNT, sm, st, p->geo, a);
                 } else {
                     auto k = analysis_pass<R, ANA_IN_PLAIN, ANA_OUT_COEF>; set_smem(k, sm);
-                    k<<<grid, PNT, sm, st>>>(p->geo, a);
+                    launch(k, grid, PNT, sm, st, p->geo, a);
                 }
             }
         }
@@ -281,12 +305,12 @@ struct Seq {
         const size_t sm = col_smem();
         Launch L(p, cls, st);
         switch (mode) {
-            case COL_FWD:   { auto k = col_pass<R, COL_FWD>;   set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
-            case COL_INV:   { auto k = col_pass<R, COL_INV>;   set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
-            case COL_VDAMP: { auto k = col_pass<R, COL_VDAMP>; set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
-            case COL_RAW:   { auto k = col_pass<R, COL_RAW>;   set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
-            case COL_NMSE:  { auto k = col_pass<R, COL_NMSE>;  set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
-            default:        { auto k = col_pass<R, COL_FINAL>; set_smem(k, sm); k<<<grid, PNT, sm, st>>>(p->geo, a); break; }
+            case COL_FWD:   { auto k = col_pass<R, COL_FWD>;   set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
+            case COL_INV:   { auto k = col_pass<R, COL_INV>;   set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
+            case COL_VDAMP: { auto k = col_pass<R, COL_VDAMP>; set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
+            case COL_RAW:   { auto k = col_pass<R, COL_RAW>;   set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
+            case COL_NMSE:  { auto k = col_pass<R, COL_NMSE>;  set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
+            default:        { auto k = col_pass<R, COL_FINAL>; set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
         }
     }
 
@@ -342,12 +366,12 @@ struct Seq {
                 constexpr int BNT = sizeof(R) == 4 ? BNT32 : BNT64;
                 auto k = sure_select<R, BNT>;
                 set_smem(k, sm);
-                k<<<grid, BNT, sm, ls>>>(p->geo, a);
+                launch(k, grid, BNT, sm, ls, p->geo, a);
             } else {
                 const size_t sm = (size_t)(SMALL_N + SMALL_N / 32 + 2) * sizeof(R);
                 auto k = sure_select<R, SNT_SMALL>;
                 set_smem(k, sm);
-                k<<<grid, SNT_SMALL, sm, ls>>>(p->geo, a);
+                launch(k, grid, SNT_SMALL, sm, ls, p->geo, a);
             }
         }
         if (forked) {

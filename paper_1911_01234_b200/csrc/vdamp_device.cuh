@@ -453,4 +453,12 @@ __device__ __forceinline__ double block_excl_scan(double v, double* sh) {
     return r;
 }
 
+// programmatic dependent launch: wait for the preceding grid (no-op when the
+// kernel was launched without the PDL attribute), then let the next grid start
+// its CTAs as SMs free up
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace vdamp

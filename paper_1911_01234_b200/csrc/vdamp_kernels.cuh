@@ -141,6 +141,7 @@ __device__ __forceinline__ void gather_coarse(const Geo& g, const SynArgs<R>& p,
 
 template <typename R, int MODE>
 __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) synth_pass(Geo g, SynArgs<R> p) {
+    pdl_enter();
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* buf = reinterpret_cast<C*>(smem_raw);
@@ -274,6 +275,7 @@ struct AnaArgs {
 
 template <typename R, int IN, int OUT>
 __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) analysis_pass(Geo g, AnaArgs<R> p) {
+    pdl_enter();
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* buf = reinterpret_cast<C*>(smem_raw);
@@ -468,6 +470,7 @@ __device__ __forceinline__ void band_profiles(int s, int j, int& prow, int& pcol
 
 template <typename R, int MODE>
 __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass(Geo g, ColArgs<R> p) {
+    pdl_enter();
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* buf = reinterpret_cast<C*>(smem_raw);
@@ -1621,6 +1624,7 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
 
 template <typename R, int NT>
 __global__ void __launch_bounds__(NT, NT >= BNT32 ? 1 : 4) sure_select(Geo g, SelArgs<R> a) {
+    pdl_enter();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     R* keys = reinterpret_cast<R*>(smem_raw);
     __shared__ SelShared<NT> S_;
