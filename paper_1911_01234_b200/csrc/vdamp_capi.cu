@@ -288,10 +288,13 @@ struct Seq {
     }
 
     size_t col_smem() const {
+        // tile buffer + twiddles; the tau partials and row profiles reuse the tile
+        // buffer after the outputs are stored (the NMSE mode's block sum sits past the twiddles)
         const int np = 2 * p->s;
         const size_t E = (size_t)p->H << p->logcw;
-        return E * sizeof(C) + (size_t)p->H * sizeof(C) + (size_t)np * PNT * sizeof(double) +
-               (size_t)np * p->cw * sizeof(double) + (size_t)np * p->H * sizeof(R);
+        const size_t tau = (size_t)np * PNT * sizeof(double) + (size_t)np * p->cw * sizeof(double) +
+                           (size_t)np * p->H * sizeof(R);
+        return std::max(E * sizeof(C), tau) + (size_t)p->H * sizeof(C) + (PNT / 32 + 2) * sizeof(double);
     }
 
     void col(int mode, const C* src, C* dst, int cls) {

@@ -140,7 +140,7 @@ __device__ __forceinline__ void gather_coarse(const Geo& g, const SynArgs<R>& p,
 }
 
 template <typename R, int MODE>
-__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) synth_pass(Geo g, SynArgs<R> p) {
+__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth_pass(Geo g, SynArgs<R> p) {
     pdl_enter();
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -274,7 +274,7 @@ struct AnaArgs {
 };
 
 template <typename R, int IN, int OUT>
-__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) analysis_pass(Geo g, AnaArgs<R> p) {
+__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis_pass(Geo g, AnaArgs<R> p) {
     pdl_enter();
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -584,7 +584,10 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass(Geo g, C
     // of each column in a fixed order (deterministic)
     // per-thread sums over its <= 16 rows in the working precision (float in
     // fp32 mode: 1e-7 relative), thread and column combination in float64
-    double* part = reinterpret_cast<double*>(tws + H);   // [np][PNT] thread partials
+    // the tile buffer is free once every thread has stored its outputs: the
+    // partials and row profiles reuse it (keeps the CTA at 34 KB of smem)
+    __syncthreads();
+    double* part = reinterpret_cast<double*>(buf);       // [np][PNT] thread partials
     R* prs = reinterpret_cast<R*>(part + np * PNT + np * cw);   // [np][H] row profiles
     for (int i = tid; i < np * H; i += PNT) prs[i] = (R)p.prow[i];
     __syncthreads();
