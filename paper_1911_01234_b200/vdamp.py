@@ -297,3 +297,67 @@ class BatchReconstructor:
             import torch
             torch.cuda.current_stream(p.device).synchronize() if stream is None else stream.synchronize()
         return x
+
+
+class StreamingReconstructor:
+    """Pipelined batches: host->device copies of batch k+1 and the device->host
+    copy of batch k-1 overlap the reconstruction of batch k.
+
+    ``submit`` takes pinned host tensors (see :meth:`BatchReconstructor.upload`)
+    and a pinned host ``out`` tensor (B, H, W); it returns at once.  ``wait``
+    blocks until every submitted batch has landed in its ``out``.  Inputs of a
+    submitted batch must not be modified until its copy has finished (two
+    batches in flight at most; ``submit`` blocks beyond that).
+    """
+
+    def __init__(self, height, width, scales, batch, *, precision="fp32", device=None):
+        import torch
+        from .plan import get_plan
+        SubbandLayout.create(height, width, scales)
+        self.plan = get_plan(height, width, scales, batch, precision, device)
+        dev = self.plan.device
+        self.compute = torch.cuda.Stream(dev)
+        self.copy = torch.cuda.Stream(dev)          # host -> device
+        self.copy_out = torch.cuda.Stream(dev)      # device -> host (never queued behind an upload)
+        self._x = [self.plan.empty_images(), self.plan.empty_images()]
+        self._stage = [None, None]
+        self._ev_used = [None, None]        # compute finished reading stage / writing x of slot
+        self._ev_out = [None, None]         # D2H of slot finished
+        self._k = 0
+
+    upload = BatchReconstructor.upload
+
+    def submit(self, host, n_iters, out):
+        import torch
+        if n_iters < 1:
+            raise ValueError(f"need at least one iteration, got {n_iters}")
+        p, s = self.plan, self._k & 1
+        self._k += 1
+        if self._ev_out[s] is not None:
+            self._ev_out[s].synchronize()      # slot s (stage and x) free again
+        with torch.cuda.stream(self.copy):
+            st = dict(y=host["y"].to(p.device, non_blocking=True),
+                      indices=host["indices"].to(p.device, non_blocking=True),
+                      probs=host["probs"].to(p.device, non_blocking=True))
+            ev_in = torch.cuda.Event()
+            ev_in.record(self.copy)
+        self._stage[s] = st
+        self.compute.wait_event(ev_in)
+        with torch.cuda.stream(self.compute):
+            p.set_measurements(st["y"], st["indices"], host["counts"], st["probs"], host["noise_var"],
+                               host.get("shared_probs", True), stream=self.compute)
+            p.run(n_iters, x_hat=self._x[s], stream=self.compute)
+            ev_done = torch.cuda.Event()
+            ev_done.record(self.compute)
+        self.copy_out.wait_event(ev_done)
+        with torch.cuda.stream(self.copy_out):
+            out.copy_(self._x[s], non_blocking=True)
+            ev_out = torch.cuda.Event()
+            ev_out.record(self.copy_out)
+        self._ev_out[s] = ev_out
+        return out
+
+    def wait(self):
+        for e in self._ev_out:
+            if e is not None:
+                e.synchronize()

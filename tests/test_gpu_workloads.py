@@ -185,3 +185,23 @@ def test_parseval_nmse_matches_finalize_path(cfg0_small):
         res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True)
         out[v] = np.array(eval(res.stdout.strip().splitlines()[-1]))
     assert np.abs(out["1"] - out["0"]).max() <= 1e-8
+
+
+def test_streaming_reconstructor_matches_sync():
+    """Pipelined submissions (copies overlapping the neighbouring batches) give
+    the synchronous call's results bitwise, for several batches in flight."""
+    import torch
+    from paper_1911_01234_b200 import vdamp, workload
+    w = workload.make_workload("cfg1", batch=4)
+    inp = vdamp.prepare_batch(w.ys, w.masks, w.pmap, w.noise_vars)
+    cfg = w.config
+    rec = vdamp.BatchReconstructor(cfg.size, cfg.size, cfg.scales, 4, precision="fp32")
+    host = rec.upload(inp, pin=True)
+    ref = rec(host["y"], host["indices"], host["counts"], host["probs"], host["noise_var"], 5).cpu().clone()
+    srec = vdamp.StreamingReconstructor(cfg.size, cfg.size, cfg.scales, 4, precision="fp32")
+    outs = [torch.empty(ref.shape, dtype=ref.dtype).pin_memory() for _ in range(3)]
+    for i in range(5):
+        srec.submit(host, 5, outs[i % 3])
+    srec.wait()
+    for o in outs:
+        assert torch.equal(o, ref)
