@@ -1417,6 +1417,9 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
                          bytes - o < 32768u ? bytes - o : 32768u, &S_.mbar);
         }
         mbar_wait(&S_.mbar, S_.mphase);
+#ifdef VDAMP_PHASE_TIMING
+        if (tid == 0 && bi < 4096) g_csort[bi][j][5] = clock64() - ph0_;   // TMA landed
+#endif
         unsigned kmn = 0xffffffffu, kmx = 0;                      // key-bit range for the counting sort
         auto build = [&](auto efc) {
             constexpr int EF = decltype(efc)::value;

@@ -24,7 +24,9 @@ for j in range(S):
 buf2 = (ctypes.c_longlong * (64 * 64 * 6))()
 lib.vdamp_debug_csort_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
 _lib.check(lib.vdamp_debug_csort_times(buf2, 64))
-c = np.frombuffer(buf2, dtype=np.int64).reshape(64, 64, 6)[:nb, S - 3:S, :5].mean((0, 1))
+c6 = np.frombuffer(buf2, dtype=np.int64).reshape(64, 64, 6)[:nb, S - 3:S, :]
+print("TMA landed after %.0f cycles (16384-key subbands)" % c6[..., 5].mean())
+c = c6[..., :5].mean((0, 1))
 print("counting sort (n=16384) cycles: minmax+coarse %.0f  table+fine hist %.0f  check+scan %.0f  scatter %.0f  bucket sort %.0f" % tuple(c))
 
 buf3 = (ctypes.c_longlong * (64 * 64 * 5))()
