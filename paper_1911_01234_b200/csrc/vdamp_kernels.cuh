@@ -798,7 +798,7 @@ template <typename R, int NT>
 __device__ void block_sort(R* s, int n) {
     if (n < 2) { __syncthreads(); return; }
     int E = n / NT;
-    const int small = n / 32 < 8 ? n / 32 : 8;
+    const int small = n / 32 < 4 ? n / 32 : 4;
     if (E < small) E = small;
     if (E < 1) E = 1;
     switch (E) {
