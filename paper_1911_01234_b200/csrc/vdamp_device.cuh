@@ -63,118 +63,6 @@ __device__ __forceinline__ C onsager(C r, R t, R alpha, R gain) {
 }
 
 // ---------------------------------------------------------------------------
-// Stockham radix-4/2 FFT over `nseq` sequences of length L held in shared
-// memory. Element e of sequence q lives at buf[q*sstr + e*estr].  Every
-// thread keeps its butterflies in registers between the load and the store
-// half of a pass, so the transform is in place.  SEQ_FAST maps consecutive
-// threads to consecutive sequences (column tiles: conflict-free), otherwise
-// to consecutive elements of one sequence (rows).  tw[m] = exp(-2 pi i m / L).
-// ---------------------------------------------------------------------------
-template <typename C, bool INV, int NT, int MAXB, bool SEQ_FAST>
-__device__ __forceinline__ void fft_pass_r4(C* buf, int logL, int logNs, int lognseq,
-                                            int sstr, int estr, const C* tw) {
-    const int logQ = logL - 2;
-    const int Q = 1 << logQ;
-    const int Ns = 1 << logNs;
-    const int total = 1 << (lognseq + logQ);
-    const int twshift = logL - logNs - 2;
-    C v[MAXB][4];
-#pragma unroll
-    for (int i = 0; i < MAXB; ++i) {
-        int bf = threadIdx.x + i * NT;
-        if (bf < total) {
-            int q, j;
-            if (SEQ_FAST) { q = bf & ((1 << lognseq) - 1); j = bf >> lognseq; }
-            else          { q = bf >> logQ; j = bf & (Q - 1); }
-            const C* base = buf + q * sstr;
-            int k = j & (Ns - 1);
-            C a0 = base[(j) * estr];
-            C a1 = base[(j + Q) * estr];
-            C a2 = base[(j + 2 * Q) * estr];
-            C a3 = base[(j + 3 * Q) * estr];
-            if (k) {
-                C w1 = tw[(k) << twshift], w2 = tw[(2 * k) << twshift], w3 = tw[(3 * k) << twshift];
-                if (INV) { w1 = cconj(w1); w2 = cconj(w2); w3 = cconj(w3); }
-                a1 = cmul(a1, w1); a2 = cmul(a2, w2); a3 = cmul(a3, w3);
-            }
-            C b0 = cadd(a0, a2), b1 = csub(a0, a2), b2 = cadd(a1, a3);
-            C b3 = cmul_mi<C, INV>(csub(a1, a3));
-            v[i][0] = cadd(b0, b2);
-            v[i][1] = cadd(b1, b3);
-            v[i][2] = csub(b0, b2);
-            v[i][3] = csub(b1, b3);
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < MAXB; ++i) {
-        int bf = threadIdx.x + i * NT;
-        if (bf < total) {
-            int q, j;
-            if (SEQ_FAST) { q = bf & ((1 << lognseq) - 1); j = bf >> lognseq; }
-            else          { q = bf >> logQ; j = bf & (Q - 1); }
-            C* base = buf + q * sstr;
-            int k = j & (Ns - 1);
-            int d = ((j - k) << 2) + k;
-            base[(d) * estr] = v[i][0];
-            base[(d + Ns) * estr] = v[i][1];
-            base[(d + 2 * Ns) * estr] = v[i][2];
-            base[(d + 3 * Ns) * estr] = v[i][3];
-        }
-    }
-    __syncthreads();
-}
-
-template <typename C, bool INV, int NT, int MAXB, bool SEQ_FAST>
-__device__ __forceinline__ void fft_pass_r2(C* buf, int logL, int lognseq, int sstr, int estr) {
-    // first pass only (Ns = 1): no twiddles
-    const int logQ = logL - 1;
-    const int Q = 1 << logQ;
-    const int total = 1 << (lognseq + logQ);
-    C v[MAXB][2];
-#pragma unroll
-    for (int i = 0; i < MAXB; ++i) {
-        int bf = threadIdx.x + i * NT;
-        if (bf < total) {
-            int q, j;
-            if (SEQ_FAST) { q = bf & ((1 << lognseq) - 1); j = bf >> lognseq; }
-            else          { q = bf >> logQ; j = bf & (Q - 1); }
-            const C* base = buf + q * sstr;
-            C a0 = base[j * estr], a1 = base[(j + Q) * estr];
-            v[i][0] = cadd(a0, a1);
-            v[i][1] = csub(a0, a1);
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < MAXB; ++i) {
-        int bf = threadIdx.x + i * NT;
-        if (bf < total) {
-            int q, j;
-            if (SEQ_FAST) { q = bf & ((1 << lognseq) - 1); j = bf >> lognseq; }
-            else          { q = bf >> logQ; j = bf & (Q - 1); }
-            C* base = buf + q * sstr;
-            base[(2 * j) * estr] = v[i][0];
-            base[(2 * j + 1) * estr] = v[i][1];
-        }
-    }
-    __syncthreads();
-}
-
-// Full unnormalised DFT (sign -1 forward, +1 inverse) of every sequence.
-// CAP = max nseq * L handled by the caller's block.
-template <typename C, bool INV, int NT, int CAP, bool SEQ_FAST>
-__device__ __forceinline__ void block_fft(C* buf, int logL, int lognseq, int sstr, int estr, const C* tw) {
-    int logNs = 0;
-    if (logL & 1) {
-        fft_pass_r2<C, INV, NT, (CAP / 2 + NT - 1) / NT, SEQ_FAST>(buf, logL, lognseq, sstr, estr);
-        logNs = 1;
-    }
-    for (; logNs < logL; logNs += 2)
-        fft_pass_r4<C, INV, NT, (CAP / 4 + NT - 1) / NT, SEQ_FAST>(buf, logL, logNs, lognseq, sstr, estr, tw);
-}
-
-// ---------------------------------------------------------------------------
 // Radix-16/8/4/2 Stockham FFT.  Each thread owns whole radix-R butterflies in
 // registers (R = 16 while >= 16 points remain, then 8/4/2).  Row sequences are
 // addressed through the padded index SP(i) = i + (i >> 4) so the stride-R
