@@ -975,7 +975,7 @@ extern "C" VDAMP_API int vdamp_debug_scan_times(long long* out, int images) {
     return guard([&] { CK(cudaMemcpyFromSymbol(out, g_scan, (size_t)images * 64 * 5 * sizeof(long long))); });
 }
 extern "C" VDAMP_API int vdamp_debug_csort_times(long long* out, int images) {
-    return guard([&] { CK(cudaMemcpyFromSymbol(out, g_csort, (size_t)images * 64 * 6 * sizeof(long long))); });
+    return guard([&] { CK(cudaMemcpyFromSymbol(out, g_csort, (size_t)images * 64 * 8 * sizeof(long long))); });
 }
 #endif
 

@@ -834,7 +834,7 @@ constexpr int CS_COARSE = 1024;   // coarse buckets (one per thread of the 1024-
 static_assert(CS_FINE / 2 + 2 * CS_COARSE <= CS_WORDS, "counting-sort tables exceed the counter region");
 
 #ifdef VDAMP_PHASE_TIMING
-__device__ long long g_csort[4096][64][6];
+__device__ long long g_csort[4096][64][8];
 #define CS_MARK(i) do { if (threadIdx.x == 0 && dbg) { long long c_ = clock64(); dbg[i] = c_ - cs0_; cs0_ = c_; } } while (0)
 #else
 #define CS_MARK(i) do { } while (0)
@@ -1445,6 +1445,9 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
         else if (ef == 8) build(std::integral_constant<int, 8>{});
         else build(std::integral_constant<int, 4>{});
         __syncthreads();
+#ifdef VDAMP_PHASE_TIMING
+        if (tid == 0 && bi < 4096) g_csort[bi][j][6] = clock64() - ph0_;   // keys built
+#endif
         if (tid == 0) S_.mphase ^= 1u;
         if (!a.tau_in && tid == 0) {
             double t = 0.0;

@@ -21,11 +21,11 @@ for j in range(S):
     m = a[:, j, :].mean(0)
     print(f"subband {j:2d} n={lens[j]:6d}  load+sort {m[0]:9.0f}  scan {m[1]:9.0f}  argmin {m[2]:7.0f} cycles")
 
-buf2 = (ctypes.c_longlong * (64 * 64 * 6))()
+buf2 = (ctypes.c_longlong * (64 * 64 * 8))()
 lib.vdamp_debug_csort_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
 _lib.check(lib.vdamp_debug_csort_times(buf2, 64))
-c6 = np.frombuffer(buf2, dtype=np.int64).reshape(64, 64, 6)[:nb, S - 3:S, :]
-print("TMA landed after %.0f cycles (16384-key subbands)" % c6[..., 5].mean())
+c6 = np.frombuffer(buf2, dtype=np.int64).reshape(64, 64, 8)[:nb, S - 3:S, :]
+print("TMA landed after %.0f cycles, keys built after %.0f (16384-key subbands)" % (c6[..., 5].mean(), c6[..., 6].mean()))
 c = c6[..., :5].mean((0, 1))
 print("counting sort (n=16384) cycles: minmax+coarse %.0f  table+fine hist %.0f  check+scan %.0f  scatter %.0f  bucket sort %.0f" % tuple(c))
 
