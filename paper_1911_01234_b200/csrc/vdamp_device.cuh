@@ -349,4 +349,31 @@ __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Both exclusive scans of scan_tile in one pass: a forward scan of `a` (sum
+// over lower threads) and a reverse scan of `b` (sum over higher threads),
+// interleaved so they share the barriers.  Same summation trees as two
+// block_excl_scan calls.  `sh` needs 2 * NT/32 doubles.
+template <int NT>
+__device__ __forceinline__ void block_excl_scan2(double a, double b, double* sh, double& ea, double& eb) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    constexpr int NW = NT / 32;
+    double ta, tb;
+    const double xa = warp_excl_scan<false>(a, ta);
+    const double xb = warp_excl_scan<true>(b, tb);
+    __syncthreads();
+    if (l == 0) { sh[w] = ta; sh[NW + w] = tb; }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double d;
+        const double wa = warp_excl_scan<false>(l < NW ? sh[l] : 0.0, d);
+        const double wb = warp_excl_scan<true>(l < NW ? sh[NW + l] : 0.0, d);
+        __syncwarp();
+        if (l < NW) { sh[l] = wa; sh[NW + l] = wb; }
+    }
+    __syncthreads();
+    ea = sh[w] + xa;
+    eb = sh[NW + w] + xb;
+    __syncthreads();
+}
+
 }  // namespace vdamp

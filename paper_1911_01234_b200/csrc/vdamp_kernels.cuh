@@ -1232,8 +1232,10 @@ __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, in
         }
     }
     SC_MARK(0);
-    const double pre = block_excl_scan<NT, false>(ssq, sh) + pre_tile;
-    const double suf = block_excl_scan<NT, true>(sinv, sh) + suf_tile;
+    double pre, suf;
+    block_excl_scan2<NT>(ssq, sinv, sh, pre, suf);
+    pre += pre_tile;
+    suf += suf_tile;
     if (tid == 0 && tilebase == 0) *totinv = suf + sinv;     // sum of all inverses
     SC_MARK(1);
     if (act) scan_keys<R, NT, EMAX, SMEM, EFIX>(keys, T, tilebase, n, tau, b0, E, pre, suf, next_tile_first, best,
