@@ -217,6 +217,15 @@ struct Seq {
     cudaStream_t& st_ = st;
     C* r() { return (C*)p->r; }
 
+    // 256-wide rows in 16-row strips: the register row-FFT kernels (F256)
+    // (VDAMP_F256=0 falls back to the generic shared-memory FFT kernels, for A/B runs)
+    static bool f256_on() {
+        static const bool on = [] { const char* e = getenv("VDAMP_F256"); return !(e && atoi(e) == 0); }();
+        return on;
+    }
+    bool f256(const Pass& ps) const { return f256_on() && p->W == 256 && ps.Wa == 256 && ps.k == 4; }
+    bool c256() const { return f256_on() && p->H == 256 && p->cw == 16; }
+
     // Haar synthesis of coefficients `coef` with params `par`; FFT -> T1 when
     // rowfft, else the image goes to `img`.
     void synth(const C* coef, const double* par, bool rowfft, C* img, int cls) {
@@ -235,7 +244,11 @@ struct Seq {
             dim3 grid(ps.nstrips, p->B);
             const size_t sm = (size_t)SPN(ps.Wa << ps.k) * sizeof(C);
             Launch L(p, cls, st);
-            if (last && rowfft) {
+            if (last && rowfft && f256(ps)) {
+                auto k = synth_pass<R, SYN_ROWFFT, true>;
+                set_smem(k, sm);
+                launch(k, grid, PNT, sm, st, p->geo, a);
+            } else if (last && rowfft) {
                 auto k = synth_pass<R, SYN_ROWFFT>;
                 const size_t smf = sm + (size_t)p->W * sizeof(C);
                 set_smem(k, smf);
@@ -266,7 +279,15 @@ struct Seq {
             dim3 grid(ps.nstrips, p->B);
             size_t sm = (size_t)SPN(ps.Wa << ps.k) * sizeof(C);
             Launch L(p, cls, st);
-            if (first && rowifft) {
+            if (first && rowifft && f256(ps)) {
+                if (vdamp_mode) {
+                    auto k = analysis_pass<R, ANA_IN_ROWIFFT, ANA_OUT_VDAMP, true>; set_smem(k, sm);
+                    launch(k, grid, PNT, sm, st, p->geo, a);
+                } else {
+                    auto k = analysis_pass<R, ANA_IN_ROWIFFT, ANA_OUT_COEF, true>; set_smem(k, sm);
+                    launch(k, grid, PNT, sm, st, p->geo, a);
+                }
+            } else if (first && rowifft) {
                 sm += (size_t)p->W * sizeof(C);
                 if (vdamp_mode) {
                     auto k = analysis_pass<R, ANA_IN_ROWIFFT, ANA_OUT_VDAMP>; set_smem(k, sm);
@@ -305,8 +326,20 @@ struct Seq {
         a.tw = (const C*)p->twH; a.cw = p->cw; a.logcw = p->logcw; a.ntiles = p->ntiles;
         a.x0r = (const C*)p->x0r; a.nmsepart = p->nmpart;
         dim3 grid(p->ntiles, p->B);
-        const size_t sm = col_smem();
         Launch L(p, cls, st);
+        if (c256() && (mode == COL_VDAMP || mode == COL_FINAL || mode == COL_NMSE)) {
+            const int np = 2 * p->s, npp = (np + 3) & ~3;
+            const size_t tau = (size_t)np * PNT * sizeof(double) + (size_t)np * 16 * sizeof(double) +
+                               (size_t)256 * npp * sizeof(R);
+            const size_t sm = std::max((size_t)4096 * sizeof(C), tau) + (COL256_WSM ? (size_t)4096 * sizeof(R) : 0);
+            switch (mode) {
+                case COL_VDAMP: { auto k = col_pass256<R, COL_VDAMP>; set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
+                case COL_NMSE:  { auto k = col_pass256<R, COL_NMSE>;  set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
+                default:        { auto k = col_pass256<R, COL_FINAL>; set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
+            }
+            return;
+        }
+        const size_t sm = col_smem();
         switch (mode) {
             case COL_FWD:   { auto k = col_pass<R, COL_FWD>;   set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
             case COL_INV:   { auto k = col_pass<R, COL_INV>;   set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }

@@ -233,6 +233,92 @@ __device__ __forceinline__ void fft_pass(C* buf, int logL, int logNs, int lognse
     __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// 256-point FFT as 16 x 16 with the data in registers.  A thread with digit d
+// (0..15) holds 16 elements of one sequence; stage A is a radix-16 DFT over the
+// held digit followed by the twiddle w^(d m), m = output index; a transpose
+// (through shared memory, done by the caller) hands each thread the 16 stage-A
+// outputs of its own m; stage B is a plain radix-16 DFT.
+//   forward: v[n1] = x[16 n1 + d]  -> (A, transpose, B) -> v[k2] = X[d + 16 k2]
+//   inverse: v[k2] = X[d + 16 k2]  -> (A, transpose, B) -> v[n2] = x[d + 16 n2]
+// (x[16 n1 + n2] -> X[k1 + 16 k2] uses w256^(n2 k1) between the stages; the
+// inverse reads the forward's output order directly, so a forward FFT, a
+// pointwise step and an inverse FFT need no transpose between them.)
+// ---------------------------------------------------------------------------
+template <typename C, int R>
+__device__ __forceinline__ void pow_twiddles(C (&v)[R], C t1, C t2, C t4, C t8) {
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+        C w;
+        switch (r) {
+            case 1: w = t1; break;
+            case 2: w = t2; break;
+            case 3: w = cmul(t2, t1); break;
+            case 4: w = t4; break;
+            case 5: w = cmul(t4, t1); break;
+            case 6: w = cmul(t4, t2); break;
+            case 7: w = cmul(cmul(t4, t2), t1); break;
+            case 8: w = t8; break;
+            case 9: w = cmul(t8, t1); break;
+            case 10: w = cmul(t8, t2); break;
+            case 11: w = cmul(cmul(t8, t2), t1); break;
+            case 12: w = cmul(t8, t4); break;
+            case 13: w = cmul(cmul(t8, t4), t1); break;
+            case 14: w = cmul(cmul(t8, t4), t2); break;
+            default: w = cmul(cmul(cmul(t8, t4), t2), t1); break;
+        }
+        v[r] = cmul(v[r], w);
+    }
+}
+
+// stage A of the 16 x 16 FFT: radix-16 DFT of v, then v[m] *= w256^(+-d m);
+// tw[m] = exp(-2 pi i m / 256) (global, L1-resident)
+template <typename C, bool INV>
+__device__ __forceinline__ void fft256_stage_a(C (&v)[16], int d, const C* __restrict__ tw) {
+    C t1 = __ldg(tw + d), t2 = __ldg(tw + 2 * d), t4 = __ldg(tw + 4 * d), t8 = __ldg(tw + 8 * d);
+    dft_r<C, INV, 16>(v);
+    if (INV) { t1 = cconj(t1); t2 = cconj(t2); t4 = cconj(t4); t8 = cconj(t8); }
+    pow_twiddles<C, 16>(v, t1, t2, t4, t8);
+}
+
+// Row FFTs of a 16 x 256 strip held in the SP-padded shared buffer (row r at
+// SP(256 r) = 272 r; element e of a row at 17 (e >> 4) + (e & 15)).  Thread
+// (r = tid >> 4, d = tid & 15).  Forward: buffer rows -> v[k2] = X_r[d + 16 k2].
+template <typename C>
+__device__ __forceinline__ void strip_fft256_fwd(C* buf, C (&v)[16], const C* __restrict__ tw) {
+    const int r = threadIdx.x >> 4, d = threadIdx.x & 15;
+    C* row = buf + 272 * r;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = row[17 * j + d];
+    fft256_stage_a<C, false>(v, d, tw);
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; ++m) row[17 * m + d] = v[m];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = row[17 * d + j];
+    dft_r<C, false, 16>(v);
+}
+
+// Inverse: v[k2] = X_r[d + 16 k2] (registers) -> natural-order rows in the
+// SP-padded buffer (unnormalised).
+template <typename C>
+__device__ __forceinline__ void strip_ifft256_to_smem(C* buf, C (&v)[16], const C* __restrict__ tw) {
+    const int r = threadIdx.x >> 4, d = threadIdx.x & 15;
+    C* row = buf + 272 * r;
+    fft256_stage_a<C, true>(v, d, tw);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) row[17 * m + d] = v[m];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = row[17 * d + j];
+    dft_r<C, true, 16>(v);
+    __syncthreads();
+#pragma unroll
+    for (int n = 0; n < 16; ++n) row[17 * n + d] = v[n];
+    __syncthreads();
+}
+
 // Full unnormalised DFT of every sequence (radix-16 passes, one final 2/4/8 pass).
 template <typename C, bool INV, int NT, int CAP, bool SEQ_FAST, bool PAD>
 __device__ __forceinline__ void block_fft16(C* buf, int logL, int lognseq, int sstr, int estr, const C* tw) {
@@ -344,6 +430,10 @@ __device__ __forceinline__ double block_excl_scan(double v, double* sh) {
 // programmatic dependent launch: wait for the preceding grid (no-op when the
 // kernel was launched without the PDL attribute), then let the next grid start
 // its CTAs as SMs free up
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// L2 prefetch hint (no register or ordering effect)
+__device__ __forceinline__ void prefetch_l2(const void* q) { asm volatile("prefetch.global.L2 [%0];" ::"l"(q)); }
 __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -139,7 +139,9 @@ __device__ __forceinline__ void gather_coarse(const Geo& g, const SynArgs<R>& p,
     }
 }
 
-template <typename R, int MODE>
+// F256: W = 256 and 16-row strips (k = 4): the row FFT runs in registers
+// (strip_fft256_fwd) and stores T1 straight from them
+template <typename R, int MODE, bool F256 = false>
 __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth_pass(Geo g, SynArgs<R> p) {
     pdl_enter();
     typedef typename CT<R>::T C;
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth_pass(Geo g,
     const double* par = p.par ? p.par + (long long)bi * g.S * 3 : nullptr;
     C* tws = buf + SP(E - 1) + 1;
     __shared__ R spar[MAXS * 3];
-    if (MODE == SYN_ROWFFT)
+    if (MODE == SYN_ROWFFT && !F256)
         for (int e = tid; e < g.W; e += PNT) tws[e] = p.tw[e];
     for (int i = tid; i < g.S * 3; i += PNT) spar[i] = par ? (R)par[i] : ((i % 3) == 2 ? R(1) : R(0));
 
@@ -254,6 +256,14 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth_pass(Geo g,
     }
 
     C* dst = p.dst + (long long)bi * p.dst_bs + (long long)st * E;
+    if constexpr (MODE == SYN_ROWFFT && F256) {
+        C v[16];
+        strip_fft256_fwd<C>(buf, v, p.tw);
+        C* drow = dst + ((tid >> 4) << 8) + (tid & 15);
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) drow[16 * k2] = v[k2];
+        return;
+    }
     if (MODE == SYN_ROWFFT) block_fft16<C, false, PNT, PCAP, false, true>(buf, g.logW, k, Wa, 1, tws);
     for (int e = tid; e < E; e += PNT) dst[e] = buf[SP(e)];
 }
@@ -273,15 +283,17 @@ struct AnaArgs {
     long long src_bs, adst_bs;
 };
 
-template <typename R, int IN, int OUT>
+// F256: W = 256 and 16-row strips: the row IFFT reads T2 straight into
+// registers (strip_ifft256_to_smem)
+template <typename R, int IN, int OUT, bool F256 = false>
 __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis_pass(Geo g, AnaArgs<R> p) {
-    pdl_enter();
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* buf = reinterpret_cast<C*>(smem_raw);
     const int st = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
     const int k = p.k, Wa = p.Wa;
     const int E = Wa << k;
+    pdl_enter();
     const C* src = p.src + (long long)bi * p.src_bs + (long long)st * E;
     C* coef = p.coef + (long long)bi * g.N;
     __shared__ R spar[MAXS * 3];
@@ -289,7 +301,13 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis_pass(Geo
         const double* par = p.par + (long long)bi * g.S * 3;
         for (int i = tid; i < g.S * 3; i += PNT) spar[i] = (R)par[i];
     }
-    if (IN == ANA_IN_ROWIFFT) {
+    if constexpr (IN == ANA_IN_ROWIFFT && F256) {
+        C v[16];
+        const C* srow = src + ((tid >> 4) << 8) + (tid & 15);
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) v[k2] = srow[16 * k2];
+        strip_ifft256_to_smem<C>(buf, v, p.tw);
+    } else if (IN == ANA_IN_ROWIFFT) {
         C* tws = buf + SP(E - 1) + 1;
         for (int e = tid; e < g.W; e += PNT) tws[e] = p.tw[e];
         for (int e = tid; e < E; e += PNT) buf[SP(e)] = src[e];
@@ -615,6 +633,180 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass(Geo g, C
         const double* Bc = p.pcol + (long long)pc_ * W + c0;
         double sacc = 0.0;
         for (int c = 0; c < cw; ++c) sacc += Bc[c] * psum[pr_ * cw + c];
+        p.taupart[((long long)bi * p.ntiles + tile) * g.S + j] = sacc;
+    }
+}
+
+template <typename R> __device__ __forceinline__ void ld4(const R* q, R& a, R& b, R& c, R& d);
+template <> __device__ __forceinline__ void ld4<float>(const float* q, float& a, float& b, float& c, float& d) {
+    const float4 t = *reinterpret_cast<const float4*>(q); a = t.x; b = t.y; c = t.z; d = t.w;
+}
+template <> __device__ __forceinline__ void ld4<double>(const double* q, double& a, double& b, double& c, double& d) {
+    const double2 t0 = reinterpret_cast<const double2*>(q)[0], t1 = reinterpret_cast<const double2*>(q)[1];
+    a = t0.x; b = t0.y; c = t1.x; d = t1.y;
+}
+
+// K2 for H = 256 (16-column tiles): the same computation as col_pass with both
+// column FFTs in registers (fft256_stage_a + one shared-memory transpose each).
+// Thread (c = tid & 15, d = tid >> 4) loads rows 16 n1 + d of column c, holds
+// X[d + 16 k2] after the forward FFT, applies the residual / finalize step to
+// those 16 frequencies and runs the inverse FFT from them directly; outputs are
+// rows d + 16 n2.  Modes: COL_VDAMP, COL_FINAL, COL_NMSE.
+// COL256_WSM=1 parks the tau weights in shared memory across the inverse FFT
+// (measured 1% slower than keeping them in registers)
+#ifndef COL256_WSM
+#define COL256_WSM 0
+#endif
+#ifndef COL256_MINB
+#define COL256_MINB 3
+#endif
+template <typename R, int MODE>
+__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? COL256_MINB : 2) col_pass256(Geo g, ColArgs<R> p) {
+    typedef typename CT<R>::T C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* buf = reinterpret_cast<C*>(smem_raw);              // [16][16][16] transpose tile
+    const int W = g.W;
+    const int tile = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
+    const int c = tid & 15, d = tid >> 4;
+    const int c0 = tile << 4;
+    const long long ib = (long long)bi * g.N;
+    const long long colbase = ib + (long long)d * W + c0 + c;   // row d of this thread's column
+    if (MODE != COL_NMSE) {
+        // the measurements do not depend on the previous kernel: pull this
+        // tile's rows of y and 1/p towards L2 before waiting on it
+        const long long ri = ib + (long long)tid * W + c0;
+        prefetch_l2(p.yg + ri);
+        if (sizeof(R) == 8) prefetch_l2(p.yg + ri + 8);
+        prefetch_l2(p.pinv + ri);
+    }
+    pdl_enter();
+    C v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = p.src[colbase + (long long)(16 * j) * W];
+    fft256_stage_a<C, false>(v, d, p.tw);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) buf[(m * 16 + d) * 16 + c] = v[m];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = buf[(d * 16 + j) * 16 + c];
+    dft_r<C, false, 16>(v);                                // v[k2] = FFT2u(row-FFT'd x)[d + 16 k2]
+    const R sc = R(1) / R(16);                             // 1 / sqrt(256)
+    if (MODE == COL_NMSE) {
+        double e2 = 0.0;
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) {
+            const long long gi = colbase + (long long)(16 * k2) * W;
+            if (p.pinv[gi] == R(0)) {
+                const C df = csub(cscale(v[k2], sc), p.x0r[gi]);
+                e2 += (double)df.x * (double)df.x + (double)df.y * (double)df.y;
+            }
+        }
+        __syncthreads();                                   // transpose reads done: buf is scratch
+        e2 = block_sum<PNT>(e2, reinterpret_cast<double*>(buf));
+        if (tid == 0) p.nmsepart[(long long)bi * p.ntiles + tile] = e2;
+        return;
+    }
+    const R cs = (R)g.sign_c;
+    // tau weights go to shared memory right away (frees 16 registers across the
+    // inverse FFT): wsm[k2][tid], past the transpose / tau-partial region
+    const int np = 2 * g.s, npp = (np + 3) & ~3;
+    const int tau_bytes = np * PNT * 8 + np * 16 * 8 + 256 * npp * (int)sizeof(R);
+#if COL256_WSM
+    R* wsm = reinterpret_cast<R*>(smem_raw + (tau_bytes > 4096 * (int)sizeof(C) ? tau_bytes : 4096 * (int)sizeof(C)));
+#else
+    R wreg[16];
+#endif
+    {
+        const double nv = (MODE == COL_VDAMP) ? p.noise_var[bi] : 0.0;
+        R pvs[16];
+        C ys[16];
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) {                  // issue all measurement loads first
+            const long long gi = colbase + (long long)(16 * k2) * W;
+            pvs[k2] = p.pinv[gi];
+            ys[k2] = p.yg[gi];
+        }
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) {
+            const C X = cscale(v[k2], sc * cs);            // c * FFT2u, so (-1)^(k1+k2) X_centred
+            const R pv = pvs[k2];
+            R wk = R(0);
+            if (MODE == COL_VDAMP) {
+                if (pv != R(0)) {
+                    const C zc = csub(ys[k2], X);                  // (-1)^(k1+k2) z  (src/vdamp.py:112)
+                    v[k2] = cscale(zc, pv);                        // P^-1 z           (src/vdamp.py:113)
+                    const double pd = (double)pv;
+                    const double z2 = (double)zc.x * (double)zc.x + (double)zc.y * (double)zc.y;
+                    wk = (R)(pd * ((pd - 1.0) * z2 + nv));         // tau weight (src/vdamp.py:74-75)
+                } else {
+                    v[k2] = mk<C>(R(0), R(0));
+                }
+            } else {  // COL_FINAL: measured k-space where sampled (src/vdamp.py:147-150)
+                v[k2] = (pv != R(0)) ? ys[k2] : X;
+            }
+#if COL256_WSM
+            if (MODE == COL_VDAMP) wsm[k2 * PNT + tid] = wk;
+#else
+            wreg[k2] = wk;
+#endif
+        }
+    }
+    fft256_stage_a<C, true>(v, d, p.tw);
+    __syncthreads();                                       // forward transpose reads done
+#pragma unroll
+    for (int m = 0; m < 16; ++m) buf[(m * 16 + d) * 16 + c] = v[m];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = buf[(d * 16 + j) * 16 + c];
+    dft_r<C, true, 16>(v);                                 // v[n2] = x[d + 16 n2]
+#pragma unroll
+    for (int n2 = 0; n2 < 16; ++n2) p.dst[colbase + (long long)(16 * n2) * W] = cscale(v[n2], sc);
+    if (MODE != COL_VDAMP) return;
+
+    // tau partials (as col_pass): per row profile q, this thread's 16 rows
+    // d + 16 k2 in registers against profiles staged row-major [row][npp]
+    // (float4 loads), then a fixed-order combination over the 16 threads of
+    // each column and the column profiles
+    __syncthreads();                                       // inverse transpose reads done
+    double* part = reinterpret_cast<double*>(buf);         // [np][PNT] thread partials
+    double* psum = part + np * PNT;                        // [np][16] column partials
+    R* prs = reinterpret_cast<R*>(psum + np * 16);         // [256][npp] row profiles
+    for (int i = tid; i < 256 * npp; i += PNT) {
+        const int k = i / npp, q = i - k * npp;
+        prs[i] = (q < np) ? (R)p.prow[q * 256 + k] : R(0);
+    }
+    __syncthreads();
+    for (int q0 = 0; q0 < np; q0 += 4) {
+        R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) {
+            R b0, b1, b2, b3;
+            ld4<R>(prs + (d + 16 * k2) * npp + q0, b0, b1, b2, b3);
+#if COL256_WSM
+            const R wk = wsm[k2 * PNT + tid];
+#else
+            const R wk = wreg[k2];
+#endif
+            a0 += b0 * wk; a1 += b1 * wk; a2 += b2 * wk; a3 += b3 * wk;
+        }
+        part[q0 * PNT + tid] = (double)a0;
+        part[(q0 + 1) * PNT + tid] = (double)a1;
+        if (q0 + 2 < np) { part[(q0 + 2) * PNT + tid] = (double)a2; part[(q0 + 3) * PNT + tid] = (double)a3; }
+    }
+    __syncthreads();
+    for (int it = tid; it < np * 16; it += PNT) {
+        const int q = it >> 4, cc = it & 15;
+        double sacc = 0.0;
+        for (int t = cc; t < PNT; t += 16) sacc += part[q * PNT + t];
+        psum[q * 16 + cc] = sacc;
+    }
+    __syncthreads();
+    for (int j = tid; j < g.S; j += PNT) {
+        int pr_, pc_;
+        band_profiles(g.s, j, pr_, pc_);
+        const double* Bc = p.pcol + (long long)pc_ * W + c0;
+        double sacc = 0.0;
+        for (int cc = 0; cc < 16; ++cc) sacc += Bc[cc] * psum[pr_ * 16 + cc];
         p.taupart[((long long)bi * p.ntiles + tile) * g.S + j] = sacc;
     }
 }
