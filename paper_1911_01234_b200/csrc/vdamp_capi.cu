@@ -245,7 +245,7 @@ struct Seq {
             const size_t sm = (size_t)SPN(ps.Wa << ps.k) * sizeof(C);
             Launch L(p, cls, st);
             if (last && rowfft && f256(ps)) {
-                auto k = synth_pass<R, SYN_ROWFFT, true>;
+                auto k = synth256<R>;
                 set_smem(k, sm);
                 launch(k, grid, PNT, sm, st, p->geo, a);
             } else if (last && rowfft) {
@@ -281,10 +281,10 @@ struct Seq {
             Launch L(p, cls, st);
             if (first && rowifft && f256(ps)) {
                 if (vdamp_mode) {
-                    auto k = analysis_pass<R, ANA_IN_ROWIFFT, ANA_OUT_VDAMP, true>; set_smem(k, sm);
+                    auto k = analysis256<R, ANA_OUT_VDAMP>; set_smem(k, sm);
                     launch(k, grid, PNT, sm, st, p->geo, a);
                 } else {
-                    auto k = analysis_pass<R, ANA_IN_ROWIFFT, ANA_OUT_COEF, true>; set_smem(k, sm);
+                    auto k = analysis256<R, ANA_OUT_COEF>; set_smem(k, sm);
                     launch(k, grid, PNT, sm, st, p->geo, a);
                 }
             } else if (first && rowifft) {

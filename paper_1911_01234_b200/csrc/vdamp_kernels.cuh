@@ -458,6 +458,252 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis_pass(Geo
     }
 }
 
+// ---------------------------------------------------- K1 / K3, W = 256 ----
+// 16-row strips of a 256-wide image with the four finest Haar levels of the
+// strip done per thread: thread (br = tid >> 6, bc = tid & 63) owns the 4x4
+// pixel block at strip rows 4 br.., columns 4 bc.., i.e. the 2x2 level-1
+// coefficients (2 br + i, 2 bc + j) and the level-2 coefficient (br, bc) of each
+// orientation; level 3 and 4 (and the approximation) are per 8x8 / 16x16 block.
+// Strip st maps to subband rows st * (16 >> l) .. of level l (src/wavelet.py:52-61).
+template <typename C>
+__device__ __forceinline__ void ld2c(const C* q, C& a, C& b) {
+    if constexpr (sizeof(C) == 8) {
+        const float4 t = *reinterpret_cast<const float4*>(q);
+        a = mk<C>(t.x, t.y); b = mk<C>(t.z, t.w);
+    } else {
+        a = q[0]; b = q[1];
+    }
+}
+template <typename C>
+__device__ __forceinline__ void st2c(C* q, C a, C b) {
+    if constexpr (sizeof(C) == 8) *reinterpret_cast<float4*>(q) = make_float4(a.x, a.y, b.x, b.y);
+    else { q[0] = a; q[1] = b; }
+}
+template <typename C> __device__ __forceinline__ C cneg_if(C a, bool neg) { return neg ? mk<C>(-a.x, -a.y) : a; }
+
+// one synthesis output of a 2x2 block (src/wavelet.py:118-129): quadrant (qi, qj)
+template <typename R, typename C>
+__device__ __forceinline__ C haar_syn_q(C ll, C lh, C hl, C hh, bool qi, bool qj) {
+    const C lo = Haar<R>::sum(ll, cneg_if(lh, qj)), hi = Haar<R>::sum(hl, cneg_if(hh, qj));
+    return Haar<R>::sum(lo, cneg_if(hi, qi));
+}
+
+template <typename R, bool ONS>
+__device__ __forceinline__ typename CT<R>::T ons_j(typename CT<R>::T x, const R* spar, int j) {
+    return ONS ? onsager<R, typename CT<R>::T>(x, spar[3 * j], spar[3 * j + 1], spar[3 * j + 2]) : x;
+}
+
+// K1 for W = 256, k = 4: r~ = Onsager(r) gathered per 4x4 block, Haar synthesis
+// of levels 4..1 in registers, (-1)^(n1+n2) / 16 folded in, register row FFT -> T1
+template <typename R>
+__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth256(Geo g, SynArgs<R> p) {
+    pdl_enter();
+    typedef typename CT<R>::T C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* buf = reinterpret_cast<C*>(smem_raw);
+    const int st = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
+    const int br = tid >> 6, bc = tid & 63;
+    const C* coef = p.coef + (long long)bi * g.N;
+    __shared__ R spar[MAXS * 3];
+    const double* par = p.par ? p.par + (long long)bi * g.S * 3 : nullptr;
+    for (int i = tid; i < g.S * 3; i += PNT) spar[i] = par ? (R)par[i] : ((i % 3) == 2 ? R(1) : R(0));
+    const int j1 = band_of(g.s, 1, 0), j2 = band_of(g.s, 2, 0), j3 = band_of(g.s, 3, 0), j4 = band_of(g.s, 4, 0);
+    // loads first: level 1 (2 x 2 per orientation, pairs along the row), 2, 3, 4, approximation
+    C d1[3][2][2], d2[3], d3[3], d4[3], a4;
+    {
+        const long long o1 = (long long)st * 1024 + (2 * br) * 128 + 2 * bc;
+#pragma unroll
+        for (int o = 0; o < 3; ++o)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) ld2c<C>(coef + g.off[j1 + o] + o1 + i * 128, d1[o][i][0], d1[o][i][1]);
+        const long long o2 = (long long)st * 256 + br * 64 + bc;
+        const long long o3 = (long long)st * 64 + (br >> 1) * 32 + (bc >> 1);
+        const long long o4 = (long long)st * 16 + (bc >> 2);
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+            d2[o] = coef[g.off[j2 + o] + o2];
+            d3[o] = coef[g.off[j3 + o] + o3];
+            d4[o] = coef[g.off[j4 + o] + o4];
+        }
+        a4 = p.asrc ? p.asrc[(long long)bi * p.asrc_bs + o4] : coef[g.off[0] + o4];
+    }
+    __syncthreads();                                        // spar
+    C px[4][4];
+    auto body = [&](auto onsc) {
+        constexpr bool ONS = decltype(onsc)::value;
+        if (!p.asrc) a4 = ons_j<R, ONS>(a4, spar, 0);
+        // levels 4 and 3: only the quadrant on this thread's path
+        const C a3 = haar_syn_q<R, C>(a4, ons_j<R, ONS>(d4[0], spar, j4), ons_j<R, ONS>(d4[1], spar, j4 + 1),
+                                      ons_j<R, ONS>(d4[2], spar, j4 + 2), (br >> 1) & 1, (bc >> 1) & 1);
+        const C a2 = haar_syn_q<R, C>(a3, ons_j<R, ONS>(d3[0], spar, j3), ons_j<R, ONS>(d3[1], spar, j3 + 1),
+                                      ons_j<R, ONS>(d3[2], spar, j3 + 2), br & 1, bc & 1);
+        const C h2 = ons_j<R, ONS>(d2[0], spar, j2), v2 = ons_j<R, ONS>(d2[1], spar, j2 + 1),
+                e2 = ons_j<R, ONS>(d2[2], spar, j2 + 2);
+        const R sc = R(1) / R(16);                          // unitary 1 / sqrt(W) of the row FFT
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const C a1 = haar_syn_q<R, C>(a2, h2, v2, e2, i, j);
+                const C lh = ons_j<R, ONS>(d1[0][i][j], spar, j1), hl = ons_j<R, ONS>(d1[1][i][j], spar, j1 + 1),
+                        hh = ons_j<R, ONS>(d1[2][i][j], spar, j1 + 2);
+                const C lo0 = Haar<R>::sum(a1, lh), lo1 = Haar<R>::dif(a1, lh);
+                const C hi0 = Haar<R>::sum(hl, hh), hi1 = Haar<R>::dif(hl, hh);
+                // (-1)^(n1+n2) on even-origin 2x2 blocks: +, -, -, +
+                px[2 * i][2 * j] = cscale(Haar<R>::sum(lo0, hi0), sc);
+                px[2 * i][2 * j + 1] = cscale(Haar<R>::sum(lo1, hi1), -sc);
+                px[2 * i + 1][2 * j] = cscale(Haar<R>::dif(lo0, hi0), -sc);
+                px[2 * i + 1][2 * j + 1] = cscale(Haar<R>::dif(lo1, hi1), sc);
+            }
+    };
+    if (par) body(std::true_type{});
+    else body(std::false_type{});
+    // pixels -> SP-padded strip rows (row r at 272 r, column e at 17 (e >> 4) + (e & 15))
+    {
+        C* b0 = buf + 272 * (4 * br) + 17 * (bc >> 2) + 4 * (bc & 3);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b0[272 * i + j] = px[i][j];
+    }
+    __syncthreads();
+    C v[16];
+    strip_fft256_fwd<C>(buf, v, p.tw);
+    C* drow = p.dst + (long long)bi * p.dst_bs + (long long)st * 4096 + ((tid >> 4) << 8) + (tid & 15);
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) drow[16 * k2] = v[k2];
+}
+
+// K3 for W = 256, k = 4: register row IFFT of T2 into the strip, then per 4x4
+// block the sign c (-1)^(n1+n2) / 16 and Haar analysis levels 1..2 in registers,
+// levels 3..4 through a small shared exchange; VDAMP: r = Onsager(r; par) + Psi u
+template <typename R, int OUT>
+__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis256(Geo g, AnaArgs<R> p) {
+    pdl_enter();
+    typedef typename CT<R>::T C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* buf = reinterpret_cast<C*>(smem_raw);
+    const int st = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
+    const int br = tid >> 6, bc = tid & 63;
+    C* coef = p.coef + (long long)bi * g.N;
+    __shared__ R spar[MAXS * 3];
+    __shared__ C x2[4][64];                                 // level-2 approximations
+    __shared__ C x3[2][32];                                 // level-3 approximations
+    if (OUT == ANA_OUT_VDAMP) {
+        const double* par = p.par + (long long)bi * g.S * 3;
+        for (int i = tid; i < g.S * 3; i += PNT) spar[i] = (R)par[i];
+    }
+    const int j1 = band_of(g.s, 1, 0), j2 = band_of(g.s, 2, 0), j3 = band_of(g.s, 3, 0), j4 = band_of(g.s, 4, 0);
+    const long long o1 = (long long)st * 1024 + (2 * br) * 128 + 2 * bc;
+    const long long o2 = (long long)st * 256 + br * 64 + bc;
+    {
+        C v[16];
+        const C* srow = p.src + (long long)bi * p.src_bs + (long long)st * 4096 + ((tid >> 4) << 8) + (tid & 15);
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) v[k2] = srow[16 * k2];
+        strip_ifft256_to_smem<C>(buf, v, p.tw);
+    }
+    const R sc = (R)g.sign_c / R(16);
+    C h1[2][2], v1[2][2], e1[2][2], l1[2][2];
+    {
+        const C* b0 = buf + 272 * (4 * br) + 17 * (bc >> 2) + 4 * (bc & 3);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const C x00 = cscale(b0[272 * (2 * i) + 2 * j], sc);
+                const C x01 = cscale(b0[272 * (2 * i) + 2 * j + 1], -sc);
+                const C x10 = cscale(b0[272 * (2 * i + 1) + 2 * j], -sc);
+                const C x11 = cscale(b0[272 * (2 * i + 1) + 2 * j + 1], sc);
+                const C lo0 = Haar<R>::sum(x00, x10), hi0 = Haar<R>::dif(x00, x10);
+                const C lo1 = Haar<R>::sum(x01, x11), hi1 = Haar<R>::dif(x01, x11);
+                l1[i][j] = Haar<R>::sum(lo0, lo1);
+                h1[i][j] = Haar<R>::dif(lo0, lo1);
+                v1[i][j] = Haar<R>::sum(hi0, hi1);
+                e1[i][j] = Haar<R>::dif(hi0, hi1);
+            }
+    }
+    // level 2 from the 2x2 level-1 approximations
+    C l2, h2, v2, e2;
+    {
+        const C lo0 = Haar<R>::sum(l1[0][0], l1[1][0]), hi0 = Haar<R>::dif(l1[0][0], l1[1][0]);
+        const C lo1 = Haar<R>::sum(l1[0][1], l1[1][1]), hi1 = Haar<R>::dif(l1[0][1], l1[1][1]);
+        l2 = Haar<R>::sum(lo0, lo1); h2 = Haar<R>::dif(lo0, lo1); v2 = Haar<R>::sum(hi0, hi1); e2 = Haar<R>::dif(hi0, hi1);
+    }
+    x2[br][bc] = l2;
+    // details of levels 1 and 2 (VDAMP: + Onsager of the previous coefficients)
+    {
+        const C n1[3][2][2] = {{{h1[0][0], h1[0][1]}, {h1[1][0], h1[1][1]}},
+                               {{v1[0][0], v1[0][1]}, {v1[1][0], v1[1][1]}},
+                               {{e1[0][0], e1[0][1]}, {e1[1][0], e1[1][1]}}};
+        const C n2[3] = {h2, v2, e2};
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+            C* q1 = coef + g.off[j1 + o] + o1;
+            C* q2 = coef + g.off[j2 + o] + o2;
+            C w1[2][2], w2 = n2[o];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) { w1[i][0] = n1[o][i][0]; w1[i][1] = n1[o][i][1]; }
+            if (OUT == ANA_OUT_VDAMP) {
+                C old1[2][2];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) ld2c<C>(q1 + i * 128, old1[i][0], old1[i][1]);
+                const C old2 = *q2;
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) w1[i][j] = cadd(ons_j<R, true>(old1[i][j], spar, j1 + o), w1[i][j]);
+                w2 = cadd(ons_j<R, true>(old2, spar, j2 + o), w2);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) st2c<C>(q1 + i * 128, w1[i][0], w1[i][1]);
+            *q2 = w2;
+        }
+    }
+    __syncthreads();
+    // level 3: 64 threads, one per 8x8 block (2 rows x 32 columns of level-3 coefficients)
+    if (tid < 64) {
+        const int r3 = tid >> 5, c3 = tid & 31;
+        const C x00 = x2[2 * r3][2 * c3], x01 = x2[2 * r3][2 * c3 + 1];
+        const C x10 = x2[2 * r3 + 1][2 * c3], x11 = x2[2 * r3 + 1][2 * c3 + 1];
+        const C lo0 = Haar<R>::sum(x00, x10), hi0 = Haar<R>::dif(x00, x10);
+        const C lo1 = Haar<R>::sum(x01, x11), hi1 = Haar<R>::dif(x01, x11);
+        x3[r3][c3] = Haar<R>::sum(lo0, lo1);
+        C n3[3] = {Haar<R>::dif(lo0, lo1), Haar<R>::sum(hi0, hi1), Haar<R>::dif(hi0, hi1)};
+        const long long o3 = (long long)st * 64 + r3 * 32 + c3;
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+            C* q = coef + g.off[j3 + o] + o3;
+            if (OUT == ANA_OUT_VDAMP) n3[o] = cadd(ons_j<R, true>(*q, spar, j3 + o), n3[o]);
+            *q = n3[o];
+        }
+    }
+    __syncthreads();
+    // level 4: 16 threads, one per 16x16 block; the approximation goes to subband 0
+    // (s == 4) or to the next pass's scratch image (s > 4)
+    if (tid < 16) {
+        const C x00 = x3[0][2 * tid], x01 = x3[0][2 * tid + 1], x10 = x3[1][2 * tid], x11 = x3[1][2 * tid + 1];
+        const C lo0 = Haar<R>::sum(x00, x10), hi0 = Haar<R>::dif(x00, x10);
+        const C lo1 = Haar<R>::sum(x01, x11), hi1 = Haar<R>::dif(x01, x11);
+        C n4[3] = {Haar<R>::dif(lo0, lo1), Haar<R>::sum(hi0, hi1), Haar<R>::dif(hi0, hi1)};
+        C a = Haar<R>::sum(lo0, lo1);
+        const long long o4 = (long long)st * 16 + tid;
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+            C* q = coef + g.off[j4 + o] + o4;
+            if (OUT == ANA_OUT_VDAMP) n4[o] = cadd(ons_j<R, true>(*q, spar, j4 + o), n4[o]);
+            *q = n4[o];
+        }
+        if (p.adst) {
+            p.adst[(long long)bi * p.adst_bs + o4] = a;
+        } else {
+            C* q = coef + g.off[0] + o4;
+            if (OUT == ANA_OUT_VDAMP) a = cadd(ons_j<R, true>(*q, spar, 0), a);
+            *q = a;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ K2 ----
 // COL_RAW: forward column FFT without the centring sign (X0 setup);
 // COL_NMSE: forward column FFT + Parseval error vs X0 off the mask (no IFFT)
