@@ -329,9 +329,7 @@ struct Seq {
         Launch L(p, cls, st);
         if (c256() && (mode == COL_VDAMP || mode == COL_FINAL || mode == COL_NMSE)) {
             const int np = 2 * p->s, npp = (np + 3) & ~3;
-            const size_t tau = (size_t)np * PNT * sizeof(double) + (size_t)np * 16 * sizeof(double) +
-                               (size_t)256 * npp * sizeof(R);
-            const size_t sm = std::max((size_t)4096 * sizeof(C), tau) + (COL256_WSM ? (size_t)4096 * sizeof(R) : 0);
+            const size_t sm = (size_t)col256_region0<R>(np) + (size_t)256 * npp * sizeof(R) + (size_t)np * 16 * sizeof(double);
             switch (mode) {
                 case COL_VDAMP: { auto k = col_pass256<R, COL_VDAMP>; set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
                 case COL_NMSE:  { auto k = col_pass256<R, COL_NMSE>;  set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }

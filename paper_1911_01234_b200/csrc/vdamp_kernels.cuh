@@ -577,8 +577,14 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth256(Geo g, S
 // K3 for W = 256, k = 4: register row IFFT of T2 into the strip, then per 4x4
 // block the sign c (-1)^(n1+n2) / 16 and Haar analysis levels 1..2 in registers,
 // levels 3..4 through a small shared exchange; VDAMP: r = Onsager(r; par) + Psi u
+#ifndef ANA256_MINB
+#define ANA256_MINB 4
+#endif
+#ifndef ANA256_EARLY
+#define ANA256_EARLY 0
+#endif
 template <typename R, int OUT>
-__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis256(Geo g, AnaArgs<R> p) {
+__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? ANA256_MINB : 2) analysis256(Geo g, AnaArgs<R> p) {
     pdl_enter();
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -596,11 +602,20 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis256(Geo g
     const int j1 = band_of(g.s, 1, 0), j2 = band_of(g.s, 2, 0), j3 = band_of(g.s, 3, 0), j4 = band_of(g.s, 4, 0);
     const long long o1 = (long long)st * 1024 + (2 * br) * 128 + 2 * bc;
     const long long o2 = (long long)st * 256 + br * 64 + bc;
+    C old1[3][2][2], old2[3];
     {
         C v[16];
         const C* srow = p.src + (long long)bi * p.src_bs + (long long)st * 4096 + ((tid >> 4) << 8) + (tid & 15);
 #pragma unroll
         for (int k2 = 0; k2 < 16; ++k2) v[k2] = srow[16 * k2];
+        if (ANA256_EARLY && OUT == ANA_OUT_VDAMP) {
+#pragma unroll
+            for (int o = 0; o < 3; ++o) {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) ld2c<C>(coef + g.off[j1 + o] + o1 + i * 128, old1[o][i][0], old1[o][i][1]);
+                old2[o] = coef[g.off[j2 + o] + o2];
+            }
+        }
         strip_ifft256_to_smem<C>(buf, v, p.tw);
     }
     const R sc = (R)g.sign_c / R(16);
@@ -645,15 +660,16 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis256(Geo g
 #pragma unroll
             for (int i = 0; i < 2; ++i) { w1[i][0] = n1[o][i][0]; w1[i][1] = n1[o][i][1]; }
             if (OUT == ANA_OUT_VDAMP) {
-                C old1[2][2];
+                if (!ANA256_EARLY) {
 #pragma unroll
-                for (int i = 0; i < 2; ++i) ld2c<C>(q1 + i * 128, old1[i][0], old1[i][1]);
-                const C old2 = *q2;
+                    for (int i = 0; i < 2; ++i) ld2c<C>(q1 + i * 128, old1[o][i][0], old1[o][i][1]);
+                    old2[o] = *q2;
+                }
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
 #pragma unroll
-                    for (int j = 0; j < 2; ++j) w1[i][j] = cadd(ons_j<R, true>(old1[i][j], spar, j1 + o), w1[i][j]);
-                w2 = cadd(ons_j<R, true>(old2, spar, j2 + o), w2);
+                    for (int j = 0; j < 2; ++j) w1[i][j] = cadd(ons_j<R, true>(old1[o][i][j], spar, j1 + o), w1[i][j]);
+                w2 = cadd(ons_j<R, true>(old2[o], spar, j2 + o), w2);
             }
 #pragma unroll
             for (int i = 0; i < 2; ++i) st2c<C>(q1 + i * 128, w1[i][0], w1[i][1]);
@@ -661,8 +677,10 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis256(Geo g
         }
     }
     __syncthreads();
-    // level 3: 64 threads, one per 8x8 block (2 rows x 32 columns of level-3 coefficients)
-    if (tid < 64) {
+    // level 3: 64 threads, one per 8x8 block (2 rows x 32 columns of level-3 coefficients);
+    // the other warps are done (warps 0-1 meet at named barrier 1 below)
+    if (tid >= 64) return;
+    {
         const int r3 = tid >> 5, c3 = tid & 31;
         const C x00 = x2[2 * r3][2 * c3], x01 = x2[2 * r3][2 * c3 + 1];
         const C x10 = x2[2 * r3 + 1][2 * c3], x11 = x2[2 * r3 + 1][2 * c3 + 1];
@@ -678,7 +696,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis256(Geo g
             *q = n3[o];
         }
     }
-    __syncthreads();
+    asm volatile("bar.sync 1, 64;" ::: "memory");
     // level 4: 16 threads, one per 16x16 block; the approximation goes to subband 0
     // (s == 4) or to the next pass's scratch image (s > 4)
     if (tid < 16) {
@@ -898,11 +916,12 @@ template <> __device__ __forceinline__ void ld4<double>(const double* q, double&
 // X[d + 16 k2] after the forward FFT, applies the residual / finalize step to
 // those 16 frequencies and runs the inverse FFT from them directly; outputs are
 // rows d + 16 n2.  Modes: COL_VDAMP, COL_FINAL, COL_NMSE.
-// COL256_WSM=1 parks the tau weights in shared memory across the inverse FFT
-// (measured 1% slower than keeping them in registers)
-#ifndef COL256_WSM
-#define COL256_WSM 0
-#endif
+// bytes of col_pass256's first shared region: the transpose tile, later the
+// tau partials [np][256] and column sums [np][16] (doubles)
+template <typename R>
+__host__ __device__ constexpr int col256_region0(int np) {
+    return (4096 * 2 * (int)sizeof(R) > np * (256 + 16) * 8) ? 4096 * 2 * (int)sizeof(R) : np * (256 + 16) * 8;
+}
 #ifndef COL256_MINB
 #define COL256_MINB 3
 #endif
@@ -917,6 +936,12 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? COL256_MINB : 2) col_pas
     const int c0 = tile << 4;
     const long long ib = (long long)bi * g.N;
     const long long colbase = ib + (long long)d * W + c0 + c;   // row d of this thread's column
+    // shared layout: [0, A) transpose tile, later the tau partials; then the row
+    // profiles [256][npp] (R) and this tile's column profiles [np][16] (double)
+    const int np = 2 * g.s, npp = (np + 3) & ~3;
+    const int A = col256_region0<R>(np);
+    R* prs = reinterpret_cast<R*>(smem_raw + A);
+    double* pcs = reinterpret_cast<double*>(smem_raw + A + 256 * npp * (int)sizeof(R));
     if (MODE != COL_NMSE) {
         // the measurements do not depend on the previous kernel: pull this
         // tile's rows of y and 1/p towards L2 before waiting on it
@@ -924,6 +949,14 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? COL256_MINB : 2) col_pas
         prefetch_l2(p.yg + ri);
         if (sizeof(R) == 8) prefetch_l2(p.yg + ri + 8);
         prefetch_l2(p.pinv + ri);
+    }
+    if (MODE == COL_VDAMP) {
+        // constant profiles, staged before the wait as well
+        for (int i = tid; i < 256 * npp; i += PNT) {
+            const int k = i / npp, q = i - k * npp;
+            prs[i] = (q < np) ? (R)p.prow[q * 256 + k] : R(0);
+        }
+        for (int i = tid; i < np * 16; i += PNT) pcs[i] = p.pcol[(long long)(i >> 4) * W + c0 + (i & 15)];
     }
     pdl_enter();
     C v[16];
@@ -953,15 +986,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? COL256_MINB : 2) col_pas
         return;
     }
     const R cs = (R)g.sign_c;
-    // tau weights go to shared memory right away (frees 16 registers across the
-    // inverse FFT): wsm[k2][tid], past the transpose / tau-partial region
-    const int np = 2 * g.s, npp = (np + 3) & ~3;
-    const int tau_bytes = np * PNT * 8 + np * 16 * 8 + 256 * npp * (int)sizeof(R);
-#if COL256_WSM
-    R* wsm = reinterpret_cast<R*>(smem_raw + (tau_bytes > 4096 * (int)sizeof(C) ? tau_bytes : 4096 * (int)sizeof(C)));
-#else
     R wreg[16];
-#endif
     {
         const double nv = (MODE == COL_VDAMP) ? p.noise_var[bi] : 0.0;
         R pvs[16];
@@ -990,11 +1015,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? COL256_MINB : 2) col_pas
             } else {  // COL_FINAL: measured k-space where sampled (src/vdamp.py:147-150)
                 v[k2] = (pv != R(0)) ? ys[k2] : X;
             }
-#if COL256_WSM
-            if (MODE == COL_VDAMP) wsm[k2 * PNT + tid] = wk;
-#else
             wreg[k2] = wk;
-#endif
         }
     }
     fft256_stage_a<C, true>(v, d, p.tw);
@@ -1016,23 +1037,13 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? COL256_MINB : 2) col_pas
     __syncthreads();                                       // inverse transpose reads done
     double* part = reinterpret_cast<double*>(buf);         // [np][PNT] thread partials
     double* psum = part + np * PNT;                        // [np][16] column partials
-    R* prs = reinterpret_cast<R*>(psum + np * 16);         // [256][npp] row profiles
-    for (int i = tid; i < 256 * npp; i += PNT) {
-        const int k = i / npp, q = i - k * npp;
-        prs[i] = (q < np) ? (R)p.prow[q * 256 + k] : R(0);
-    }
-    __syncthreads();
     for (int q0 = 0; q0 < np; q0 += 4) {
         R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
 #pragma unroll
         for (int k2 = 0; k2 < 16; ++k2) {
             R b0, b1, b2, b3;
             ld4<R>(prs + (d + 16 * k2) * npp + q0, b0, b1, b2, b3);
-#if COL256_WSM
-            const R wk = wsm[k2 * PNT + tid];
-#else
             const R wk = wreg[k2];
-#endif
             a0 += b0 * wk; a1 += b1 * wk; a2 += b2 * wk; a3 += b3 * wk;
         }
         part[q0 * PNT + tid] = (double)a0;
@@ -1050,9 +1061,8 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? COL256_MINB : 2) col_pas
     for (int j = tid; j < g.S; j += PNT) {
         int pr_, pc_;
         band_profiles(g.s, j, pr_, pc_);
-        const double* Bc = p.pcol + (long long)pc_ * W + c0;
         double sacc = 0.0;
-        for (int cc = 0; cc < 16; ++cc) sacc += Bc[cc] * psum[pr_ * 16 + cc];
+        for (int cc = 0; cc < 16; ++cc) sacc += pcs[pc_ * 16 + cc] * psum[pr_ * 16 + cc];
         p.taupart[((long long)bi * p.ntiles + tile) * g.S + j] = sacc;
     }
 }
