@@ -289,7 +289,9 @@ def main():
     launches = plan.launch_count()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     # per-kernel-class breakdown (roofline): the same steps again with CUDA
-    # events around every launch, on the launching stream; not used for value
+    # events around every launch, on the launching stream; not used for value.
+    # One lane, so each event pair brackets its own kernel only.
+    plan.set_lanes(1)
     plan.set_timing(True)
     for i in range(args.steps):
         flush.fill_(float(i))

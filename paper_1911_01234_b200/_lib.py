@@ -53,6 +53,7 @@ SIGNATURES = {
     "vdamp_set_timing": (_I, [_P, _I]),
     "vdamp_kernel_times": (_I, [_P, _DP, _I64P]),
     "vdamp_set_graphs": (_I, [_P, _I]),
+    "vdamp_set_lanes": (_I, [_P, _I]),
     "vdamp_mc_accumulate": (_I, [_P, _P, _P, _P, _P, _P, _P]),
     "vdamp_baseline_run": (_I, [_P, _I, _I, _P, _P, _P, _P, _P]),
     "vdamp_launch_count": (_I, [_P, _I64P, _I]),

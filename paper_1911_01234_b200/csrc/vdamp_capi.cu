@@ -91,6 +91,13 @@ struct Plan {
     cudaStream_t gstream = nullptr; // capture/launch stream when the caller passes the legacy default stream
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // image lanes: vdamp_run (throughput path: no trace / NMSE / snapshots) runs
+    // the batch as `lanes` contiguous image ranges on their own streams, so one
+    // lane's latency-bound SURE tail overlaps the FFT kernels of the others
+    int lanes = 1;
+    struct Lane { cudaStream_t st = nullptr, side = nullptr; cudaEvent_t fork = nullptr, join = nullptr, done = nullptr; };
+    std::vector<Lane> lane;
+    cudaEvent_t lane_start = nullptr;
     bool have_meas = false;
     bool have_gt = false;
     size_t bytes = 0;
@@ -522,6 +529,20 @@ struct Seq {
     }
 };
 
+void set_lanes(Plan* p, int nl) {
+    p->lanes = std::max(1, std::min(p->B, nl));
+    while ((int)p->lane.size() < p->lanes) {
+        Plan::Lane l;
+        CK(cudaStreamCreateWithFlags(&l.st, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&l.side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&l.fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&l.join, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming));
+        p->lane.push_back(l);
+    }
+    if (p->lanes > 1 && !p->lane_start) CK(cudaEventCreateWithFlags(&p->lane_start, cudaEventDisableTiming));
+}
+
 template <typename F>
 int guard(F&& f) {
     try {
@@ -567,6 +588,11 @@ void free_plan(Plan* p) {
     if (p->ev_in) cudaEventDestroy(p->ev_in);
     if (p->ev_out) cudaEventDestroy(p->ev_out);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+    for (auto& l : p->lane) {
+        cudaStreamDestroy(l.st); cudaStreamDestroy(l.side);
+        cudaEventDestroy(l.fork); cudaEventDestroy(l.join); cudaEventDestroy(l.done);
+    }
+    if (p->lane_start) cudaEventDestroy(p->lane_start);
     if (p->ev_join) cudaEventDestroy(p->ev_join);
     delete p;
 }
@@ -696,6 +722,11 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         if (const char* ge = getenv("VDAMP_GRAPHS")) p->graphs = atoi(ge) != 0;
         CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+        // lanes of ~16 images (cfg1, 64 x 256^2: 1 lane 337k, 4 lanes 366k, 8 lanes
+        // 354k img-iter/s); VDAMP_LANES overrides
+        int nl = std::max(1, std::min(8, batch / 16));
+        if (const char* le = getenv("VDAMP_LANES")) nl = atoi(le);
+        set_lanes(p, nl);
         CK(cudaMemset(p->yg, 0, img * cs));
         CK(cudaMemset(p->pinv, 0, img * rs));
         if (precision == VDAMP_FP32) {
@@ -802,6 +833,37 @@ int vdamp_set_ground_truth(vdamp_plan_t plan, const void* x0, void* stream) {
     });
 }
 
+// A view of images [b0, b0 + nb) of plan p: every batch-indexed buffer offset,
+// B = nb, the lane's side stream and events.  Launch counts and timing events
+// are merged back by lane_merge.
+Plan lane_view(const Plan* p, int b0, int nb, const Plan::Lane& l) {
+    Plan v = *p;
+    const size_t rs = p->prec == VDAMP_FP32 ? sizeof(float) : sizeof(double);
+    const size_t ci = (size_t)b0 * p->N * p->csz, ri = (size_t)b0 * p->N * rs;
+    auto off = [](void* q, size_t b) -> void* { return q ? (void*)((char*)q + b) : nullptr; };
+    v.r = off(p->r, ci); v.T1 = off(p->T1, ci); v.T2 = off(p->T2, ci); v.yg = off(p->yg, ci);
+    v.pinv = off(p->pinv, ri); v.kA = off(p->kA, ri); v.kB = off(p->kB, ri);
+    for (size_t i = 1; i < p->passes.size(); ++i)
+        v.scratch[i] = off(p->scratch[i], (size_t)b0 * p->passes[i].Ha * p->passes[i].Wa * p->csz);
+    v.par = p->par + (size_t)b0 * p->S * 3;
+    v.parf = p->parf + (size_t)b0 * p->S * 3;
+    v.taupart = p->taupart + (size_t)b0 * p->ntiles * p->S;
+    v.nvar = p->nvar + b0;
+    v.trtmp = p->trtmp + (size_t)b0 * p->S * TRACE_F;
+    v.B = nb;
+    v.side = l.side; v.ev_fork = l.fork; v.ev_join = l.join;
+    v.ev.clear();
+    v.lane.clear(); v.lanes = 1;
+    return v;
+}
+
+void lane_merge(Plan* p, Plan& v, long long l0, const long long* c0) {
+    p->launches += v.launches - l0;
+    for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) p->cls_launches[c] += v.cls_launches[c] - c0[c];
+    for (auto& e : v.ev) p->ev.push_back(e);
+    if (v.pend != cudaSuccess && p->pend == cudaSuccess) p->pend = v.pend;
+}
+
 int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double* nmse, void* const* snapshots,
               void* stream) {
     return guard([&] {
@@ -812,6 +874,31 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
         if (!x_hat) throw Err{VDAMP_ERR_ARG, "null x_hat"};
         cudaStream_t caller = (cudaStream_t)stream;
         cudaStream_t st = caller;
+        if (!p->graphs && p->lanes > 1 && !trace && !nmse && !snapshots) {
+            CK(cudaSetDevice(p->dev));
+            CK(cudaEventRecord(p->lane_start, caller));
+            const int L = p->lanes;
+            for (int li = 0; li < L; ++li) {
+                const int b0 = (int)((long long)p->B * li / L), b1 = (int)((long long)p->B * (li + 1) / L);
+                Plan::Lane& l = p->lane[li];
+                CK(cudaStreamWaitEvent(l.st, p->lane_start, 0));
+                Plan v = lane_view(p, b0, b1 - b0, l);
+                long long c0[VDAMP_KERNEL_CLASSES];
+                for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) c0[c] = v.cls_launches[c];
+                const long long l0 = v.launches;
+                void* xo = (char*)x_hat + (size_t)b0 * p->N * p->csz;
+                try {
+                    dispatch(&v, (void*)l.st, [&](auto& s) {
+                        typedef typename std::remove_reference<decltype(s)>::type S_;
+                        s.run(n_iters, (typename S_::C*)xo, nullptr, nullptr, nullptr);
+                    });
+                } catch (...) { lane_merge(p, v, l0, c0); throw; }
+                lane_merge(p, v, l0, c0);
+                CK(cudaEventRecord(l.done, l.st));
+                CK(cudaStreamWaitEvent(caller, l.done, 0));
+            }
+            return;
+        }
         if (!p->graphs) {
             dispatch(p, stream, [&](auto& s) {
                 typedef typename std::remove_reference<decltype(s)>::type S_;
@@ -1069,6 +1156,15 @@ int vdamp_set_graphs(vdamp_plan_t plan, int enable) {
         Plan* p = P(plan);
         p->graphs = enable != 0;
         drop_graph(p);
+    });
+}
+
+int vdamp_set_lanes(vdamp_plan_t plan, int lanes) {
+    return guard([&] {
+        Plan* p = P(plan);
+        if (lanes < 1) throw Err{VDAMP_ERR_ARG, "lanes must be >= 1"};
+        CK(cudaSetDevice(p->dev));
+        set_lanes(p, lanes);
     });
 }
 

@@ -187,6 +187,10 @@ class Plan:
     def set_graphs(self, enable: bool):
         _lib.check(_lib.load().vdamp_set_graphs(self.handle, int(bool(enable))))
 
+    def set_lanes(self, lanes: int):
+        """Run the batch as `lanes` image ranges on their own streams (throughput path)."""
+        _lib.check(_lib.load().vdamp_set_lanes(self.handle, int(lanes)))
+
     def launch_count(self, reset=False) -> int:
         v = ctypes.c_int64()
         _lib.check(_lib.load().vdamp_launch_count(self.handle, ctypes.byref(v), int(bool(reset))))
