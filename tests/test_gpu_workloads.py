@@ -205,3 +205,21 @@ def test_streaming_reconstructor_matches_sync():
     srec.wait()
     for o in outs:
         assert torch.equal(o, ref)
+
+
+def test_lanes_bitwise_equal():
+    """The throughput path's image lanes (vdamp_set_lanes) give bitwise the same x_hat as one lane."""
+    import torch
+    from paper_1911_01234_b200 import vdamp, workload
+    w = workload.make_workload("cfg1", batch=12)
+    inp = vdamp.prepare_batch(w.ys, w.masks, w.pmap, w.noise_vars)
+    rec = vdamp.BatchReconstructor(256, 256, 4, 12, precision="fp32")
+    args = rec.upload(inp, pin=False)
+    outs = []
+    for lanes in (1, 3, 5):
+        rec.plan.set_lanes(lanes)
+        outs.append(rec(args["y"], args["indices"], args["counts"], args["probs"], args["noise_var"], 6,
+                        shared_probs=args["shared_probs"]).cpu().numpy().copy())
+    rec.plan.set_lanes(1)
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    assert np.isfinite(outs[0]).all()
