@@ -51,6 +51,7 @@ struct Plan {
     std::vector<int> item_list;
     size_t csz;                     // bytes per complex element
     int cw, logcw, ntiles, rowlog;  // column tile width, row_pass rows per CTA
+    int nsm = 148;                  // SMs of the device
     // device buffers
     void* r = nullptr;
     void* T1 = nullptr;
@@ -67,6 +68,15 @@ struct Plan {
     long long* offs = nullptr;      // [B+1] measurement offsets
     void* twH = nullptr;
     void* twW = nullptr;
+    // fp32 subbands > SCAP: value-range split over several CTAs (big_keys / big_range)
+    bool bigpath = false;
+    std::vector<int> large;         // subband ids
+    int big_ranges = 0, big_chunks = 0;
+    unsigned* bhist = nullptr;      // [B][nlarge][BIGB]
+    unsigned* btick = nullptr;      // [B][nlarge]
+    double* bbest = nullptr;        // [B][nlarge][ranges][4]
+    double* baux = nullptr;         // [B][nlarge][2]
+    double* berrp = nullptr;        // [B][nlarge][chunks][2]
     void* kA = nullptr;             // sort scratch (large subbands only)
     void* kB = nullptr;
     void* x0 = nullptr;             // ground truth image (owned copy)
@@ -376,10 +386,33 @@ struct Seq {
         // the small-subband kernel runs on a side stream, concurrently with the
         // big one (its CTAs fill the SMs the big kernel's tail leaves idle)
         bool forked = false;
+        if constexpr (std::is_same<R, float>::value) {
+            if (p->bigpath) {
+                // subbands > SCAP: keys + histogram, then value ranges over several CTAs
+                BigArgs b;
+                b.nlarge = (int)p->large.size(); b.ranges = p->big_ranges; b.chunks = p->big_chunks;
+                for (int i = 0; i < b.nlarge; ++i) b.list[i] = p->large[i];
+                b.hist = p->bhist; b.tick = p->btick; b.best = p->bbest; b.aux = p->baux; b.errp = p->berrp;
+                {
+                    Launch L(p, 3, st_);
+                    const size_t sm = (size_t)BIGB * sizeof(unsigned);
+                    set_smem(big_keys, sm);
+                    launch(big_keys, dim3(b.chunks, b.nlarge, p->B), 1024, sm, st_, p->geo, a, b);
+                }
+
+                {
+                    Launch L(p, 3, st_);
+                    const size_t slot16 = ((size_t)SCAP + SCAP / 32 + 2 + 3) & ~(size_t)3;
+                    const size_t sm = 2 * slot16 * sizeof(float) + CS_WORDS * sizeof(unsigned);
+                    set_smem(big_range, sm);
+                    launch(big_range, dim3(b.ranges, b.nlarge, p->B), 1024, sm, st_, p->geo, a, b);
+                }
+            }
+        }
         for (int big = 1; big >= 0; --big) {
             std::vector<int> st{0}, li;
             for (int j = 0; j < p->S; ++j)
-                if ((p->geo.len[j] > SMALL_N) == (big == 1)) li.push_back(j);
+                if ((p->geo.len[j] > SMALL_N) == (big == 1) && !(p->bigpath && p->geo.len[j] > SCAP)) li.push_back(j);
             // longest items first (grid is image-fastest, so they are all scheduled first)
             std::stable_sort(li.begin(), li.end(), [&](int x, int y) { return p->geo.len[x] > p->geo.len[y]; });
             for (size_t i = 0; i < li.size(); ++i) st.push_back((int)i + 1);
@@ -578,7 +611,7 @@ void free_plan(Plan* p) {
     if (!p) return;
     cudaSetDevice(p->dev);
     void* bufs[] = {p->what, p->btau, p->berr, p->x0r, p->nmconst, p->nmpart, p->r, p->T1, p->T2, p->yg, p->pinv, p->par, p->parf, p->taupart, p->prow, p->pcol,
-                    p->nvar, p->offs, p->twH, p->twW, p->kA, p->kB, p->x0, p->w0, p->xtmp, p->trtmp};
+                    p->nvar, p->offs, p->twH, p->twW, p->kA, p->kB, p->bhist, p->btick, p->bbest, p->baux, p->berrp, p->x0, p->w0, p->xtmp, p->trtmp};
     for (void* b : bufs) if (b) cudaFree(b);
     for (void* b : p->scratch) if (b) cudaFree(b);
     for (auto& e : p->ev) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
@@ -710,6 +743,30 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
             if (maxlen / capk > MAXTILES) throw Err{VDAMP_ERR_UNSUPPORTED, "subband too large"};
             p->kA = dalloc(p, img * rs);
             p->kB = dalloc(p, img * rs);
+            CK(cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, device));
+            const char* be = getenv("VDAMP_BIGRANGE");
+            if (precision == VDAMP_FP32 && !(be && atoi(be) == 0)) {
+                for (int j = 0; j < p->S; ++j) if (g.len[j] > capk) p->large.push_back(j);
+                // only when the single-CTA path would leave most SMs idle: with many large
+                // subbands per batch (cfg2: 32 x 3) it fills the GPU and is measured faster
+                // (482 vs 708 us per iteration); cfg3 (1 x 6) gains 4x
+                const bool few = (long long)batch * (long long)p->large.size() * 4 <= (long long)p->nsm ||
+                                 (be && atoi(be) == 1);
+                if (!few) p->large.clear();
+                if (few && (int)p->large.size() <= BIG_MAXL && (maxlen + capk / 2 - 1) / (capk / 2) <= BIG_RMAX) {
+                    p->bigpath = true;
+                    const size_t nl = p->large.size();
+                    p->big_ranges = (maxlen + capk / 2 - 1) / (capk / 2);
+                    p->big_chunks = (maxlen + BIG_CHUNK - 1) / BIG_CHUNK;
+                    p->bhist = (unsigned*)dalloc(p, (size_t)batch * nl * BIGB * sizeof(unsigned));
+                    p->btick = (unsigned*)dalloc(p, (size_t)batch * nl * sizeof(unsigned));
+                    p->bbest = (double*)dalloc(p, (size_t)batch * nl * p->big_ranges * 4 * sizeof(double));
+                    p->baux = (double*)dalloc(p, (size_t)batch * nl * 2 * sizeof(double));
+                    p->berrp = (double*)dalloc(p, (size_t)batch * nl * p->big_chunks * 2 * sizeof(double));
+                    CK(cudaMemset(p->bhist, 0, (size_t)batch * nl * BIGB * sizeof(unsigned)));
+                    CK(cudaMemset(p->btick, 0, (size_t)batch * nl * sizeof(unsigned)));
+                }
+            }
         }
         CK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&p->gstream, cudaStreamNonBlocking));
@@ -850,6 +907,14 @@ Plan lane_view(const Plan* p, int b0, int nb, const Plan::Lane& l) {
     v.taupart = p->taupart + (size_t)b0 * p->ntiles * p->S;
     v.nvar = p->nvar + b0;
     v.trtmp = p->trtmp + (size_t)b0 * p->S * TRACE_F;
+    if (p->bigpath) {
+        const size_t nl = p->large.size();
+        v.bhist = p->bhist + (size_t)b0 * nl * BIGB;
+        v.btick = p->btick + (size_t)b0 * nl;
+        v.bbest = p->bbest + (size_t)b0 * nl * p->big_ranges * 4;
+        v.baux = p->baux + (size_t)b0 * nl * 2;
+        v.berrp = p->berrp + (size_t)b0 * nl * p->big_chunks * 2;
+    }
     v.B = nb;
     v.side = l.side; v.ev_fork = l.fork; v.ev_join = l.join;
     v.ev.clear();

@@ -1634,7 +1634,7 @@ __device__ R* global_merge_sort(R* A, R* B, R* smem, int n, int CAP) {
 // Evaluate the candidates owned by this thread on one tile of sorted
 // magnitudes (src/denoise.py:62-118):  candidate t = m_i at the end of each
 // tie run, plus the stationary point of the quadratic piece that starts there.
-template <typename R, int NT, int EMAX, bool SMEM, int EFIX>
+template <typename R, int NT, int EMAX, bool SMEM, int EFIX, bool RAG>
 __device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, int n, double tau, int b0, int E,
                                           double pre, double suf, double next_tile_first, Best& best,
                                           const double* sreg, const double* slo, const double* shi);
@@ -1645,7 +1645,9 @@ __device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, in
 // cancels.  The per-key suffixes go to shared scratch (slo/shi, key e of thread
 // t at [e * NT + t], conflict-free; keys e >= EMAX/2 in shi) when SMEM, to
 // registers otherwise (small E only: a register array of 16 doubles spills).
-template <typename R, int NT, int EMAX, bool SMEM, int EFIX = 0>
+// RAG: T < NT * EFIX real keys (the rest of the sorted tile is padding above
+// them and is skipped)
+template <typename R, int NT, int EMAX, bool SMEM, int EFIX = 0, bool RAG = false>
 __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, int n, double tau,
                                           double pre_tile, double suf_tile, double next_tile_first,
                                           double* sh, Best* wbest, Best* run, double* totinv, double* slo,
@@ -1660,7 +1662,7 @@ __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, in
 #endif
     // EFIX > 0: T == NT * EFIX known at compile time (fully unrolled, unguarded)
     const int E = EFIX ? EFIX : (T >= NT ? T / NT : 1);
-    const bool act = EFIX ? true : tid * E < T;
+    const bool act = EFIX ? (!RAG || tid * E < T) : tid * E < T;
     const int b0 = tid * E;
     constexpr int HALF = EMAX / 2 > 0 ? EMAX / 2 : 1;
     constexpr bool FKEY = sizeof(R) == 4;
@@ -1670,7 +1672,7 @@ __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, in
         // one conversion per key (F2F/I2F/MUFU issue at 1/4 of the DFMA rate)
 #pragma unroll ((SMEM && !EFIX) ? 4 : EMAX)
         for (int e = EMAX - 1; e >= 0; --e) {
-            if (e < E) {
+            if (e < E && (!RAG || b0 + e < T)) {
                 if constexpr (SMEM) (e < HALF ? slo : shi)[(e % HALF) * NT + tid] = sinv;
                 else sreg[e] = sinv;
                 const double m = (double)keys[KI(b0 + e)];
@@ -1686,7 +1688,7 @@ __device__ __forceinline__ void scan_tile(const R* keys, int T, int tilebase, in
     suf += suf_tile;
     if (tid == 0 && tilebase == 0) *totinv = suf + sinv;     // sum of all inverses
     SC_MARK(1);
-    if (act) scan_keys<R, NT, EMAX, SMEM, EFIX>(keys, T, tilebase, n, tau, b0, E, pre, suf, next_tile_first, best,
+    if (act) scan_keys<R, NT, EMAX, SMEM, EFIX, RAG>(keys, T, tilebase, n, tau, b0, E, pre, suf, next_tile_first, best,
                                           sreg, slo, shi);
     // tile argmin (ties -> smaller t) merged into the running best by thread 0
     for (int o = 16; o > 0; o >>= 1) {
@@ -1730,7 +1732,7 @@ __device__ __forceinline__ double div_pos(double a, double b) {
 // the loop; the winner's (t, count, inverse sum) are rebuilt afterwards.
 // Candidates arrive in increasing t, so a strict '<' keeps the smaller t of
 // a tie.
-template <typename R, int NT, int EMAX, bool SMEM, int EFIX>
+template <typename R, int NT, int EMAX, bool SMEM, int EFIX, bool RAG>
 __device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, int n, double tau, int b0, int E,
                                           double pre, double suf, double next_tile_first, Best& best,
                                           const double* sreg, const double* slo, const double* shi) {
@@ -1744,7 +1746,7 @@ __device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, in
     int bcode = -1;
 #pragma unroll (SMEM ? 4 : EMAX)
     for (int e = 0; e < EMAX; ++e) {
-        if (e < E) {
+        if (e < E && (!RAG || b0 + e < T)) {
             const int il = b0 + e;
             zacc += m * m;                                     // sum_{j <= i} m_j^2
             cnt -= 1.0;
@@ -2094,6 +2096,298 @@ __global__ void __launch_bounds__(NT, NT >= BNT32 ? 1 : 4) sure_select(Geo g, Se
     for (int q = a.item_start[it]; q < a.item_start[it + 1]; ++q) {
         select_band<R, NT>(g, a, a.item_list[q], bi, keys, S_);
         __syncthreads();
+    }
+}
+
+// -------------------------------------------- K4, subbands > SCAP (fp32) ----
+// A subband of n > SCAP keys is split by value over several CTAs:
+//  big_keys:  |r| -> kA and a histogram of the float bits >> 17 (1/64 octave,
+//             BIGB buckets) per subband; trace error partials per chunk.
+//  big_range: CTA q of a subband owns the buckets whose exclusive prefix count
+//             lies in [q T, (q+1) T), T = SCAP - (largest bucket), so it holds at
+//             most SCAP keys.  One pass over the subband (loads batched 8 deep)
+//             gathers them into shared memory while summing m^2 of the keys below
+//             and 1/m of the keys above in float64 (fixed per-thread order + tree:
+//             deterministic, no cancellation); the keys are counting-sorted and
+//             scanned exactly with those offsets.  The last CTA of the subband
+//             (ticket) merges the range winners (ties -> smaller t), adds t = 0
+//             and writes the parameters.  A bucket > SCAP/2 (massive ties) falls
+//             back to the single-CTA global path (select_band) for that subband.
+constexpr int BIGB = 16384;          // histogram buckets: positive float bits >> 17
+constexpr int BIG_CHUNK = 16384;     // keys per big_keys CTA (1024 threads x 16)
+constexpr int BIG_MAXL = 12;         // subbands > SCAP per image
+constexpr int BIG_RMAX = 64;         // value ranges per subband (n <= 2^20 at T >= SCAP/2)
+
+struct BigArgs {
+    int nlarge, ranges, chunks;      // large subbands, big_range CTAs and chunk CTAs per subband
+    int list[BIG_MAXL];              // their subband ids
+    unsigned* hist;                  // [B][nlarge][BIGB] (zero between uses)
+    unsigned* tick;                  // [B][nlarge] (zero between uses)
+    double* best;                    // [B][nlarge][ranges][4]
+    double* aux;                     // [B][nlarge][2]: sum of all 1/m, smallest key
+    double* errp;                    // [B][nlarge][chunks][2]: trace |r - w0|^2, |w0|^2
+};
+
+__global__ void __launch_bounds__(1024) big_keys(Geo g, SelArgs<float> a, BigArgs b) {
+    pdl_enter();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned* hs = reinterpret_cast<unsigned*>(smem_raw);    // [BIGB]
+    __shared__ double sh[40];
+    const int ch = blockIdx.x, jl = blockIdx.y, bi = blockIdx.z, tid = threadIdx.x;
+    const int j = b.list[jl], n = g.len[j];
+    const int e0 = ch * BIG_CHUNK;
+    if (e0 >= n) return;
+    const long long base = (long long)bi * g.N + g.off[j];
+    for (int i = tid; i < BIGB; i += 1024) hs[i] = 0;
+    __syncthreads();
+    double err = 0.0, ref = 0.0;
+#pragma unroll 4
+    for (int q = 0; q < BIG_CHUNK / 1024; ++q) {
+        const int e = e0 + tid + q * 1024;
+        if (e < n) {
+            const float2 v = a.r[base + e];
+            const float m = cmag(v);
+            a.kA[base + e] = m;
+            atomicAdd(&hs[__float_as_uint(m) >> 17], 1u);
+            if (a.w0) {
+                const float2 w = a.w0[base + e];
+                const double dx = (double)v.x - (double)w.x, dy = (double)v.y - (double)w.y;
+                err += dx * dx + dy * dy;
+                ref += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
+            }
+        }
+    }
+    __syncthreads();
+    unsigned* hg = b.hist + ((long long)bi * b.nlarge + jl) * BIGB;
+    for (int i = tid; i < BIGB; i += 1024)
+        if (hs[i]) atomicAdd(&hg[i], hs[i]);
+    if (a.w0) {
+        err = block_sum<1024>(err, sh);
+        ref = block_sum<1024>(ref, sh);
+        if (tid == 0) {
+            double* ep = b.errp + (((long long)bi * b.nlarge + jl) * b.chunks + ch) * 2;
+            ep[0] = err; ep[1] = ref;
+        }
+    }
+}
+
+// histogram -> exclusive prefix counts in cbs[BIGB], largest bucket, last
+// nonempty bucket (1024 threads; sh needs 66 + 34 doubles, su 2 words)
+__device__ __forceinline__ void big_prefix(const unsigned* hg, unsigned* cbs, double* sh, unsigned* su,
+                                           unsigned& maxb, int& blast) {
+    constexpr int NT = 1024, HPT = BIGB / NT;
+    const int tid = threadIdx.x;
+    unsigned h[HPT], hsum = 0, hmax = 0;
+    int hl = -1;
+#pragma unroll
+    for (int i = 0; i < HPT; ++i) {
+        h[i] = __ldcg(hg + tid * HPT + i);
+        hsum += h[i];
+        hmax = max(hmax, h[i]);
+        if (h[i]) hl = tid * HPT + i;
+    }
+    unsigned P = (unsigned)block_excl_scan<NT, false>((double)hsum, sh + 66);
+#pragma unroll
+    for (int i = 0; i < HPT; ++i) { cbs[tid * HPT + i] = P; P += h[i]; }
+    for (int o = 16; o > 0; o >>= 1) {
+        hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+        hl = max(hl, __shfl_xor_sync(0xffffffffu, hl, o));
+    }
+    if (tid < 2) su[tid] = 0;
+    __syncthreads();
+    if ((tid & 31) == 0) { atomicMax(&su[0], hmax); atomicMax(&su[1], (unsigned)(hl + 1)); }
+    __syncthreads();
+    maxb = su[0];
+    blast = (int)su[1] - 1;
+}
+
+template <typename R, int NT> __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R* keys,
+                                                          SelShared<NT>& S_);
+
+__global__ void __launch_bounds__(1024, 1) big_range(Geo g, SelArgs<float> a, BigArgs b) {
+    pdl_enter();
+    constexpr int NT = 1024;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* keys = reinterpret_cast<float*>(smem_raw);
+    constexpr int SLOT = (SCAP + SCAP / 32 + 2 + 3) & ~3;
+    float* stage = keys + SLOT;
+    unsigned* ccnt = reinterpret_cast<unsigned*>(stage + SLOT);
+    __shared__ SelShared<NT> S_;
+    __shared__ unsigned s_u[4];
+    __shared__ int s_last;
+    double* sh = S_.sh;
+    const int q = blockIdx.x, jl = blockIdx.y, bi = blockIdx.z, tid = threadIdx.x;
+    const int j = b.list[jl], n = g.len[j];
+    const long long base = (long long)bi * g.N + g.off[j];
+    const long long sb = (long long)bi * b.nlarge + jl;
+    unsigned* cbs = reinterpret_cast<unsigned*>(stage);         // bucket -> exclusive prefix count
+    static_assert(BIGB <= SLOT, "histogram prefix must fit the stage region");
+    if (tid == 0) { mbar_init(&S_.mbar, 1); S_.mphase = 0; }
+    unsigned maxb;
+    int blast;
+    big_prefix(b.hist + sb * BIGB, cbs, sh, s_u, maxb, blast);
+    const bool fallback = maxb > (unsigned)(SCAP / 2) || blast < 0;
+    const unsigned T = (unsigned)SCAP - maxb;
+    const int nranges = fallback ? 1 : (int)(cbs[blast] / T) + 1;
+    int Tn = 0, s0 = 0;
+    double ssq = 0.0, sinv = 0.0, nxt = INFINITY;
+    unsigned kmn = 0xffffffffu, kmx = 0;
+    if (fallback) {
+        if (q == 0) select_band<float, NT>(g, a, j, bi, keys, S_);
+    } else if (q < nranges) {
+        // tau (column-tile partials in tile order, or given)
+        if (!a.tau_in)
+            for (int i = tid; i < a.ntiles; i += NT) S_.tpart[i] = a.taupart[((long long)bi * a.ntiles + i) * g.S + j];
+        const unsigned lo = (unsigned)q * T, hi = lo + T;
+        if (tid == 0) s_u[2] = 0;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            if (a.tau_in) t = a.tau_in[(long long)bi * g.S + j];
+            else for (int i = 0; i < a.ntiles; ++i) t += S_.tpart[i];
+            S_.tau = t;
+        }
+        // one pass over the subband: own keys -> smem, offsets of the others
+        float nmin = INFINITY;
+        unsigned nbelow = 0;
+        const int lane = tid & 31;
+        constexpr int LB = 8;
+        for (int e0 = 0; e0 < n; e0 += NT * LB) {
+            float kk[LB];
+#pragma unroll
+            for (int u = 0; u < LB; ++u) {
+                const int e = e0 + tid + u * NT;
+                kk[u] = e < n ? __ldcg(a.kA + base + e) : -1.0f;
+            }
+#pragma unroll
+            for (int u = 0; u < LB; ++u) {
+                const float k = kk[u];
+                int cls = -1;                                      // 0 below, 1 own, 2 above
+                if (k >= 0.0f) {
+                    const unsigned c = cbs[__float_as_uint(k) >> 17];
+                    cls = c < lo ? 0 : (c < hi ? 1 : 2);
+                }
+                if (cls == 0) { ssq = fma((double)k, (double)k, ssq); ++nbelow; }
+                else if (cls == 2) { if (k > 0.0f) sinv += rcp_posf((double)k); nmin = fminf(nmin, k); }
+                const unsigned own = __ballot_sync(0xffffffffu, cls == 1);
+                if (own) {
+                    unsigned wb = 0;
+                    if (lane == 0) wb = atomicAdd(&s_u[2], (unsigned)__popc(own));
+                    wb = __shfl_sync(0xffffffffu, wb, 0);
+                    if (cls == 1) {
+                        const unsigned uk = __float_as_uint(k);
+                        keys[KI((int)(wb + __popc(own & ((1u << lane) - 1u))))] = k;
+                        if (uk) kmn = min(kmn, uk);
+                        kmx = max(kmx, uk);
+                    }
+                }
+            }
+        }
+        ssq = block_sum<NT>(ssq, sh);
+        sinv = block_sum<NT>(sinv, sh);
+        s0 = (int)block_sum<NT>((double)nbelow, sh);
+        for (int o = 16; o > 0; o >>= 1) {
+            nmin = fminf(nmin, __shfl_xor_sync(0xffffffffu, nmin, o));
+            kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
+            kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
+        }
+        if (tid == 0) { s_u[0] = 0xffffffffu; s_u[1] = 0; s_u[3] = 0x7f800000u; }
+        __syncthreads();
+        if (lane == 0) { atomicMin(&s_u[0], kmn); atomicMax(&s_u[1], kmx); atomicMin(&s_u[3], __float_as_uint(nmin)); }
+        __syncthreads();
+        Tn = (int)s_u[2];
+        kmn = s_u[0]; kmx = s_u[1];
+        const float nm = __uint_as_float(s_u[3]);
+        nxt = nm < INFINITY ? (double)nm : INFINITY;
+        // pad to 4096 / 8192 / 16384 keys with distinct values just above the
+        // range's largest key (sorted behind the real keys, skipped by the scan)
+        const int npad = Tn <= 4096 ? 4096 : (Tn <= 8192 ? 8192 : 16384);
+        for (int i = Tn + tid; i < npad; i += NT) keys[KI(i)] = __uint_as_float(kmx + 1u + (unsigned)(i - Tn));
+        if (npad > Tn) kmx += (unsigned)(npad - Tn);
+        __syncthreads();
+        const float* skeys = keys;
+        {
+            const int cs = npad == 16384 ? counting_sort<NT, 16>(keys, stage, ccnt, npad, kmn, kmx, sh)
+                         : npad == 8192  ? counting_sort<NT, 8>(keys, stage, ccnt, npad, kmn, kmx, sh)
+                                         : counting_sort<NT, 4>(keys, stage, ccnt, npad, kmn, kmx, sh);
+            if (cs == 1) skeys = stage;
+            else if (cs == 0) block_sort<float, NT>(keys, npad);
+        }
+        // exact scan of the range with the offsets of the keys below / above
+        double* slo;
+        double* shi;
+        if (skeys == stage) { slo = reinterpret_cast<double*>(keys); shi = reinterpret_cast<double*>(ccnt); }
+        else { slo = reinterpret_cast<double*>(stage); shi = slo + 8 * NT; }
+        if (tid == 0) S_.run = Best{INFINITY, INFINITY, 0.0, 0.0};
+        const double tau = fmax(S_.tau, TAU_FLOOR);
+        if (npad == 16384)
+            scan_tile<float, NT, 16, true, 16, true>(skeys, Tn, s0, n, tau, ssq, sinv, nxt, sh, S_.best, &S_.run,
+                                                     &S_.totinv, slo, shi);
+        else if (npad == 8192)
+            scan_tile<float, NT, 16, true, 8, true>(skeys, Tn, s0, n, tau, ssq, sinv, nxt, sh, S_.best, &S_.run,
+                                                    &S_.totinv, slo, shi);
+        else
+            scan_tile<float, NT, 16, true, 4, true>(skeys, Tn, s0, n, tau, ssq, sinv, nxt, sh, S_.best, &S_.run,
+                                                    &S_.totinv, slo, shi);
+        __syncthreads();
+        if (tid == 0) {
+            double* bp = b.best + (sb * b.ranges + q) * 4;
+            bp[0] = S_.run.risk; bp[1] = S_.run.t; bp[2] = S_.run.cnt; bp[3] = S_.run.inv;
+            if (q == 0) { b.aux[sb * 2] = S_.totinv; b.aux[sb * 2 + 1] = (double)skeys[0]; }
+        }
+    }
+    // ticket: the last CTA of the subband merges, then clears histogram and cursors
+    if (tid == 0) {
+        __threadfence();
+        s_last = atomicAdd(&b.tick[sb], 1u) == (unsigned)gridDim.x - 1u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    unsigned* hg = b.hist + sb * BIGB;
+    for (int i = tid; i < BIGB; i += NT) hg[i] = 0;
+    if (tid == 0) {
+        b.tick[sb] = 0;
+        if (!fallback) {
+            Best bb{INFINITY, INFINITY, 0.0, 0.0};
+            for (int r = 0; r < nranges; ++r) {
+                const double* bp = b.best + (sb * b.ranges + r) * 4;
+                consider(bb, __ldcg(bp), __ldcg(bp + 1), __ldcg(bp + 2), __ldcg(bp + 3));
+            }
+            double s_tau = 0.0;
+            if (a.tau_in) s_tau = a.tau_in[(long long)bi * g.S + j];
+            else for (int i = 0; i < a.ntiles; ++i) s_tau += __ldcg(a.taupart + ((long long)bi * a.ntiles + i) * g.S + j);
+            const double tau = fmax(s_tau, TAU_FLOOR);
+            // candidate t = 0 when no magnitude is zero (src/denoise.py:84)
+            const double m0 = __ldcg(b.aux + sb * 2 + 1);
+            if (m0 > 0) {
+                const double totinv = __ldcg(b.aux + sb * 2);
+                const double nn = (double)n;
+                consider(bb, 0.0 + 0.0 * nn - nn * tau + tau * (2.0 * nn - 0.0 * totinv), 0.0, nn, totinv);
+                const double ts = tau * totinv / (2.0 * nn);
+                if (ts > 0.0 && ts < m0) {
+                    const double rsk = 0.0 + ts * ts * nn - nn * tau + tau * (2.0 * nn - ts * totinv);
+                    consider(bb, rsk, ts, nn, totinv);
+                }
+            }
+            const double alpha = (bb.cnt - 0.5 * bb.t * bb.inv) / (double)n;   // src/denoise.py:169
+            const bool clamped = alpha >= ALPHA_CLAMP;                         // src/vdamp.py:121-124
+            const double ac = clamped ? ALPHA_CLAMP : alpha;
+            const long long pj = ((long long)bi * g.S + j);
+            if (a.par) { a.par[3 * pj] = bb.t; a.par[3 * pj + 1] = ac; a.par[3 * pj + 2] = 1.0 / (1.0 - ac); }
+            if (a.parf) { a.parf[3 * pj] = bb.t; a.parf[3 * pj + 1] = 0.0; a.parf[3 * pj + 2] = 1.0; }
+            if (a.trace) {
+                double e2 = 0.0, r2 = 0.0;
+                if (a.w0)
+                    for (int c = 0; c * BIG_CHUNK < n; ++c) {
+                        const double* ep = b.errp + (sb * b.chunks + c) * 2;
+                        e2 += __ldcg(ep); r2 += __ldcg(ep + 1);
+                    }
+                double* tr = a.trace + pj * TRACE_F;
+                tr[0] = s_tau; tr[1] = bb.t; tr[2] = bb.t / tau; tr[3] = ac; tr[4] = alpha;
+                tr[5] = clamped ? 1.0 : 0.0; tr[6] = e2; tr[7] = r2;
+            }
+        }
     }
 }
 

@@ -198,3 +198,42 @@ def test_finalize_vs_reference(oracle):
     assert relmax(x, oracle.finalize(w, p)) <= 1e-12
     # consistency: sampled frequencies equal y
     assert relmax(oracle.forward(x, mask.indices), g["y"]) <= 1e-12
+
+
+@pytest.mark.parametrize("shape", [(512, 512, 2), (1024, 1024, 1)])
+@pytest.mark.parametrize("kind", ["gauss", "ties", "zeros", "sparse", "diverged"])
+def test_sure_select_fp32_large_subbands(oracle, shape, kind, monkeypatch):
+    """fp32 subbands > 16,384 keys (value ranges over several CTAs, big_keys/big_range;
+    massive ties fall back to the single-CTA path).  Real float32 inputs make the GPU's
+    float keys and the oracle's float64 magnitudes identical, so the argmin must agree."""
+    from paper_1911_01234_b200 import denoise, wavelet
+    from paper_1911_01234_b200.plan import clear_plans
+    h, w, s = shape
+    rng = np.random.default_rng(hash((shape, kind, 32)) % 2**32)
+    lay = wavelet.SubbandLayout.create(h, w, s)
+    z = _tricky_coeffs(rng, h * w, kind)
+    r = (np.abs(z) * np.where(rng.random(h * w) < 0.5, -1.0, 1.0)).astype(np.float32).astype(np.complex128)
+    tau = rng.uniform(0.2, 2.0, lay.n_subbands)
+    if kind == "diverged":
+        tau = tau * 1e24
+    wh_o, al_o, lam_o, t_o = oracle.denoise_colored(r, tau, oracle.band_table(h, w, s))
+    outs = {}
+    for env in ("1", "0"):
+        monkeypatch.setenv("VDAMP_BIGRANGE", env)
+        clear_plans()
+        outs[env] = denoise.denoise_colored(wavelet.WaveletCoeffs(r, lay), denoise.SubbandVector(tau),
+                                            precision="fp32")
+    clear_plans()
+    bands = oracle.band_table(h, w, s)
+    for env, (wh, al, lam) in outs.items():
+        t_g = lam.values * tau
+        same = np.isclose(t_g, t_o, rtol=1e-12, atol=0)
+        assert np.allclose(al.values[same], al_o[same], rtol=1e-9, atol=1e-12), env
+        # any other choice must be a near-tie of the exact risk (flat SURE on the
+        # diverged data: float64 sums in a different order pick a neighbour)
+        for jb in np.flatnonzero(~same):
+            seg = r[bands[jb].offset:bands[jb].offset + bands[jb].length]
+            r_g, r_o = oracle.sure_risk(seg, tau[jb], t_g[jb]), oracle.sure_risk(seg, tau[jb], t_o[jb])
+            assert r_g <= r_o + 1e-10 * abs(r_o), (env, jb, t_g[jb], t_o[jb])
+        if kind != "diverged":
+            assert same.all(), env

@@ -223,3 +223,24 @@ def test_lanes_bitwise_equal():
     rec.plan.set_lanes(1)
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
     assert np.isfinite(outs[0]).all()
+
+
+def test_cfg2_fp32_large_subband_path(monkeypatch):
+    """512^2 fp32 VDAMP: the multi-CTA large-subband SURE path (default) against the
+    single-CTA global path (VDAMP_BIGRANGE=0): same thresholds, same reconstruction."""
+    from paper_1911_01234_b200 import vdamp, workload
+    from paper_1911_01234_b200.plan import clear_plans
+    w = workload.make_workload("cfg2", batch=2)
+    res = {}
+    for env in ("1", "0"):
+        monkeypatch.setenv("VDAMP_BIGRANGE", env)
+        clear_plans()
+        res[env] = vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, 5, 8, ground_truths=w.x0,
+                                   precision="fp32")
+    clear_plans()
+    (a, ta), (b, tb) = res["1"], res["0"]
+    assert rel2(a, b) <= 1e-5
+    for t1, t2 in zip(ta, tb):
+        for r1, r2 in zip(t1.records, t2.records):
+            assert np.allclose(r1.thresholds, r2.thresholds, rtol=1e-6)
+            assert abs(r1.nmse_db - r2.nmse_db) <= 1e-3
