@@ -299,6 +299,7 @@ def main():
     torch.cuda.synchronize(dev)
     ktimes = plan.kernel_times()
     plan.set_timing(False)
+    plan.set_lanes(0)                       # back to the default lanes (the e2e arms share this plan)
     total_s = max_over_ranks(float(np.sum(step_ms)) / 1e3)
     images_all = B * world
     value = images_all * cfg.n_iters * args.steps / total_s

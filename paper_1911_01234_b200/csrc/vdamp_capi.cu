@@ -562,6 +562,14 @@ struct Seq {
     }
 };
 
+// lanes of ~16 images (cfg1, 64 x 256^2: 1 lane 337k, 4 lanes 366k, 8 lanes
+// 354k img-iter/s); VDAMP_LANES overrides
+int default_lanes(int batch) {
+    int nl = std::max(1, std::min(8, batch / 16));
+    if (const char* le = getenv("VDAMP_LANES")) nl = atoi(le);
+    return nl;
+}
+
 void set_lanes(Plan* p, int nl) {
     p->lanes = std::max(1, std::min(p->B, nl));
     while ((int)p->lane.size() < p->lanes) {
@@ -779,11 +787,7 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         if (const char* ge = getenv("VDAMP_GRAPHS")) p->graphs = atoi(ge) != 0;
         CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
-        // lanes of ~16 images (cfg1, 64 x 256^2: 1 lane 337k, 4 lanes 366k, 8 lanes
-        // 354k img-iter/s); VDAMP_LANES overrides
-        int nl = std::max(1, std::min(8, batch / 16));
-        if (const char* le = getenv("VDAMP_LANES")) nl = atoi(le);
-        set_lanes(p, nl);
+        set_lanes(p, default_lanes(batch));
         CK(cudaMemset(p->yg, 0, img * cs));
         CK(cudaMemset(p->pinv, 0, img * rs));
         if (precision == VDAMP_FP32) {
@@ -1227,9 +1231,9 @@ int vdamp_set_graphs(vdamp_plan_t plan, int enable) {
 int vdamp_set_lanes(vdamp_plan_t plan, int lanes) {
     return guard([&] {
         Plan* p = P(plan);
-        if (lanes < 1) throw Err{VDAMP_ERR_ARG, "lanes must be >= 1"};
+        if (lanes < 0) throw Err{VDAMP_ERR_ARG, "lanes must be >= 0"};
         CK(cudaSetDevice(p->dev));
-        set_lanes(p, lanes);
+        set_lanes(p, lanes == 0 ? default_lanes(p->B) : lanes);
     });
 }
 

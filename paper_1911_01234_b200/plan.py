@@ -188,7 +188,7 @@ class Plan:
         _lib.check(_lib.load().vdamp_set_graphs(self.handle, int(bool(enable))))
 
     def set_lanes(self, lanes: int):
-        """Run the batch as `lanes` image ranges on their own streams (throughput path)."""
+        """Run the batch as `lanes` image ranges on their own streams (throughput path; 0 = default)."""
         _lib.check(_lib.load().vdamp_set_lanes(self.handle, int(lanes)))
 
     def launch_count(self, reset=False) -> int:

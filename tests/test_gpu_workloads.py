@@ -220,7 +220,7 @@ def test_lanes_bitwise_equal():
         rec.plan.set_lanes(lanes)
         outs.append(rec(args["y"], args["indices"], args["counts"], args["probs"], args["noise_var"], 6,
                         shared_probs=args["shared_probs"]).cpu().numpy().copy())
-    rec.plan.set_lanes(1)
+    rec.plan.set_lanes(0)
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
     assert np.isfinite(outs[0]).all()
 
