@@ -298,6 +298,7 @@ struct Seq {
             Launch L(p, cls, st);
             if (first && rowifft && f256(ps)) {
                 if (vdamp_mode) {
+                    if (ANA256_TMA) sm += 4096 * sizeof(C) + 16;        // old-coefficient landing zone
                     auto k = analysis256<R, ANA_OUT_VDAMP>; set_smem(k, sm);
                     launch(k, grid, PNT, sm, st, p->geo, a);
                 } else {

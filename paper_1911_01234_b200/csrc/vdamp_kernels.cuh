@@ -583,9 +583,14 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth256(Geo g, S
 #ifndef ANA256_EARLY
 #define ANA256_EARLY 0
 #endif
+// ANA256_TMA: the strip's previous coefficients (levels 1-4 and the approximation,
+// 4096 complex) are bulk-copied into shared memory before the PDL wait (they
+// were written four kernels back), overlapping the T2 loads and the row IFFT
+#ifndef ANA256_TMA
+#define ANA256_TMA 1
+#endif
 template <typename R, int OUT>
 __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? ANA256_MINB : 2) analysis256(Geo g, AnaArgs<R> p) {
-    pdl_enter();
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* buf = reinterpret_cast<C*>(smem_raw);
@@ -595,13 +600,32 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? ANA256_MINB : 2) analysi
     __shared__ R spar[MAXS * 3];
     __shared__ C x2[4][64];                                 // level-2 approximations
     __shared__ C x3[2][32];                                 // level-3 approximations
+    const int j1 = band_of(g.s, 1, 0), j2 = band_of(g.s, 2, 0), j3 = band_of(g.s, 3, 0), j4 = band_of(g.s, 4, 0);
+    const long long o1 = (long long)st * 1024 + (2 * br) * 128 + 2 * bc;
+    const long long o2 = (long long)st * 256 + br * 64 + bc;
+    // old coefficients in shared memory (TMA): [3][1024] level 1, [3][256] level 2,
+    // [3][64] level 3, [3][16] level 4, [16] approximation
+    constexpr bool OT = ANA256_TMA && OUT == ANA_OUT_VDAMP;
+    C* ob = buf + SP(4095) + 1;
+    ob = reinterpret_cast<C*>((reinterpret_cast<uintptr_t>(ob) + 15) & ~(uintptr_t)15);
+    __shared__ __align__(8) unsigned long long obar;
+    if (OT && tid == 0) {
+        mbar_init(&obar, 1);
+        const unsigned cs = (unsigned)sizeof(C);
+        mbar_expect_tx(&obar, (p.adst ? 4080u : 4096u) * cs);
+        for (int o = 0; o < 3; ++o) {
+            bulk_g2s(ob + o * 1024, coef + g.off[j1 + o] + (long long)st * 1024, 1024u * cs, &obar);
+            bulk_g2s(ob + 3072 + o * 256, coef + g.off[j2 + o] + (long long)st * 256, 256u * cs, &obar);
+            bulk_g2s(ob + 3840 + o * 64, coef + g.off[j3 + o] + (long long)st * 64, 64u * cs, &obar);
+            bulk_g2s(ob + 4032 + o * 16, coef + g.off[j4 + o] + (long long)st * 16, 16u * cs, &obar);
+        }
+        if (!p.adst) bulk_g2s(ob + 4080, coef + g.off[0] + (long long)st * 16, 16u * cs, &obar);
+    }
     if (OUT == ANA_OUT_VDAMP) {
         const double* par = p.par + (long long)bi * g.S * 3;
         for (int i = tid; i < g.S * 3; i += PNT) spar[i] = (R)par[i];
     }
-    const int j1 = band_of(g.s, 1, 0), j2 = band_of(g.s, 2, 0), j3 = band_of(g.s, 3, 0), j4 = band_of(g.s, 4, 0);
-    const long long o1 = (long long)st * 1024 + (2 * br) * 128 + 2 * bc;
-    const long long o2 = (long long)st * 256 + br * 64 + bc;
+    pdl_enter();
     C old1[3][2][2], old2[3];
     {
         C v[16];
@@ -660,7 +684,15 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? ANA256_MINB : 2) analysi
 #pragma unroll
             for (int i = 0; i < 2; ++i) { w1[i][0] = n1[o][i][0]; w1[i][1] = n1[o][i][1]; }
             if (OUT == ANA_OUT_VDAMP) {
-                if (!ANA256_EARLY) {
+                if (OT) {
+                    if (o == 0) mbar_wait(&obar, 0);
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) {
+                        old1[o][i][0] = ob[o * 1024 + (2 * br + i) * 128 + 2 * bc];
+                        old1[o][i][1] = ob[o * 1024 + (2 * br + i) * 128 + 2 * bc + 1];
+                    }
+                    old2[o] = ob[3072 + o * 256 + br * 64 + bc];
+                } else if (!ANA256_EARLY) {
 #pragma unroll
                     for (int i = 0; i < 2; ++i) ld2c<C>(q1 + i * 128, old1[o][i][0], old1[o][i][1]);
                     old2[o] = *q2;
@@ -692,7 +724,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? ANA256_MINB : 2) analysi
 #pragma unroll
         for (int o = 0; o < 3; ++o) {
             C* q = coef + g.off[j3 + o] + o3;
-            if (OUT == ANA_OUT_VDAMP) n3[o] = cadd(ons_j<R, true>(*q, spar, j3 + o), n3[o]);
+            if (OUT == ANA_OUT_VDAMP) n3[o] = cadd(ons_j<R, true>(OT ? ob[3840 + o * 64 + r3 * 32 + c3] : *q, spar, j3 + o), n3[o]);
             *q = n3[o];
         }
     }
@@ -709,14 +741,14 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? ANA256_MINB : 2) analysi
 #pragma unroll
         for (int o = 0; o < 3; ++o) {
             C* q = coef + g.off[j4 + o] + o4;
-            if (OUT == ANA_OUT_VDAMP) n4[o] = cadd(ons_j<R, true>(*q, spar, j4 + o), n4[o]);
+            if (OUT == ANA_OUT_VDAMP) n4[o] = cadd(ons_j<R, true>(OT ? ob[4032 + o * 16 + tid] : *q, spar, j4 + o), n4[o]);
             *q = n4[o];
         }
         if (p.adst) {
             p.adst[(long long)bi * p.adst_bs + o4] = a;
         } else {
             C* q = coef + g.off[0] + o4;
-            if (OUT == ANA_OUT_VDAMP) a = cadd(ons_j<R, true>(*q, spar, 0), a);
+            if (OUT == ANA_OUT_VDAMP) a = cadd(ons_j<R, true>(OT ? ob[4080 + tid] : *q, spar, 0), a);
             *q = a;
         }
     }
