@@ -245,7 +245,9 @@ struct Seq {
 
     // Haar synthesis of coefficients `coef` with params `par`; FFT -> T1 when
     // rowfft, else the image goes to `img`.
-    void synth(const C* coef, const double* par, bool rowfft, C* img, int cls) {
+    // early: coef was written at least two kernels before this synthesis (not by
+    // the immediately preceding kernel), so synth256 may read it before its PDL wait
+    void synth(const C* coef, const double* par, bool rowfft, C* img, int cls, bool early = false) {
         const int P = (int)p->passes.size();
         for (int i = P - 1; i >= 0; --i) {
             const Pass& ps = p->passes[i];
@@ -261,10 +263,13 @@ struct Seq {
             dim3 grid(ps.nstrips, p->B);
             const size_t sm = (size_t)SPN(ps.Wa << ps.k) * sizeof(C);
             Launch L(p, cls, st);
+            a.early = 0;
             if (last && rowfft && f256(ps)) {
+                a.early = early ? 1 : 0;
+                const size_t sme = sm;                             // coefficients land in the pixel buffer
                 auto k = synth256<R>;
-                set_smem(k, sm);
-                launch(k, grid, PNT, sm, st, p->geo, a);
+                set_smem(k, sme);
+                launch(k, grid, PNT, sme, st, p->geo, a);
             } else if (last && rowfft) {
                 auto k = synth_pass<R, SYN_ROWFFT>;
                 const size_t smf = sm + (size_t)p->W * sizeof(C);
@@ -469,7 +474,7 @@ struct Seq {
 
     // one VDAMP iteration from (r, par) -> (r, par)   (src/vdamp.py:99-144)
     void iteration(double* trace, void* snapshot) {
-        synth(r(), p->par, true, nullptr, 0);
+        synth(r(), p->par, true, nullptr, 0, true);        // r: written by K3 two kernels back
         col(COL_VDAMP, (const C*)p->T1, (C*)p->T2, 1);
         analysis(nullptr, true, r(), p->par, true, 2);
         if (snapshot) CK(cudaMemcpyAsync(snapshot, p->r, (size_t)p->B * p->N * sizeof(C), cudaMemcpyDeviceToDevice, st));

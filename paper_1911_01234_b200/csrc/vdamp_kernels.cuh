@@ -94,6 +94,8 @@ struct SynArgs {
     const typename CT<R>::T* tw;     // twiddles, length W (ROWFFT)
     int a, b, k, Wa, logWa;
     long long asrc_bs, dst_bs;
+    int early;                       // synth256: coef was written >= 2 kernels back, so it may be
+                                     // bulk-copied before the PDL wait (not after momentum_update)
 };
 
 // Gather the coarse part of a strip (levels a+1..a+k-1 and the approximation
@@ -497,7 +499,6 @@ __device__ __forceinline__ typename CT<R>::T ons_j(typename CT<R>::T x, const R*
 // of levels 4..1 in registers, (-1)^(n1+n2) / 16 folded in, register row FFT -> T1
 template <typename R>
 __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth256(Geo g, SynArgs<R> p) {
-    pdl_enter();
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* buf = reinterpret_cast<C*>(smem_raw);
@@ -505,29 +506,67 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth256(Geo g, S
     const int br = tid >> 6, bc = tid & 63;
     const C* coef = p.coef + (long long)bi * g.N;
     __shared__ R spar[MAXS * 3];
+    const int j1 = band_of(g.s, 1, 0), j2 = band_of(g.s, 2, 0), j3 = band_of(g.s, 3, 0), j4 = band_of(g.s, 4, 0);
+    // early: the strip's coefficients (levels 1-4 and the approximation, 4096
+    // complex, same layout as analysis256's) are bulk-copied into shared memory
+    // before the PDL wait (into the pixel buffer: they are in registers before
+    // the first pixel is stored); only the parameters come from the previous kernel
+    C* ob = buf;
+    __shared__ __align__(8) unsigned long long obar;
+    const bool early = p.early != 0;
+    if (early && tid == 0) {
+        mbar_init(&obar, 1);
+        const unsigned cs = (unsigned)sizeof(C);
+        mbar_expect_tx(&obar, (p.asrc ? 4080u : 4096u) * cs);
+        for (int o = 0; o < 3; ++o) {
+            bulk_g2s(ob + o * 1024, coef + g.off[j1 + o] + (long long)st * 1024, 1024u * cs, &obar);
+            bulk_g2s(ob + 3072 + o * 256, coef + g.off[j2 + o] + (long long)st * 256, 256u * cs, &obar);
+            bulk_g2s(ob + 3840 + o * 64, coef + g.off[j3 + o] + (long long)st * 64, 64u * cs, &obar);
+            bulk_g2s(ob + 4032 + o * 16, coef + g.off[j4 + o] + (long long)st * 16, 16u * cs, &obar);
+        }
+        if (!p.asrc) bulk_g2s(ob + 4080, coef + g.off[0] + (long long)st * 16, 16u * cs, &obar);
+    }
+    pdl_enter();
     const double* par = p.par ? p.par + (long long)bi * g.S * 3 : nullptr;
     for (int i = tid; i < g.S * 3; i += PNT) spar[i] = par ? (R)par[i] : ((i % 3) == 2 ? R(1) : R(0));
-    const int j1 = band_of(g.s, 1, 0), j2 = band_of(g.s, 2, 0), j3 = band_of(g.s, 3, 0), j4 = band_of(g.s, 4, 0);
-    // loads first: level 1 (2 x 2 per orientation, pairs along the row), 2, 3, 4, approximation
+    // level 1 (2 x 2 per orientation, pairs along the row), 2, 3, 4, approximation
     C d1[3][2][2], d2[3], d3[3], d4[3], a4;
     {
-        const long long o1 = (long long)st * 1024 + (2 * br) * 128 + 2 * bc;
-#pragma unroll
-        for (int o = 0; o < 3; ++o)
-#pragma unroll
-            for (int i = 0; i < 2; ++i) ld2c<C>(coef + g.off[j1 + o] + o1 + i * 128, d1[o][i][0], d1[o][i][1]);
-        const long long o2 = (long long)st * 256 + br * 64 + bc;
-        const long long o3 = (long long)st * 64 + (br >> 1) * 32 + (bc >> 1);
         const long long o4 = (long long)st * 16 + (bc >> 2);
+        if (early) {
+            a4 = p.asrc ? p.asrc[(long long)bi * p.asrc_bs + o4] : mk<C>(R(0), R(0));
+            __syncthreads();                                // obar initialised before anyone waits
+            mbar_wait(&obar, 0);
 #pragma unroll
-        for (int o = 0; o < 3; ++o) {
-            d2[o] = coef[g.off[j2 + o] + o2];
-            d3[o] = coef[g.off[j3 + o] + o3];
-            d4[o] = coef[g.off[j4 + o] + o4];
+            for (int o = 0; o < 3; ++o) {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    d1[o][i][0] = ob[o * 1024 + (2 * br + i) * 128 + 2 * bc];
+                    d1[o][i][1] = ob[o * 1024 + (2 * br + i) * 128 + 2 * bc + 1];
+                }
+                d2[o] = ob[3072 + o * 256 + br * 64 + bc];
+                d3[o] = ob[3840 + o * 64 + (br >> 1) * 32 + (bc >> 1)];
+                d4[o] = ob[4032 + o * 16 + (bc >> 2)];
+            }
+            if (!p.asrc) a4 = ob[4080 + (bc >> 2)];
+        } else {
+            const long long o1 = (long long)st * 1024 + (2 * br) * 128 + 2 * bc;
+#pragma unroll
+            for (int o = 0; o < 3; ++o)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) ld2c<C>(coef + g.off[j1 + o] + o1 + i * 128, d1[o][i][0], d1[o][i][1]);
+            const long long o2 = (long long)st * 256 + br * 64 + bc;
+            const long long o3 = (long long)st * 64 + (br >> 1) * 32 + (bc >> 1);
+#pragma unroll
+            for (int o = 0; o < 3; ++o) {
+                d2[o] = coef[g.off[j2 + o] + o2];
+                d3[o] = coef[g.off[j3 + o] + o3];
+                d4[o] = coef[g.off[j4 + o] + o4];
+            }
+            a4 = p.asrc ? p.asrc[(long long)bi * p.asrc_bs + o4] : coef[g.off[0] + o4];
         }
-        a4 = p.asrc ? p.asrc[(long long)bi * p.asrc_bs + o4] : coef[g.off[0] + o4];
     }
-    __syncthreads();                                        // spar
+    __syncthreads();                                        // spar; every thread holds its coefficients (buf free)
     C px[4][4];
     auto body = [&](auto onsc) {
         constexpr bool ONS = decltype(onsc)::value;
