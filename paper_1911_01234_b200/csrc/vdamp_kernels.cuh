@@ -141,9 +141,7 @@ __device__ __forceinline__ void gather_coarse(const Geo& g, const SynArgs<R>& p,
     }
 }
 
-// F256: W = 256 and 16-row strips (k = 4): the row FFT runs in registers
-// (strip_fft256_fwd) and stores T1 straight from them
-template <typename R, int MODE, bool F256 = false>
+template <typename R, int MODE>
 __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth_pass(Geo g, SynArgs<R> p) {
     pdl_enter();
     typedef typename CT<R>::T C;
@@ -156,7 +154,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth_pass(Geo g,
     const double* par = p.par ? p.par + (long long)bi * g.S * 3 : nullptr;
     C* tws = buf + SP(E - 1) + 1;
     __shared__ R spar[MAXS * 3];
-    if (MODE == SYN_ROWFFT && !F256)
+    if (MODE == SYN_ROWFFT)
         for (int e = tid; e < g.W; e += PNT) tws[e] = p.tw[e];
     for (int i = tid; i < g.S * 3; i += PNT) spar[i] = par ? (R)par[i] : ((i % 3) == 2 ? R(1) : R(0));
 
@@ -258,14 +256,6 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth_pass(Geo g,
     }
 
     C* dst = p.dst + (long long)bi * p.dst_bs + (long long)st * E;
-    if constexpr (MODE == SYN_ROWFFT && F256) {
-        C v[16];
-        strip_fft256_fwd<C>(buf, v, p.tw);
-        C* drow = dst + ((tid >> 4) << 8) + (tid & 15);
-#pragma unroll
-        for (int k2 = 0; k2 < 16; ++k2) drow[16 * k2] = v[k2];
-        return;
-    }
     if (MODE == SYN_ROWFFT) block_fft16<C, false, PNT, PCAP, false, true>(buf, g.logW, k, Wa, 1, tws);
     for (int e = tid; e < E; e += PNT) dst[e] = buf[SP(e)];
 }
@@ -285,9 +275,7 @@ struct AnaArgs {
     long long src_bs, adst_bs;
 };
 
-// F256: W = 256 and 16-row strips: the row IFFT reads T2 straight into
-// registers (strip_ifft256_to_smem)
-template <typename R, int IN, int OUT, bool F256 = false>
+template <typename R, int IN, int OUT>
 __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis_pass(Geo g, AnaArgs<R> p) {
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -303,13 +291,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis_pass(Geo
         const double* par = p.par + (long long)bi * g.S * 3;
         for (int i = tid; i < g.S * 3; i += PNT) spar[i] = (R)par[i];
     }
-    if constexpr (IN == ANA_IN_ROWIFFT && F256) {
-        C v[16];
-        const C* srow = src + ((tid >> 4) << 8) + (tid & 15);
-#pragma unroll
-        for (int k2 = 0; k2 < 16; ++k2) v[k2] = srow[16 * k2];
-        strip_ifft256_to_smem<C>(buf, v, p.tw);
-    } else if (IN == ANA_IN_ROWIFFT) {
+    if (IN == ANA_IN_ROWIFFT) {
         C* tws = buf + SP(E - 1) + 1;
         for (int e = tid; e < g.W; e += PNT) tws[e] = p.tw[e];
         for (int e = tid; e < E; e += PNT) buf[SP(e)] = src[e];
@@ -616,12 +598,6 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth256(Geo g, S
 // K3 for W = 256, k = 4: register row IFFT of T2 into the strip, then per 4x4
 // block the sign c (-1)^(n1+n2) / 16 and Haar analysis levels 1..2 in registers,
 // levels 3..4 through a small shared exchange; VDAMP: r = Onsager(r; par) + Psi u
-#ifndef ANA256_MINB
-#define ANA256_MINB 4
-#endif
-#ifndef ANA256_EARLY
-#define ANA256_EARLY 0
-#endif
 // ANA256_TMA: the strip's previous coefficients (levels 1-4 and the approximation,
 // 4096 complex) are bulk-copied into shared memory before the PDL wait (they
 // were written four kernels back), overlapping the T2 loads and the row IFFT
@@ -629,7 +605,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth256(Geo g, S
 #define ANA256_TMA 1
 #endif
 template <typename R, int OUT>
-__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? ANA256_MINB : 2) analysis256(Geo g, AnaArgs<R> p) {
+__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis256(Geo g, AnaArgs<R> p) {
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* buf = reinterpret_cast<C*>(smem_raw);
@@ -671,14 +647,6 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? ANA256_MINB : 2) analysi
         const C* srow = p.src + (long long)bi * p.src_bs + (long long)st * 4096 + ((tid >> 4) << 8) + (tid & 15);
 #pragma unroll
         for (int k2 = 0; k2 < 16; ++k2) v[k2] = srow[16 * k2];
-        if (ANA256_EARLY && OUT == ANA_OUT_VDAMP) {
-#pragma unroll
-            for (int o = 0; o < 3; ++o) {
-#pragma unroll
-                for (int i = 0; i < 2; ++i) ld2c<C>(coef + g.off[j1 + o] + o1 + i * 128, old1[o][i][0], old1[o][i][1]);
-                old2[o] = coef[g.off[j2 + o] + o2];
-            }
-        }
         strip_ifft256_to_smem<C>(buf, v, p.tw);
     }
     const R sc = (R)g.sign_c / R(16);
@@ -731,7 +699,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? ANA256_MINB : 2) analysi
                         old1[o][i][1] = ob[o * 1024 + (2 * br + i) * 128 + 2 * bc + 1];
                     }
                     old2[o] = ob[3072 + o * 256 + br * 64 + bc];
-                } else if (!ANA256_EARLY) {
+                } else {
 #pragma unroll
                     for (int i = 0; i < 2; ++i) ld2c<C>(q1 + i * 128, old1[o][i][0], old1[o][i][1]);
                     old2[o] = *q2;
@@ -993,11 +961,8 @@ template <typename R>
 __host__ __device__ constexpr int col256_region0(int np) {
     return (4096 * 2 * (int)sizeof(R) > np * (256 + 16) * 8) ? 4096 * 2 * (int)sizeof(R) : np * (256 + 16) * 8;
 }
-#ifndef COL256_MINB
-#define COL256_MINB 3
-#endif
 template <typename R, int MODE>
-__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? COL256_MINB : 2) col_pass256(Geo g, ColArgs<R> p) {
+__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass256(Geo g, ColArgs<R> p) {
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* buf = reinterpret_cast<C*>(smem_raw);              // [16][16][16] transpose tile

@@ -244,3 +244,26 @@ def test_cfg2_fp32_large_subband_path(monkeypatch):
         for r1, r2 in zip(t1.records, t2.records):
             assert np.allclose(r1.thresholds, r2.thresholds, rtol=1e-6)
             assert abs(r1.nmse_db - r2.nmse_db) <= 1e-3
+
+
+def test_256_kernels_match_generic_path(tmp_path):
+    """The W = H = 256 kernels (register FFTs, per-block Haar, TMA staging) against the
+    generic shared-memory kernels (VDAMP_F256=0, read once per process: a subprocess)."""
+    import os, subprocess, sys
+    from paper_1911_01234_b200 import vdamp, workload
+    code = (
+        "import numpy as np, sys\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "from paper_1911_01234_b200 import vdamp, workload\n"
+        "w = workload.make_workload('cfg1', batch=2)\n"
+        "for prec in ('fp64', 'fp32'):\n"
+        "    x, t = vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, 4, 6, ground_truths=w.x0, precision=prec)\n"
+        f"    np.save({str(tmp_path)!r} + '/x_' + prec + '.npy', x)\n"
+    )
+    env = dict(os.environ, VDAMP_F256="0")
+    subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
+    w = workload.make_workload("cfg1", batch=2)
+    for prec, tol in (("fp64", 1e-10), ("fp32", 1e-3)):
+        x, _ = vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, 4, 6, ground_truths=w.x0, precision=prec)
+        xg = np.load(str(tmp_path / f"x_{prec}.npy"))
+        assert rel2(x, xg) <= tol, prec
