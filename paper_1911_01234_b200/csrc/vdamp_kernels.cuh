@@ -1535,6 +1535,138 @@ template <typename R> struct KeyU;
 template <> struct KeyU<float> { typedef unsigned int U; };
 template <> struct KeyU<double> { typedef unsigned long long U; };
 
+// fp32 version with the data-equalised bucket map of counting_sort: a coarse
+// histogram (1024 buckets over the key-bit range) assigns each coarse bucket a
+// run of the GNBF fine buckets proportional to its population, so crowded value
+// ranges spread out (~2 keys per bucket at 65,536 keys) and the in-bucket ranking
+// stays O(1) per key.  Loads are batched GLB deep.  Zeros (fine bucket 0) are all
+// equal and need no ranking.  Returns false if a nonzero bucket exceeds CS_MAXB.
+template <int NT>
+__device__ __noinline__ bool global_counting_sort_eq(float* A, float* B, unsigned* cnt, int n, double* sh) {
+    constexpr int GNBF = 30720, NC = 1024, TILE = 16384, GLB = 8;
+    static_assert(NC % NT == 0 || NT % NC == 0, "coarse buckets per thread");
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    unsigned* ka = reinterpret_cast<unsigned*>(A);
+    unsigned* kb = reinterpret_cast<unsigned*>(B);
+    unsigned* hc = cnt + GNBF;                       // coarse histogram
+    unsigned* tab = hc + NC;                         // coarse bucket -> fine start | width << 16
+    unsigned* tl = cnt + 32768;                      // ranking tile
+    unsigned mn = 0xffffffffu, mx = 0;
+    for (int e0 = tid; e0 < n; e0 += NT * GLB) {
+        unsigned k[GLB];
+#pragma unroll
+        for (int u = 0; u < GLB; ++u) k[u] = e0 + u * NT < n ? __ldcg(ka + e0 + u * NT) : 0u;
+#pragma unroll
+        for (int u = 0; u < GLB; ++u) { if (k[u]) mn = min(mn, k[u]); mx = max(mx, k[u]); }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    unsigned* red = reinterpret_cast<unsigned*>(sh);
+    __syncthreads();
+    if (lane == 0) { red[w] = mn; red[32 + w] = mx; }
+    for (int i = tid; i < GNBF + NC; i += NT) cnt[i] = 0;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned a = red[0], b = red[32];
+        for (int i = 1; i < NT / 32; ++i) { a = min(a, red[i]); b = max(b, red[32 + i]); }
+        red[64] = a; red[65] = b;
+    }
+    __syncthreads();
+    mn = red[64]; mx = red[65];
+    if (mn > mx) mn = mx;                            // all zeros
+    const unsigned dd = mx - mn;
+    int lc = dd < (unsigned)NC ? 0 : (32 - __clz(dd)) - 10;
+    if (((mx >> lc) - (mn >> lc)) >= (unsigned)NC) ++lc;
+    const unsigned cb = mn >> lc;
+    for (int e0 = tid; e0 < n; e0 += NT * GLB) {
+        unsigned k[GLB];
+#pragma unroll
+        for (int u = 0; u < GLB; ++u) k[u] = e0 + u * NT < n ? __ldcg(ka + e0 + u * NT) : 0u;
+#pragma unroll
+        for (int u = 0; u < GLB; ++u) if (k[u]) atomicAdd(&hc[(k[u] >> lc) - cb], 1u);
+    }
+    __syncthreads();
+    {
+        constexpr int CPT = NC / NT > 0 ? NC / NT : 1;
+        unsigned h[CPT], hs = 0;
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) { h[q] = tid * CPT + q < NC ? hc[tid * CPT + q] : 0u; hs += h[q]; }
+        unsigned P = (unsigned)block_excl_scan<NT, false>((double)hs, sh + 66);
+        if (tid == NT - 1) red[66] = P + hs;
+        __syncthreads();
+        const unsigned tot = red[66];
+        const double scl = tot ? (double)(GNBF - 1) / (double)tot : 0.0;
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+            if (tid * CPT + q < NC) {
+                const unsigned fs = __double2uint_rz((double)P * scl);
+                const unsigned fe = __double2uint_rz((double)(P + h[q]) * scl);
+                tab[tid * CPT + q] = fs | ((fe - fs) << 16);
+            }
+            P += h[q];
+        }
+    }
+    __syncthreads();
+    auto bucket = [&](unsigned k) -> unsigned { return cs_fine(k, lc, cb, tab, (unsigned)GNBF - 1u); };
+    for (int e0 = tid; e0 < n; e0 += NT * GLB) {
+        unsigned k[GLB];
+#pragma unroll
+        for (int u = 0; u < GLB; ++u) k[u] = e0 + u * NT < n ? __ldcg(ka + e0 + u * NT) : 0xffffffffu;
+#pragma unroll
+        for (int u = 0; u < GLB; ++u) if (k[u] != 0xffffffffu) atomicAdd(&cnt[bucket(k[u])], 1u);
+    }
+    __syncthreads();
+    {
+        unsigned big = 0;
+        for (int i = 1 + tid; i < GNBF; i += NT) big |= cnt[i] > (unsigned)CS_MAXB;
+        if (__syncthreads_or(big)) return false;
+    }
+    {
+        constexpr int PER = GNBF / NT;
+        static_assert(GNBF % NT == 0, "fine buckets per thread");
+        unsigned tot = 0;
+        for (int i = 0; i < PER; ++i) tot += cnt[tid * PER + i];
+        unsigned run = (unsigned)block_excl_scan<NT, false>((double)tot, sh + 66);
+        for (int i = 0; i < PER; ++i) { const unsigned c = cnt[tid * PER + i]; cnt[tid * PER + i] = run; run += c; }
+    }
+    __syncthreads();
+    for (int e0 = tid; e0 < n; e0 += NT * GLB) {
+        unsigned k[GLB];
+#pragma unroll
+        for (int u = 0; u < GLB; ++u) k[u] = e0 + u * NT < n ? __ldcg(ka + e0 + u * NT) : 0xffffffffu;
+#pragma unroll
+        for (int u = 0; u < GLB; ++u) if (k[u] != 0xffffffffu) kb[atomicAdd(&cnt[bucket(k[u])], 1u)] = k[u];
+    }
+    __syncthreads();
+    // cnt[b] = end of bucket b.  Zeros (bucket 0) are equal: copy.  Then rank
+    // inside buckets tile by tile in shared memory (tiles end on bucket boundaries).
+    const int z = (int)cnt[0];
+    for (int i = tid; i < z; i += NT) ka[i] = 0u;
+    int S0 = z;
+    while (S0 < n) {
+        int E0 = S0 + TILE < n ? S0 + TILE : n;
+        if (E0 < n) {
+            const unsigned bE = bucket(__ldcg(kb + E0));
+            E0 = bE ? (int)cnt[bE - 1] : 0;            // start of the bucket holding position E0
+        }
+        for (int i = S0 + tid; i < E0; i += NT) tl[i - S0] = __ldcg(kb + i);
+        __syncthreads();
+        for (int i = S0 + tid; i < E0; i += NT) {
+            const unsigned x = tl[i - S0];
+            const unsigned b = bucket(x);
+            const int e1 = (int)cnt[b], s0 = b ? (int)cnt[b - 1] : 0;
+            unsigned rank = 0;
+            for (int q = s0; q < e1; ++q) { const unsigned y = tl[q - S0]; rank += (y < x) || (y == x && q < i); }
+            ka[s0 + rank] = x;
+        }
+        __syncthreads();
+        S0 = E0;
+    }
+    return true;
+}
+
 template <typename R, int NT>
 __device__ bool global_counting_sort(R* A, R* B, unsigned* cnt, int n, double* sh) {
     typedef typename KeyU<R>::U U;
@@ -1997,14 +2129,23 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
     } else {
         // whole subband -> global scratch keys, counting sort there (L2-resident)
         R* ka = a.kA + base;
-        for (int e = tid; e < n; e += NT) {
-            const C v = rs[e];
-            ka[e] = cmag(v);
-            if (w0) {
-                const C w = w0[e];
-                const double dx = (double)v.x - (double)w.x, dy = (double)v.y - (double)w.y;
-                err += dx * dx + dy * dy;
-                ref += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
+        constexpr int LB = 8;                                      // loads in flight per thread
+        for (int e0 = tid; e0 < n; e0 += NT * LB) {
+            C v[LB];
+#pragma unroll
+            for (int u = 0; u < LB; ++u) if (e0 + u * NT < n) v[u] = rs[e0 + u * NT];
+#pragma unroll
+            for (int u = 0; u < LB; ++u) {
+                const int e = e0 + u * NT;
+                if (e < n) {
+                    ka[e] = cmag(v[u]);
+                    if (w0) {
+                        const C w = w0[e];
+                        const double dx = (double)v[u].x - (double)w.x, dy = (double)v[u].y - (double)w.y;
+                        err += dx * dx + dy * dy;
+                        ref += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
+                    }
+                }
             }
         }
         __syncthreads();
@@ -2016,8 +2157,12 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
         flush_err();
         sorted = ka;
         if constexpr (NT >= BNT32) {
-            if (!global_counting_sort<R, NT>(ka, a.kB + base, reinterpret_cast<unsigned*>(keys), n, sh))
-                sorted = global_merge_sort<R, NT>(ka, a.kB + base, keys, n, CAPK);
+            bool ok;
+            if constexpr (sizeof(R) == 4)
+                ok = global_counting_sort_eq<NT>(ka, a.kB + base, reinterpret_cast<unsigned*>(keys), n, sh);
+            else
+                ok = global_counting_sort<R, NT>(ka, a.kB + base, reinterpret_cast<unsigned*>(keys), n, sh);
+            if (!ok) sorted = global_merge_sort<R, NT>(ka, a.kB + base, keys, n, CAPK);
         }
         // tile totals (ascending squares, descending inverses)
         for (int t = 0; t < ntl; ++t) {
