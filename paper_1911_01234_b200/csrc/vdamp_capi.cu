@@ -64,6 +64,7 @@ struct Plan {
     double* taupart = nullptr;      // [B][ntiles][S]
     double* prow = nullptr;         // [2s][H]
     double* pcol = nullptr;         // [2s][W]
+    void* prs256 = nullptr;         // H = 256: row profiles [256][npp] in the working precision
     double* nvar = nullptr;         // [B]
     long long* offs = nullptr;      // [B+1] measurement offsets
     void* twH = nullptr;
@@ -348,6 +349,7 @@ struct Seq {
         a.prow = p->prow; a.pcol = p->pcol; a.taupart = p->taupart;
         a.tw = (const C*)p->twH; a.cw = p->cw; a.logcw = p->logcw; a.ntiles = p->ntiles;
         a.x0r = (const C*)p->x0r; a.nmsepart = p->nmpart;
+        a.prs256 = (const R*)p->prs256;
         dim3 grid(p->ntiles, p->B);
         Launch L(p, cls, st);
         if (c256() && (mode == COL_VDAMP || mode == COL_FINAL || mode == COL_NMSE)) {
@@ -626,7 +628,7 @@ void dispatch(Plan* p, void* stream, F&& f) {
 void free_plan(Plan* p) {
     if (!p) return;
     cudaSetDevice(p->dev);
-    void* bufs[] = {p->what, p->btau, p->berr, p->x0r, p->nmconst, p->nmpart, p->r, p->T1, p->T2, p->yg, p->pinv, p->par, p->parf, p->taupart, p->prow, p->pcol,
+    void* bufs[] = {p->what, p->btau, p->berr, p->x0r, p->nmconst, p->nmpart, p->r, p->T1, p->T2, p->yg, p->pinv, p->par, p->parf, p->taupart, p->prow, p->pcol, p->prs256,
                     p->nvar, p->offs, p->twH, p->twW, p->kA, p->kB, p->bhist, p->btick, p->bbest, p->baux, p->berrp, p->x0, p->w0, p->xtmp, p->trtmp};
     for (void* b : bufs) if (b) cudaFree(b);
     for (void* b : p->scratch) if (b) cudaFree(b);
@@ -807,6 +809,12 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         }
         make_profiles<<<dim3((height + 127) / 128, 2 * scales), 128>>>(p->prow, height, scales);
         make_profiles<<<dim3((width + 127) / 128, 2 * scales), 128>>>(p->pcol, width, scales);
+        if (height == 256) {
+            const int np = 2 * scales, npp = (np + 3) & ~3;
+            p->prs256 = dalloc(p, (size_t)256 * npp * rs);
+            if (precision == VDAMP_FP32) arrange_prs256<float><<<(256 * npp + 255) / 256, 256>>>((float*)p->prs256, p->prow, np, npp);
+            else arrange_prs256<double><<<(256 * npp + 255) / 256, 256>>>((double*)p->prs256, p->prow, np, npp);
+        }
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());
         *out = reinterpret_cast<vdamp_plan_t>(p);

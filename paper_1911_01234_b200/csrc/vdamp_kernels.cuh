@@ -780,6 +780,7 @@ struct ColArgs {
     int cw, logcw, ntiles;
     const typename CT<R>::T* x0r;    // COL_NMSE: raw unitary FFT2 of s_in * x0
     double* nmsepart;                // COL_NMSE: [B][ntiles] error partials
+    const R* prs256;                 // col_pass256: row profiles as [256][npp] (npp = 2s rounded up to 4)
 };
 
 __device__ __forceinline__ void band_profiles(int s, int j, int& prow, int& pcol) {
@@ -986,13 +987,16 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass256(Geo g
         if (sizeof(R) == 8) prefetch_l2(p.yg + ri + 8);
         prefetch_l2(p.pinv + ri);
     }
-    if (MODE == COL_VDAMP) {
-        // constant profiles, staged before the wait as well
-        for (int i = tid; i < 256 * npp; i += PNT) {
-            const int k = i / npp, q = i - k * npp;
-            prs[i] = (q < np) ? (R)p.prow[q * 256 + k] : R(0);
-        }
-        for (int i = tid; i < np * 16; i += PNT) pcs[i] = p.pcol[(long long)(i >> 4) * W + c0 + (i & 15)];
+    __shared__ __align__(8) unsigned long long pbar;
+    if (MODE == COL_VDAMP && tid == 0) {
+        // constant profiles, bulk-copied before the wait as well: the row
+        // profiles pre-arranged [256][npp] at plan creation, the tile's 16
+        // columns of each column profile
+        mbar_init(&pbar, 1);
+        const unsigned rb = 256u * (unsigned)npp * (unsigned)sizeof(R);
+        mbar_expect_tx(&pbar, rb + (unsigned)np * 128u);
+        bulk_g2s(prs, p.prs256, rb, &pbar);
+        for (int q = 0; q < np; ++q) bulk_g2s(pcs + q * 16, p.pcol + (long long)q * W + c0, 128u, &pbar);
     }
     pdl_enter();
     C v[16];
@@ -1071,6 +1075,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass256(Geo g
     // (float4 loads), then a fixed-order combination over the 16 threads of
     // each column and the column profiles
     __syncthreads();                                       // inverse transpose reads done
+    mbar_wait(&pbar, 0);                                   // profiles landed
     double* part = reinterpret_cast<double*>(buf);         // [np][PNT] thread partials
     double* psum = part + np * PNT;                        // [np][16] column partials
     for (int q0 = 0; q0 < np; q0 += 4) {
@@ -2618,6 +2623,15 @@ __global__ void make_twiddles(typename CT<R>::T* tw, int L) {
 }
 
 // |fft1c(atom)|^2 of the 1D Haar atom, profile p = 2*(level-1) + high (src/vdamp.py:41-51, separable)
+// col_pass256's row-profile table: [256][npp], profile q of row k at k * npp + q
+template <typename R>
+__global__ void arrange_prs256(R* prs, const double* prow, int np, int npp) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 256 * npp) return;
+    const int k = i / npp, q = i - k * npp;
+    prs[i] = (q < np) ? (R)prow[q * 256 + k] : R(0);
+}
+
 __global__ void make_profiles(double* prof, int L, int s) {
     const int pidx = blockIdx.y;
     const int level = pidx / 2 + 1, high = pidx & 1;
