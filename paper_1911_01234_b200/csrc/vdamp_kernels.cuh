@@ -2387,8 +2387,6 @@ __device__ __forceinline__ void big_prefix(const unsigned* hg, unsigned* cbs, do
     blast = (int)su[1] - 1;
 }
 
-template <typename R, int NT> __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R* keys,
-                                                          SelShared<NT>& S_);
 
 __global__ void __launch_bounds__(1024, 1) big_range(Geo g, SelArgs<float> a, BigArgs b) {
     pdl_enter();
