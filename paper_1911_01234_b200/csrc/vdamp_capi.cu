@@ -243,6 +243,7 @@ struct Seq {
     }
     bool f256(const Pass& ps) const { return f256_on() && p->W == 256 && ps.Wa == 256 && ps.k == 4; }
     bool c256() const { return f256_on() && p->H == 256 && p->cw == 16; }
+    bool c512() const { return f256_on() && p->H == 512 && p->cw == 8; }
 
     // Haar synthesis of coefficients `coef` with params `par`; FFT -> T1 when
     // rowfft, else the image goes to `img`.
@@ -352,6 +353,16 @@ struct Seq {
         a.prs256 = (const R*)p->prs256;
         dim3 grid(p->ntiles, p->B);
         Launch L(p, cls, st);
+        if (c512() && (mode == COL_VDAMP || mode == COL_FINAL || mode == COL_NMSE)) {
+            const int np = 2 * p->s, npp = (np + 3) & ~3;
+            const size_t sm = (size_t)col512_region0<R>(np) + (size_t)512 * npp * sizeof(R) + (size_t)np * 8 * sizeof(double);
+            switch (mode) {
+                case COL_VDAMP: { auto k = col_pass512<R, COL_VDAMP>; set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
+                case COL_NMSE:  { auto k = col_pass512<R, COL_NMSE>;  set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
+                default:        { auto k = col_pass512<R, COL_FINAL>; set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
+            }
+            return;
+        }
         if (c256() && (mode == COL_VDAMP || mode == COL_FINAL || mode == COL_NMSE)) {
             const int np = 2 * p->s, npp = (np + 3) & ~3;
             const size_t sm = (size_t)col256_region0<R>(np) + (size_t)256 * npp * sizeof(R) + (size_t)np * 16 * sizeof(double);
@@ -809,11 +820,11 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         }
         make_profiles<<<dim3((height + 127) / 128, 2 * scales), 128>>>(p->prow, height, scales);
         make_profiles<<<dim3((width + 127) / 128, 2 * scales), 128>>>(p->pcol, width, scales);
-        if (height == 256) {
+        if (height == 256 || height == 512) {
             const int np = 2 * scales, npp = (np + 3) & ~3;
-            p->prs256 = dalloc(p, (size_t)256 * npp * rs);
-            if (precision == VDAMP_FP32) arrange_prs256<float><<<(256 * npp + 255) / 256, 256>>>((float*)p->prs256, p->prow, np, npp);
-            else arrange_prs256<double><<<(256 * npp + 255) / 256, 256>>>((double*)p->prs256, p->prow, np, npp);
+            p->prs256 = dalloc(p, (size_t)height * npp * rs);
+            if (precision == VDAMP_FP32) arrange_prs256<float><<<(height * npp + 255) / 256, 256>>>((float*)p->prs256, p->prow, np, npp, height);
+            else arrange_prs256<double><<<(height * npp + 255) / 256, 256>>>((double*)p->prs256, p->prow, np, npp, height);
         }
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());

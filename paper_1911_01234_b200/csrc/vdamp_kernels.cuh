@@ -780,7 +780,7 @@ struct ColArgs {
     int cw, logcw, ntiles;
     const typename CT<R>::T* x0r;    // COL_NMSE: raw unitary FFT2 of s_in * x0
     double* nmsepart;                // COL_NMSE: [B][ntiles] error partials
-    const R* prs256;                 // col_pass256: row profiles as [256][npp] (npp = 2s rounded up to 4)
+    const R* prs256;                 // col_pass256/512: row profiles as [H][npp] (npp = 2s rounded up to 4)
 };
 
 __device__ __forceinline__ void band_profiles(int s, int j, int& prow, int& pcol) {
@@ -959,6 +959,10 @@ template <> __device__ __forceinline__ void ld4<double>(const double* q, double&
 // bytes of col_pass256's first shared region: the transpose tile, later the
 // tau partials [np][256] and column sums [np][16] (doubles)
 template <typename R>
+__host__ __device__ constexpr int col512_region0(int np) {
+    return (4096 * 2 * (int)sizeof(R) > np * (256 + 8) * 8) ? 4096 * 2 * (int)sizeof(R) : np * (256 + 8) * 8;
+}
+template <typename R>
 __host__ __device__ constexpr int col256_region0(int np) {
     return (4096 * 2 * (int)sizeof(R) > np * (256 + 16) * 8) ? 4096 * 2 * (int)sizeof(R) : np * (256 + 16) * 8;
 }
@@ -1104,6 +1108,183 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass256(Geo g
         band_profiles(g.s, j, pr_, pc_);
         double sacc = 0.0;
         for (int cc = 0; cc < 16; ++cc) sacc += pcs[pc_ * 16 + cc] * psum[pr_ * 16 + cc];
+        p.taupart[((long long)bi * p.ntiles + tile) * g.S + j] = sacc;
+    }
+}
+
+// K2 for H = 512 (8-column tiles): the same computation as col_pass with both
+// 512-point column FFTs in registers, 512 = 16 x 32 with the 32-point stage
+// split radix-2 across a lane pair.  Thread (c = tid & 7, t = tid >> 3):
+//   A: v[n1] = x[32 n1 + t]; DFT16 over n1; w512^(t k1); transpose
+//   B: thread t = 2 k1 + b takes y_k1[2 a + b], a = 0..15; DFT16 over a; w32^(b k');
+//      radix-2 with its partner (lane ^ 8) -> X[k1 + 16 k' + 256 b], k' = 0..15
+// The inverse runs the same steps backwards with conjugate twiddles.
+template <typename C, bool INV>
+__device__ __forceinline__ void pow_twiddles512(C (&v)[16], int e, const C* __restrict__ tw) {
+    // v[m] *= w512^(+-e m), m = 1..15 (e <= 31)
+    C t1 = __ldg(tw + e), t2 = __ldg(tw + 2 * e), t4 = __ldg(tw + 4 * e), t8 = __ldg(tw + 8 * e);
+    if (INV) { t1 = cconj(t1); t2 = cconj(t2); t4 = cconj(t4); t8 = cconj(t8); }
+    pow_twiddles<C, 16>(v, t1, t2, t4, t8);
+}
+
+template <typename R, int MODE>
+__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass512(Geo g, ColArgs<R> p) {
+    typedef typename CT<R>::T C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* buf = reinterpret_cast<C*>(smem_raw);              // [16 k1][32 t][8 c] transpose tile
+    const int W = g.W;
+    const int tile = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
+    const int c = tid & 7, t = tid >> 3;
+    const int k1 = t >> 1, b = t & 1;
+    const int c0 = tile << 3;
+    const long long ib = (long long)bi * g.N;
+    const int np = 2 * g.s, npp = (np + 3) & ~3;
+    const int A = col512_region0<R>(np);
+    R* prs = reinterpret_cast<R*>(smem_raw + A);          // [512][npp]
+    double* pcs = reinterpret_cast<double*>(smem_raw + A + 512 * npp * (int)sizeof(R));   // [np][8]
+    // frequency rows this thread holds after the forward FFT: k1 + 16 k' + 256 b
+    const long long fbase = ib + (long long)(k1 + 256 * b) * W + c0 + c;
+    if (MODE != COL_NMSE) {
+        const long long r0 = ib + (long long)(2 * tid) * W + c0;         // 2 rows per thread
+        prefetch_l2(p.yg + r0); prefetch_l2(p.yg + r0 + W);
+        prefetch_l2(p.pinv + r0); prefetch_l2(p.pinv + r0 + W);
+    }
+    __shared__ __align__(8) unsigned long long pbar;
+    if (MODE == COL_VDAMP && tid == 0) {
+        mbar_init(&pbar, 1);
+        const unsigned rb = 512u * (unsigned)npp * (unsigned)sizeof(R);
+        mbar_expect_tx(&pbar, rb + (unsigned)np * 64u);
+        for (unsigned o = 0; o < rb; o += 32768u) bulk_g2s(reinterpret_cast<char*>(prs) + o,
+                                                           reinterpret_cast<const char*>(p.prs256) + o,
+                                                           rb - o < 32768u ? rb - o : 32768u, &pbar);
+        for (int q = 0; q < np; ++q) bulk_g2s(pcs + q * 8, p.pcol + (long long)q * W + c0, 64u, &pbar);
+    }
+    pdl_enter();
+    C v[16];
+    {
+        const C* src = p.src + ib + (long long)t * W + c0 + c;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = src[(long long)(32 * j) * W];
+    }
+    // A
+    dft_r<C, false, 16>(v);
+    pow_twiddles512<C, false>(v, t, p.tw);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) buf[(m * 32 + t) * 8 + c] = v[m];
+    __syncthreads();
+    // B
+#pragma unroll
+    for (int a = 0; a < 16; ++a) v[a] = buf[(k1 * 32 + 2 * a + b) * 8 + c];
+    dft_r<C, false, 16>(v);
+    if (b) pow_twiddles512<C, false>(v, 16, p.tw);         // w32^k' = w512^(16 k')
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        const C o = mk<C>(__shfl_xor_sync(0xffffffffu, v[m].x, 8), __shfl_xor_sync(0xffffffffu, v[m].y, 8));
+        v[m] = b ? csub(o, v[m]) : cadd(v[m], o);          // Z0 + w Z1 | Z0 - w Z1
+    }
+    const R sc = R(1) / sqrt(R(512));
+    if (MODE == COL_NMSE) {
+        double e2 = 0.0;
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const long long gi = fbase + (long long)(16 * m) * W;
+            if (p.pinv[gi] == R(0)) {
+                const C df = csub(cscale(v[m], sc), p.x0r[gi]);
+                e2 += (double)df.x * (double)df.x + (double)df.y * (double)df.y;
+            }
+        }
+        __syncthreads();
+        e2 = block_sum<PNT>(e2, reinterpret_cast<double*>(buf));
+        if (tid == 0) p.nmsepart[(long long)bi * p.ntiles + tile] = e2;
+        return;
+    }
+    const R cs = (R)g.sign_c;
+    R wreg[16];
+    {
+        const double nv = (MODE == COL_VDAMP) ? p.noise_var[bi] : 0.0;
+        R pvs[16];
+        C ys[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const long long gi = fbase + (long long)(16 * m) * W;
+            pvs[m] = p.pinv[gi];
+            ys[m] = p.yg[gi];
+        }
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const C X = cscale(v[m], sc * cs);
+            const R pv = pvs[m];
+            R wk = R(0);
+            if (MODE == COL_VDAMP) {
+                if (pv != R(0)) {
+                    const C zc = csub(ys[m], X);                   // (-1)^(k1+k2) z  (src/vdamp.py:112)
+                    v[m] = cscale(zc, pv);                         // P^-1 z           (src/vdamp.py:113)
+                    const double pd = (double)pv;
+                    const double z2 = (double)zc.x * (double)zc.x + (double)zc.y * (double)zc.y;
+                    wk = (R)(pd * ((pd - 1.0) * z2 + nv));         // tau weight (src/vdamp.py:74-75)
+                } else {
+                    v[m] = mk<C>(R(0), R(0));
+                }
+            } else {  // COL_FINAL
+                v[m] = (pv != R(0)) ? ys[m] : X;
+            }
+            wreg[m] = wk;
+        }
+    }
+    // B^-1: radix-2 with the partner, conjugate w32, inverse DFT16 -> y_k1[2 a + b]
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        const C o = mk<C>(__shfl_xor_sync(0xffffffffu, v[m].x, 8), __shfl_xor_sync(0xffffffffu, v[m].y, 8));
+        v[m] = b ? csub(o, v[m]) : cadd(v[m], o);          // U0 + U1 | U0 - U1
+    }
+    if (b) pow_twiddles512<C, true>(v, 16, p.tw);
+    dft_r<C, true, 16>(v);
+    __syncthreads();                                       // forward transpose reads done
+#pragma unroll
+    for (int a = 0; a < 16; ++a) buf[(k1 * 32 + 2 * a + b) * 8 + c] = v[a];
+    __syncthreads();
+    // A^-1
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = buf[(m * 32 + t) * 8 + c];
+    pow_twiddles512<C, true>(v, t, p.tw);
+    dft_r<C, true, 16>(v);                                 // v[n1] = x[32 n1 + t]
+    {
+        C* dst = p.dst + ib + (long long)t * W + c0 + c;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) dst[(long long)(32 * j) * W] = cscale(v[j], sc);
+    }
+    if (MODE != COL_VDAMP) return;
+    // tau partials: rows k1 + 16 m + 256 b of column c
+    __syncthreads();
+    mbar_wait(&pbar, 0);
+    double* part = reinterpret_cast<double*>(buf);         // [np][PNT]
+    double* psum = part + np * PNT;                        // [np][8]
+    for (int q0 = 0; q0 < np; q0 += 4) {
+        R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            R b0, b1, b2, b3;
+            ld4<R>(prs + (k1 + 16 * m + 256 * b) * npp + q0, b0, b1, b2, b3);
+            const R wk = wreg[m];
+            a0 += b0 * wk; a1 += b1 * wk; a2 += b2 * wk; a3 += b3 * wk;
+        }
+        part[q0 * PNT + tid] = (double)a0;
+        part[(q0 + 1) * PNT + tid] = (double)a1;
+        if (q0 + 2 < np) { part[(q0 + 2) * PNT + tid] = (double)a2; part[(q0 + 3) * PNT + tid] = (double)a3; }
+    }
+    __syncthreads();
+    for (int it = tid; it < np * 8; it += PNT) {
+        const int q = it >> 3, cc = it & 7;
+        double sacc = 0.0;
+        for (int tt = cc; tt < PNT; tt += 8) sacc += part[q * PNT + tt];
+        psum[q * 8 + cc] = sacc;
+    }
+    __syncthreads();
+    for (int j = tid; j < g.S; j += PNT) {
+        int pr_, pc_;
+        band_profiles(g.s, j, pr_, pc_);
+        double sacc = 0.0;
+        for (int cc = 0; cc < 8; ++cc) sacc += pcs[pc_ * 8 + cc] * psum[pr_ * 8 + cc];
         p.taupart[((long long)bi * p.ntiles + tile) * g.S + j] = sacc;
     }
 }
@@ -2623,11 +2804,11 @@ __global__ void make_twiddles(typename CT<R>::T* tw, int L) {
 // |fft1c(atom)|^2 of the 1D Haar atom, profile p = 2*(level-1) + high (src/vdamp.py:41-51, separable)
 // col_pass256's row-profile table: [256][npp], profile q of row k at k * npp + q
 template <typename R>
-__global__ void arrange_prs256(R* prs, const double* prow, int np, int npp) {
+__global__ void arrange_prs256(R* prs, const double* prow, int np, int npp, int H) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 256 * npp) return;
+    if (i >= H * npp) return;
     const int k = i / npp, q = i - k * npp;
-    prs[i] = (q < np) ? (R)prow[q * 256 + k] : R(0);
+    prs[i] = (q < np) ? (R)prow[q * H + k] : R(0);
 }
 
 __global__ void make_profiles(double* prof, int L, int s) {

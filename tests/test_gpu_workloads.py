@@ -247,8 +247,9 @@ def test_cfg2_fp32_large_subband_path(monkeypatch):
 
 
 def test_256_kernels_match_generic_path(tmp_path):
-    """The W = H = 256 kernels (register FFTs, per-block Haar, TMA staging) against the
-    generic shared-memory kernels (VDAMP_F256=0, read once per process: a subprocess)."""
+    """The W = H = 256 kernels (register FFTs, per-block Haar, TMA staging) and the H = 512
+    column kernel against the generic shared-memory kernels (VDAMP_F256=0, read once per
+    process: a subprocess)."""
     import os, subprocess, sys
     from paper_1911_01234_b200 import vdamp, workload
     code = (
@@ -259,6 +260,9 @@ def test_256_kernels_match_generic_path(tmp_path):
         "for prec in ('fp64', 'fp32'):\n"
         "    x, t = vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, 4, 6, ground_truths=w.x0, precision=prec)\n"
         f"    np.save({str(tmp_path)!r} + '/x_' + prec + '.npy', x)\n"
+        "w = workload.make_workload('cfg2', batch=1)\n"
+        "x, t = vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, 5, 4, ground_truths=w.x0, precision='fp64')\n"
+        f"np.save({str(tmp_path)!r} + '/x_512.npy', x)\n"
     )
     env = dict(os.environ, VDAMP_F256="0")
     subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
@@ -267,3 +271,6 @@ def test_256_kernels_match_generic_path(tmp_path):
         x, _ = vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, 4, 6, ground_truths=w.x0, precision=prec)
         xg = np.load(str(tmp_path / f"x_{prec}.npy"))
         assert rel2(x, xg) <= tol, prec
+    w = workload.make_workload("cfg2", batch=1)             # 512-point column kernel
+    x, _ = vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, 5, 4, ground_truths=w.x0, precision="fp64")
+    assert rel2(x, np.load(str(tmp_path / "x_512.npy"))) <= 1e-10
