@@ -1128,7 +1128,7 @@ __device__ __forceinline__ void pow_twiddles512(C (&v)[16], int e, const C* __re
 }
 
 template <typename R, int MODE>
-__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass512(Geo g, ColArgs<R> p) {
+__global__ void __launch_bounds__(PNT, 2) col_pass512(Geo g, ColArgs<R> p) {   // 2 CTAs/SM: spill-free
     typedef typename CT<R>::T C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* buf = reinterpret_cast<C*>(smem_raw);              // [16 k1][32 t][8 c] transpose tile
