@@ -243,6 +243,7 @@ struct Seq {
     }
     bool f256(const Pass& ps) const { return f256_on() && p->W == 256 && ps.Wa == 256 && ps.k == 4; }
     bool c256() const { return f256_on() && p->H == 256 && p->cw == 16; }
+    bool f512(const Pass& ps) const { return f256_on() && p->W == 512 && ps.Wa == 512 && ps.k == 3; }
     bool c512() const { return f256_on() && p->H == 512 && p->cw == 8; }
 
     // Haar synthesis of coefficients `coef` with params `par`; FFT -> T1 when
@@ -272,6 +273,11 @@ struct Seq {
                 auto k = synth256<R>;
                 set_smem(k, sme);
                 launch(k, grid, PNT, sme, st, p->geo, a);
+            } else if (last && rowfft && f512(ps)) {
+                a.early = early ? 1 : 0;
+                auto k = synth512<R>;
+                set_smem(k, sm);
+                launch(k, grid, PNT, sm, st, p->geo, a);
             } else if (last && rowfft) {
                 auto k = synth_pass<R, SYN_ROWFFT>;
                 const size_t smf = sm + (size_t)p->W * sizeof(C);
@@ -310,6 +316,15 @@ struct Seq {
                     launch(k, grid, PNT, sm, st, p->geo, a);
                 } else {
                     auto k = analysis256<R, ANA_OUT_COEF>; set_smem(k, sm);
+                    launch(k, grid, PNT, sm, st, p->geo, a);
+                }
+            } else if (first && rowifft && f512(ps)) {
+                if (vdamp_mode) {
+                    sm += 4096 * sizeof(C) + 16;                   // old-coefficient landing zone
+                    auto k = analysis512<R, ANA_OUT_VDAMP>; set_smem(k, sm);
+                    launch(k, grid, PNT, sm, st, p->geo, a);
+                } else {
+                    auto k = analysis512<R, ANA_OUT_COEF>; set_smem(k, sm);
                     launch(k, grid, PNT, sm, st, p->geo, a);
                 }
             } else if (first && rowifft) {

@@ -281,6 +281,14 @@ __device__ __forceinline__ void fft256_stage_a(C (&v)[16], int d, const C* __res
     pow_twiddles<C, 16>(v, t1, t2, t4, t8);
 }
 
+template <typename C, bool INV>
+__device__ __forceinline__ void pow_twiddles512(C (&v)[16], int e, const C* __restrict__ tw) {
+    // v[m] *= w512^(+-e m), m = 1..15 (e <= 31)
+    C t1 = __ldg(tw + e), t2 = __ldg(tw + 2 * e), t4 = __ldg(tw + 4 * e), t8 = __ldg(tw + 8 * e);
+    if (INV) { t1 = cconj(t1); t2 = cconj(t2); t4 = cconj(t4); t8 = cconj(t8); }
+    pow_twiddles<C, 16>(v, t1, t2, t4, t8);
+}
+
 // Row FFTs of a 16 x 256 strip held in the SP-padded shared buffer (row r at
 // SP(256 r) = 272 r; element e of a row at 17 (e >> 4) + (e & 15)).  Thread
 // (r = tid >> 4, d = tid & 15).  Forward: buffer rows -> v[k2] = X_r[d + 16 k2].

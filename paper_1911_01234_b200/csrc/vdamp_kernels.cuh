@@ -761,6 +761,293 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis256(Geo g
     }
 }
 
+// ---------------------------------------------------- K1 / K3, W = 512 ----
+// 8-row strips of a 512-wide image (first pass, levels 1-3): thread (br = tid >> 7,
+// bc = tid & 127) owns the 4x4 pixel block at strip rows 4 br.., columns 4 bc..;
+// the level-3 coefficient of its 8x8 block is shared by 2 x 2 threads.  Row
+// FFTs: 512 = 16 x 32, thread (r = tid >> 5, t = tid & 31) of each row, the
+// 32-point stage split radix-2 across lane pairs (t = 2 k1 + b).  Strip row r at
+// SP(544 r) = 544 r (a 512-wide row is 544 padded elements).
+// Coefficient chunks of a strip (TMA landing zone layout, 4096 complex):
+// [3][1024] level 1 (4 rows x 256), [3][256] level 2 (2 x 128), [3][64] level 3,
+// [64] approximation (subband 0 when s == 3).
+
+// forward row FFTs of the 8 x 512 strip in buf -> v[k'] = X_r[k1 + 16 k' + 256 b]
+template <typename C>
+__device__ __forceinline__ void strip_fft512_fwd(C* buf, C (&v)[16], const C* __restrict__ tw) {
+    const int r = threadIdx.x >> 5, t = threadIdx.x & 31, k1 = t >> 1, b = t & 1;
+    C* row = buf + 544 * r;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = row[SP(32 * j + t)];
+    dft_r<C, false, 16>(v);
+    pow_twiddles512<C, false>(v, t, tw);
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; ++m) row[SP(32 * m + t)] = v[m];
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 16; ++a) v[a] = row[SP(32 * k1 + 2 * a + b)];
+    dft_r<C, false, 16>(v);
+    if (b) pow_twiddles512<C, false>(v, 16, tw);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        const C o = mk<C>(__shfl_xor_sync(0xffffffffu, v[m].x, 1), __shfl_xor_sync(0xffffffffu, v[m].y, 1));
+        v[m] = b ? csub(o, v[m]) : cadd(v[m], o);
+    }
+}
+
+// inverse: v[k'] = X_r[k1 + 16 k' + 256 b] -> natural-order rows in buf (unnormalised)
+template <typename C>
+__device__ __forceinline__ void strip_ifft512_to_smem(C* buf, C (&v)[16], const C* __restrict__ tw) {
+    const int r = threadIdx.x >> 5, t = threadIdx.x & 31, k1 = t >> 1, b = t & 1;
+    C* row = buf + 544 * r;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        const C o = mk<C>(__shfl_xor_sync(0xffffffffu, v[m].x, 1), __shfl_xor_sync(0xffffffffu, v[m].y, 1));
+        v[m] = b ? csub(o, v[m]) : cadd(v[m], o);
+    }
+    if (b) pow_twiddles512<C, true>(v, 16, tw);
+    dft_r<C, true, 16>(v);
+#pragma unroll
+    for (int a = 0; a < 16; ++a) row[SP(32 * k1 + 2 * a + b)] = v[a];
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = row[SP(32 * m + t)];
+    pow_twiddles512<C, true>(v, t, tw);
+    dft_r<C, true, 16>(v);
+    __syncthreads();
+#pragma unroll
+    for (int n = 0; n < 16; ++n) row[SP(32 * n + t)] = v[n];
+    __syncthreads();
+}
+
+// K1 for W = 512, k = 3
+template <typename R>
+__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) synth512(Geo g, SynArgs<R> p) {
+    typedef typename CT<R>::T C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* buf = reinterpret_cast<C*>(smem_raw);
+    const int st = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
+    const int br = tid >> 7, bc = tid & 127;
+    const C* coef = p.coef + (long long)bi * g.N;
+    __shared__ R spar[MAXS * 3];
+    const int j1 = band_of(g.s, 1, 0), j2 = band_of(g.s, 2, 0), j3 = band_of(g.s, 3, 0);
+    C* ob = buf;                                            // coefficient landing zone (early)
+    __shared__ __align__(8) unsigned long long obar;
+    const bool early = p.early != 0;
+    if (early && tid == 0) {
+        mbar_init(&obar, 1);
+        const unsigned cs = (unsigned)sizeof(C);
+        mbar_expect_tx(&obar, (p.asrc ? 4032u : 4096u) * cs);
+        for (int o = 0; o < 3; ++o) {
+            bulk_g2s(ob + o * 1024, coef + g.off[j1 + o] + (long long)st * 1024, 1024u * cs, &obar);
+            bulk_g2s(ob + 3072 + o * 256, coef + g.off[j2 + o] + (long long)st * 256, 256u * cs, &obar);
+            bulk_g2s(ob + 3840 + o * 64, coef + g.off[j3 + o] + (long long)st * 64, 64u * cs, &obar);
+        }
+        if (!p.asrc) bulk_g2s(ob + 4032, coef + g.off[0] + (long long)st * 64, 64u * cs, &obar);
+    }
+    pdl_enter();
+    const double* par = p.par ? p.par + (long long)bi * g.S * 3 : nullptr;
+    for (int i = tid; i < g.S * 3; i += PNT) spar[i] = par ? (R)par[i] : ((i % 3) == 2 ? R(1) : R(0));
+    C d1[3][2][2], d2[3], d3[3], a3;
+    {
+        const long long o3 = (long long)st * 64 + (bc >> 1);
+        if (early) {
+            a3 = p.asrc ? p.asrc[(long long)bi * p.asrc_bs + o3] : mk<C>(R(0), R(0));
+            __syncthreads();
+            mbar_wait(&obar, 0);
+#pragma unroll
+            for (int o = 0; o < 3; ++o) {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    d1[o][i][0] = ob[o * 1024 + (2 * br + i) * 256 + 2 * bc];
+                    d1[o][i][1] = ob[o * 1024 + (2 * br + i) * 256 + 2 * bc + 1];
+                }
+                d2[o] = ob[3072 + o * 256 + br * 128 + bc];
+                d3[o] = ob[3840 + o * 64 + (bc >> 1)];
+            }
+            if (!p.asrc) a3 = ob[4032 + (bc >> 1)];
+        } else {
+            const long long o1 = (long long)st * 1024 + (2 * br) * 256 + 2 * bc;
+#pragma unroll
+            for (int o = 0; o < 3; ++o)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) ld2c<C>(coef + g.off[j1 + o] + o1 + i * 256, d1[o][i][0], d1[o][i][1]);
+            const long long o2 = (long long)st * 256 + br * 128 + bc;
+#pragma unroll
+            for (int o = 0; o < 3; ++o) {
+                d2[o] = coef[g.off[j2 + o] + o2];
+                d3[o] = coef[g.off[j3 + o] + o3];
+            }
+            a3 = p.asrc ? p.asrc[(long long)bi * p.asrc_bs + o3] : coef[g.off[0] + o3];
+        }
+    }
+    __syncthreads();                                        // spar; every thread holds its coefficients (buf free)
+    C px[4][4];
+    auto body = [&](auto onsc) {
+        constexpr bool ONS = decltype(onsc)::value;
+        if (!p.asrc) a3 = ons_j<R, ONS>(a3, spar, 0);
+        const C a2 = haar_syn_q<R, C>(a3, ons_j<R, ONS>(d3[0], spar, j3), ons_j<R, ONS>(d3[1], spar, j3 + 1),
+                                      ons_j<R, ONS>(d3[2], spar, j3 + 2), br & 1, bc & 1);
+        const C h2 = ons_j<R, ONS>(d2[0], spar, j2), v2 = ons_j<R, ONS>(d2[1], spar, j2 + 1),
+                e2 = ons_j<R, ONS>(d2[2], spar, j2 + 2);
+        const R sc = R(1) / sqrt(R(512));                   // unitary 1 / sqrt(W) of the row FFT
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const C a1 = haar_syn_q<R, C>(a2, h2, v2, e2, i, j);
+                const C lh = ons_j<R, ONS>(d1[0][i][j], spar, j1), hl = ons_j<R, ONS>(d1[1][i][j], spar, j1 + 1),
+                        hh = ons_j<R, ONS>(d1[2][i][j], spar, j1 + 2);
+                const C lo0 = Haar<R>::sum(a1, lh), lo1 = Haar<R>::dif(a1, lh);
+                const C hi0 = Haar<R>::sum(hl, hh), hi1 = Haar<R>::dif(hl, hh);
+                px[2 * i][2 * j] = cscale(Haar<R>::sum(lo0, hi0), sc);
+                px[2 * i][2 * j + 1] = cscale(Haar<R>::sum(lo1, hi1), -sc);
+                px[2 * i + 1][2 * j] = cscale(Haar<R>::dif(lo0, hi0), -sc);
+                px[2 * i + 1][2 * j + 1] = cscale(Haar<R>::dif(lo1, hi1), sc);
+            }
+    };
+    if (par) body(std::true_type{});
+    else body(std::false_type{});
+    {
+        C* b0 = buf + 544 * (4 * br) + SP(4 * bc);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b0[544 * i + j] = px[i][j];
+    }
+    __syncthreads();
+    C v[16];
+    strip_fft512_fwd<C>(buf, v, p.tw);
+    {
+        const int r = tid >> 5, t = tid & 31;
+        C* drow = p.dst + (long long)bi * p.dst_bs + (long long)st * 4096 + r * 512 + (t >> 1) + 256 * (t & 1);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) drow[16 * m] = v[m];
+    }
+}
+
+// K3 for W = 512, k = 3
+template <typename R, int OUT>
+__global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 4 : 2) analysis512(Geo g, AnaArgs<R> p) {
+    typedef typename CT<R>::T C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* buf = reinterpret_cast<C*>(smem_raw);
+    const int st = blockIdx.x, bi = blockIdx.y, tid = threadIdx.x;
+    const int br = tid >> 7, bc = tid & 127;
+    C* coef = p.coef + (long long)bi * g.N;
+    __shared__ R spar[MAXS * 3];
+    __shared__ C x2[2][128];                                // level-2 approximations
+    const int j1 = band_of(g.s, 1, 0), j2 = band_of(g.s, 2, 0), j3 = band_of(g.s, 3, 0);
+    const long long o1 = (long long)st * 1024 + (2 * br) * 256 + 2 * bc;
+    const long long o2 = (long long)st * 256 + br * 128 + bc;
+    constexpr bool OT = OUT == ANA_OUT_VDAMP;
+    C* ob = buf + SP(4095) + 1;
+    ob = reinterpret_cast<C*>((reinterpret_cast<uintptr_t>(ob) + 15) & ~(uintptr_t)15);
+    __shared__ __align__(8) unsigned long long obar;
+    if (OT && tid == 0) {
+        mbar_init(&obar, 1);
+        const unsigned cs = (unsigned)sizeof(C);
+        mbar_expect_tx(&obar, (p.adst ? 4032u : 4096u) * cs);
+        for (int o = 0; o < 3; ++o) {
+            bulk_g2s(ob + o * 1024, coef + g.off[j1 + o] + (long long)st * 1024, 1024u * cs, &obar);
+            bulk_g2s(ob + 3072 + o * 256, coef + g.off[j2 + o] + (long long)st * 256, 256u * cs, &obar);
+            bulk_g2s(ob + 3840 + o * 64, coef + g.off[j3 + o] + (long long)st * 64, 64u * cs, &obar);
+        }
+        if (!p.adst) bulk_g2s(ob + 4032, coef + g.off[0] + (long long)st * 64, 64u * cs, &obar);
+    }
+    if (OUT == ANA_OUT_VDAMP) {
+        const double* par = p.par + (long long)bi * g.S * 3;
+        for (int i = tid; i < g.S * 3; i += PNT) spar[i] = (R)par[i];
+    }
+    pdl_enter();
+    {
+        C v[16];
+        const int r = tid >> 5, t = tid & 31;
+        const C* srow = p.src + (long long)bi * p.src_bs + (long long)st * 4096 + r * 512 + (t >> 1) + 256 * (t & 1);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) v[m] = srow[16 * m];
+        strip_ifft512_to_smem<C>(buf, v, p.tw);
+    }
+    const R sc = (R)g.sign_c / sqrt(R(512));
+    C h1[2][2], v1[2][2], e1[2][2], l1[2][2];
+    {
+        const C* b0 = buf + 544 * (4 * br) + SP(4 * bc);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const C x00 = cscale(b0[544 * (2 * i) + 2 * j], sc);
+                const C x01 = cscale(b0[544 * (2 * i) + 2 * j + 1], -sc);
+                const C x10 = cscale(b0[544 * (2 * i + 1) + 2 * j], -sc);
+                const C x11 = cscale(b0[544 * (2 * i + 1) + 2 * j + 1], sc);
+                const C lo0 = Haar<R>::sum(x00, x10), hi0 = Haar<R>::dif(x00, x10);
+                const C lo1 = Haar<R>::sum(x01, x11), hi1 = Haar<R>::dif(x01, x11);
+                l1[i][j] = Haar<R>::sum(lo0, lo1);
+                h1[i][j] = Haar<R>::dif(lo0, lo1);
+                v1[i][j] = Haar<R>::sum(hi0, hi1);
+                e1[i][j] = Haar<R>::dif(hi0, hi1);
+            }
+    }
+    C l2, h2, v2, e2;
+    {
+        const C lo0 = Haar<R>::sum(l1[0][0], l1[1][0]), hi0 = Haar<R>::dif(l1[0][0], l1[1][0]);
+        const C lo1 = Haar<R>::sum(l1[0][1], l1[1][1]), hi1 = Haar<R>::dif(l1[0][1], l1[1][1]);
+        l2 = Haar<R>::sum(lo0, lo1); h2 = Haar<R>::dif(lo0, lo1); v2 = Haar<R>::sum(hi0, hi1); e2 = Haar<R>::dif(hi0, hi1);
+    }
+    x2[br][bc] = l2;
+    {
+        const C n1[3][2][2] = {{{h1[0][0], h1[0][1]}, {h1[1][0], h1[1][1]}},
+                               {{v1[0][0], v1[0][1]}, {v1[1][0], v1[1][1]}},
+                               {{e1[0][0], e1[0][1]}, {e1[1][0], e1[1][1]}}};
+        const C n2[3] = {h2, v2, e2};
+        if (OT) mbar_wait(&obar, 0);
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+            C* q1 = coef + g.off[j1 + o] + o1;
+            C* q2 = coef + g.off[j2 + o] + o2;
+            C w1[2][2], w2 = n2[o];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) { w1[i][0] = n1[o][i][0]; w1[i][1] = n1[o][i][1]; }
+            if (OUT == ANA_OUT_VDAMP) {
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int j = 0; j < 2; ++j)
+                        w1[i][j] = cadd(ons_j<R, true>(ob[o * 1024 + (2 * br + i) * 256 + 2 * bc + j], spar, j1 + o), w1[i][j]);
+                w2 = cadd(ons_j<R, true>(ob[3072 + o * 256 + br * 128 + bc], spar, j2 + o), w2);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) st2c<C>(q1 + i * 256, w1[i][0], w1[i][1]);
+            *q2 = w2;
+        }
+    }
+    __syncthreads();
+    // level 3: 64 threads, one per 8x8 block (one row of 64 level-3 coefficients)
+    if (tid >= 64) return;
+    {
+        const C x00 = x2[0][2 * tid], x01 = x2[0][2 * tid + 1], x10 = x2[1][2 * tid], x11 = x2[1][2 * tid + 1];
+        const C lo0 = Haar<R>::sum(x00, x10), hi0 = Haar<R>::dif(x00, x10);
+        const C lo1 = Haar<R>::sum(x01, x11), hi1 = Haar<R>::dif(x01, x11);
+        C n3[3] = {Haar<R>::dif(lo0, lo1), Haar<R>::sum(hi0, hi1), Haar<R>::dif(hi0, hi1)};
+        C a = Haar<R>::sum(lo0, lo1);
+        const long long o3 = (long long)st * 64 + tid;
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+            C* q = coef + g.off[j3 + o] + o3;
+            if (OUT == ANA_OUT_VDAMP) n3[o] = cadd(ons_j<R, true>(ob[3840 + o * 64 + tid], spar, j3 + o), n3[o]);
+            *q = n3[o];
+        }
+        if (p.adst) {
+            p.adst[(long long)bi * p.adst_bs + o3] = a;
+        } else {
+            C* q = coef + g.off[0] + o3;
+            if (OUT == ANA_OUT_VDAMP) a = cadd(ons_j<R, true>(ob[4032 + tid], spar, 0), a);
+            *q = a;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ K2 ----
 // COL_RAW: forward column FFT without the centring sign (X0 setup);
 // COL_NMSE: forward column FFT + Parseval error vs X0 off the mask (no IFFT)
@@ -1119,13 +1406,6 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass256(Geo g
 //   B: thread t = 2 k1 + b takes y_k1[2 a + b], a = 0..15; DFT16 over a; w32^(b k');
 //      radix-2 with its partner (lane ^ 8) -> X[k1 + 16 k' + 256 b], k' = 0..15
 // The inverse runs the same steps backwards with conjugate twiddles.
-template <typename C, bool INV>
-__device__ __forceinline__ void pow_twiddles512(C (&v)[16], int e, const C* __restrict__ tw) {
-    // v[m] *= w512^(+-e m), m = 1..15 (e <= 31)
-    C t1 = __ldg(tw + e), t2 = __ldg(tw + 2 * e), t4 = __ldg(tw + 4 * e), t8 = __ldg(tw + 8 * e);
-    if (INV) { t1 = cconj(t1); t2 = cconj(t2); t4 = cconj(t4); t8 = cconj(t8); }
-    pow_twiddles<C, 16>(v, t1, t2, t4, t8);
-}
 
 template <typename R, int MODE>
 __global__ void __launch_bounds__(PNT, 2) col_pass512(Geo g, ColArgs<R> p) {   // 2 CTAs/SM: spill-free
