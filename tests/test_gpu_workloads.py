@@ -274,3 +274,35 @@ def test_256_kernels_match_generic_path(tmp_path):
     w = workload.make_workload("cfg2", batch=1)             # 512-point column kernel
     x, _ = vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, 5, 4, ground_truths=w.x0, precision="fp64")
     assert rel2(x, np.load(str(tmp_path / "x_512.npy"))) <= 1e-10
+
+
+@pytest.mark.parametrize("size,scales", [(256, 5), (256, 6), (256, 8), (512, 3), (512, 4), (512, 6)])
+def test_dedicated_kernel_geometries_fp64_vs_oracle(oracle, size, scales):
+    """The 256/512 kernels with extra coarse passes (approximation through the scratch image)
+    or with the approximation subband in the first pass (512, s = 3): fp64 against the oracle."""
+    from paper_1911_01234_b200 import vdamp, workload
+    cfg = workload.Config(f"geo{size}s{scales}", 1, size, 12, scales, 4.0, 16, 40.0, 4)
+    w = workload.make_workload(cfg)
+    xs, trs = vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, scales, cfg.n_iters, ground_truths=w.x0,
+                              precision="fp64")
+    ref = _oracle_run(oracle, w, 0, cfg.n_iters, scales)
+    assert rel2(xs[0], ref.x_hat) <= 1e-8
+    dn = np.abs(trs[0].nmse_curve() - np.array([r.nmse_db for r in ref.records])).max()
+    assert dn <= 1e-6, dn
+
+
+@pytest.mark.parametrize("h,w,scales", [(256, 512, 4), (512, 256, 3), (256, 128, 4), (512, 1024, 3)])
+def test_rectangular_geometries_fp64_vs_oracle(oracle, h, w, scales):
+    """Mixed geometries: 256-point column kernel with a generic or 512-point row side and vice
+    versa (each side picks its own kernels), fp64 against the oracle."""
+    from paper_1911_01234_b200 import sampling, vdamp
+    rng = np.random.default_rng(h * 7 + w + scales)
+    x0 = sampling.random_ellipse_phantom(h, w, 10, rng) * np.exp(1j * sampling.smooth_phase(h, w, rng))
+    pmap = sampling.polynomial_pmap(h, w, undersampling=4.0)
+    mask = sampling.draw_mask(pmap, 11)
+    data = sampling.synthesize(x0, mask, 40.0, seed=12)
+    x, tr = vdamp.run(data.values, mask, pmap, data.noise_var, scales, 4, ground_truth=x0, precision="fp64")
+    ref = oracle.run(data.values, mask.indices, pmap.probs, data.noise_var, scales, 4, ground_truth=x0)
+    assert rel2(x, ref.x_hat) <= 1e-8
+    dn = np.abs(tr.nmse_curve() - np.array([r.nmse_db for r in ref.records])).max()
+    assert dn <= 1e-6, dn
