@@ -416,7 +416,7 @@ struct Seq {
         a.w0 = use_w0 ? (const C*)p->w0 : nullptr;
         a.kA = (R*)p->kA; a.kB = (R*)p->kB;
         // big subbands: 1024-thread CTAs with the full sort workspace; small ones:
-        // 256-thread CTAs with little shared memory, many per SM
+        // 128-thread CTAs with little shared memory, many per SM
         // the small-subband kernel runs on a side stream, concurrently with the
         // big one (its CTAs fill the SMs the big kernel's tail leaves idle)
         bool forked = false;

@@ -29,7 +29,10 @@ constexpr int SNT = 1024;         // threads of the per-image reduction kernels
 // memory would miss the ~30 KB of L1 left beside 200 KB of shared memory),
 // 1024 for fp64
 constexpr int BNT32 = 1024, BNT64 = 1024;
-constexpr int SNT_SMALL = 256;    // threads of the small-subband SURE kernel
+// threads of the small-subband SURE kernel: 128 (8 keys per thread at 1024 keys, up to
+// 128 registers) measured 400k vs 384k img-iter/s at 256 threads (cfg1); 64 threads
+// (236 registers) 401k; capping the 128-thread CTAs at 64 or 80 registers: 373k / 391k
+constexpr int SNT_SMALL = 128;
 constexpr int SMALL_N = 1024;     // subbands up to this size use the small kernel
 constexpr int SCAP = 16384;       // fp32 magnitudes sorted in shared memory at once
 template <typename R> struct Scap { static constexpr int v = SCAP; };
