@@ -609,12 +609,22 @@ int default_lanes(int batch) {
     return nl;
 }
 
+// side streams (small-subband SURE kernels) get the highest priority, so their
+// CTAs are placed first as SMs free up: 420k vs 412k img-iter/s (cfg1)
+cudaStream_t create_side_stream() {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    cudaStream_t s = nullptr;
+    CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
+    return s;
+}
+
 void set_lanes(Plan* p, int nl) {
     p->lanes = std::max(1, std::min(p->B, nl));
     while ((int)p->lane.size() < p->lanes) {
         Plan::Lane l;
         CK(cudaStreamCreateWithFlags(&l.st, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&l.side, cudaStreamNonBlocking));
+        l.side = create_side_stream();
         CK(cudaEventCreateWithFlags(&l.fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&l.join, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming));
@@ -815,7 +825,7 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
                 }
             }
         }
-        CK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+        p->side = create_side_stream();
         CK(cudaStreamCreateWithFlags(&p->gstream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
