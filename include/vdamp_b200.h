@@ -163,7 +163,7 @@ VDAMP_API int vdamp_set_graphs(vdamp_plan_t plan, int enable);
 /* Image lanes of vdamp_run's throughput path (no trace, NMSE or snapshots, no
  * graph): the batch runs as `lanes` contiguous image ranges on their own streams,
  * joined back into the caller's stream.  Results are identical for any lane count
- * (images are independent).  Default min(4, batch / 16) (2 from 256 images), env VDAMP_LANES overrides;
+ * (images are independent).  Default min(4, batch / 16) (1 from 256 images), env VDAMP_LANES overrides;
  * lanes = 0 restores the default. */
 VDAMP_API int vdamp_set_lanes(vdamp_plan_t plan, int lanes);
 /* total kernel launches issued by this plan since creation or the last reset */

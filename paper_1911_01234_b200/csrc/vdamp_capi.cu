@@ -599,12 +599,12 @@ struct Seq {
     }
 };
 
-// lanes of >= 16 images, at most 4; 2 for very large batches (cfg1, 64 x 256^2:
-// 2 / 3 / 4 / 8 lanes 402k / 401k / 420k / 372k; cfg4, 1024 x 256^2: 2 / 4 / 8 lanes
-// 458k / 447k / 433k; cfg2, 32 x 512^2: 1 / 2 / 4 lanes 41.1k / 43.8k / 41.6k img-iter/s);
-// VDAMP_LANES overrides
+// lanes of >= 16 images, at most 4; none for very large batches, which fill the GPU
+// by themselves (cfg1, 64 x 256^2: 2 / 3 / 4 / 8 lanes 402k / 401k / 420k / 372k;
+// cfg4, 1024 x 256^2: 1 / 2 / 4 / 8 lanes 466k / 458k / 447k / 433k; cfg2, 32 x 512^2:
+// 1 / 2 / 4 lanes 41.1k / 43.8k / 41.6k img-iter/s); VDAMP_LANES overrides
 int default_lanes(int batch) {
-    int nl = batch >= 256 ? 2 : std::max(1, std::min(4, batch / 16));
+    int nl = batch >= 256 ? 1 : std::max(1, std::min(4, batch / 16));
     if (const char* le = getenv("VDAMP_LANES")) nl = atoi(le);
     return nl;
 }
