@@ -2375,8 +2375,10 @@ __device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, in
                                           const double* sreg, const double* slo, const double* shi) {
     const int tid = threadIdx.x;
     constexpr int HALF = EMAX / 2 > 0 ? EMAX / 2 : 1;
-    const double nt = (double)n * tau;
-    double zacc = pre;
+    // risk(m) = sum_{j<=i} m_j^2 - n tau + 2 tau cnt + m (m cnt - tau inv_above)
+    // (the reference's expression regrouped: zn carries the first two terms)
+    const double tau2 = 2.0 * tau;
+    double zn = pre - (double)n * tau;
     double m = (double)keys[KI(b0)];
     double cnt = (double)(n - (tilebase + b0));                // keys above, counted down exactly
     double brisk = INFINITY;
@@ -2385,7 +2387,7 @@ __device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, in
     for (int e = 0; e < EMAX; ++e) {
         if (e < E && (!RAG || b0 + e < T)) {
             const int il = b0 + e;
-            zacc += m * m;                                     // sum_{j <= i} m_j^2
+            zn = fma(m, m, zn);                                // + sum_{j <= i} m_j^2
             cnt -= 1.0;
             const double nxt = (il + 1 < T) ? (double)keys[KI(il + 1)] : next_tile_first;
             if (m != nxt) {
@@ -2393,15 +2395,17 @@ __device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, in
                 if constexpr (SMEM) sl = (e < HALF ? slo : shi)[(e % HALF) * NT + tid];
                 else sl = sreg[e];
                 const double inv_above = suf + sl;             // both >= 0: no cancellation
-                const double risk = zacc + m * m * cnt - nt + tau * (2.0 * cnt - m * inv_above);
+                const double ti = tau * inv_above, g = m * cnt;
+                const double base = fma(tau2, cnt, zn);
+                const double risk = fma(m, g - ti, base);
                 if (risk < brisk) { brisk = risk; bcode = 2 * e; }
-                // stationary point ts = tau*inv/(2 cnt) inside (m, nxt)?  Pre-test by
+                // stationary point ts = ti/(2 cnt) inside (m, nxt)?  Pre-test by
                 // multiplication with a relative guard, divide only for survivors.
-                const double ti = tau * inv_above, c2 = 2.0 * cnt;
-                if (cnt > 0 && ti > c2 * m * (1.0 - 1e-12) && ti < c2 * nxt * (1.0 + 1e-12)) {
+                if (cnt > 0 && ti > g * (2.0 - 2e-12) && ti < (cnt * nxt) * (2.0 + 2e-12)) {
+                    const double c2 = 2.0 * cnt;
                     const double ts = div_pos(ti, c2);
                     if (ts > m && ts < nxt) {
-                        const double rs = zacc + ts * ts * cnt - nt + tau * (2.0 * cnt - ts * inv_above);
+                        const double rs = fma(ts, ts * cnt - ti, base);
                         if (rs < brisk) { brisk = rs; bcode = 2 * e + 1; }
                     }
                 }
@@ -2705,10 +2709,11 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             const double totinv = s_totinv;
             const double nn = (double)n;
             Best bb = S_.run;
-            consider(bb, 0.0 + 0.0 * nn - nn * tau + tau * (2.0 * nn - 0.0 * totinv), 0.0, nn, totinv);
+            const double base0 = fma(2.0 * tau, nn, -(nn * tau));   // scan_keys' grouping at t = 0
+            consider(bb, base0, 0.0, nn, totinv);
             const double ts = tau * totinv / (2.0 * nn);
             if (ts > 0.0 && ts < m0) {
-                const double rsk = 0.0 + ts * ts * nn - nn * tau + tau * (2.0 * nn - ts * totinv);
+                const double rsk = fma(ts, ts * nn - tau * totinv, base0);
                 consider(bb, rsk, ts, nn, totinv);
             }
             S_.run = bb;
@@ -3011,10 +3016,11 @@ __global__ void __launch_bounds__(1024, 1) big_range(Geo g, SelArgs<float> a, Bi
             if (m0 > 0) {
                 const double totinv = __ldcg(b.aux + sb * 2);
                 const double nn = (double)n;
-                consider(bb, 0.0 + 0.0 * nn - nn * tau + tau * (2.0 * nn - 0.0 * totinv), 0.0, nn, totinv);
+                const double base0 = fma(2.0 * tau, nn, -(nn * tau));   // scan_keys' grouping at t = 0
+                consider(bb, base0, 0.0, nn, totinv);
                 const double ts = tau * totinv / (2.0 * nn);
                 if (ts > 0.0 && ts < m0) {
-                    const double rsk = 0.0 + ts * ts * nn - nn * tau + tau * (2.0 * nn - ts * totinv);
+                    const double rsk = fma(ts, ts * nn - tau * totinv, base0);
                     consider(bb, rsk, ts, nn, totinv);
                 }
             }
