@@ -380,7 +380,9 @@ struct Seq {
         }
         if (c256() && (mode == COL_VDAMP || mode == COL_FINAL || mode == COL_NMSE)) {
             const int np = 2 * p->s, npp = (np + 3) & ~3;
-            const size_t sm = (size_t)col256_region0<R>(np) + (size_t)256 * npp * sizeof(R) + (size_t)np * 16 * sizeof(double);
+            // transpose tile | row profiles | column profiles | tau partials [np][PNT]
+            const size_t sm = (size_t)col256_region0<R>(np) + (size_t)256 * npp * sizeof(R) +
+                              (size_t)np * 16 * sizeof(double) + (size_t)np * PNT * sizeof(double);
             switch (mode) {
                 case COL_VDAMP: { auto k = col_pass256<R, COL_VDAMP>; set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }
                 case COL_NMSE:  { auto k = col_pass256<R, COL_NMSE>;  set_smem(k, sm); launch(k, grid, PNT, sm, st, p->geo, a); break; }

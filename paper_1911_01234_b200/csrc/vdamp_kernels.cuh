@@ -1080,6 +1080,17 @@ __device__ __forceinline__ void band_profiles(int s, int j, int& prow, int& pcol
     pcol = 2 * (l - 1) + (o != 1 ? 1 : 0);
 }
 
+// tau weight p^-1 ((p^-1 - 1) |z|^2 + sigma^2) of one sampled point
+// (src/vdamp.py:74-75).  fp32 mode stores it as float anyway and every term is
+// >= 0 (p^-1 >= 1), so it is evaluated in float there (no cancellation; the
+// float64 version cost a quarter of the column kernel in F2F conversions).
+__device__ __forceinline__ float tau_weight(float pv, float2 zc, double, float nvf) {
+    return pv * fmaf(pv - 1.0f, fmaf(zc.x, zc.x, zc.y * zc.y), nvf);
+}
+__device__ __forceinline__ double tau_weight(double pv, double2 zc, double nv, float) {
+    return pv * ((pv - 1.0) * (zc.x * zc.x + zc.y * zc.y) + nv);
+}
+
 template <typename R, int MODE>
 __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass(Geo g, ColArgs<R> p) {
     pdl_enter();
@@ -1143,6 +1154,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass(Geo g, C
     }
     const R cs = (R)g.sign_c;
     const double nv = (MODE == COL_VDAMP) ? p.noise_var[bi] : 0.0;
+    const float nvf = (float)nv;
     // tau partials: tau_j = sum_w a_j(w1) b_j(w2) weight(w) (separable |F psi_j|^2,
     // src/vdamp.py:59-78).  Thread tid always sees column c = tid % cw (PNT is a
     // multiple of cw), so it accumulates its rows' weights per row profile in
@@ -1173,9 +1185,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass(Geo g, C
                 if (pv != R(0)) {
                     const C zc = csub(ys[i], X);             // (-1)^(k1+k2) z  (src/vdamp.py:112)
                     v = cscale(zc, pv);                      // P^-1 z           (src/vdamp.py:113)
-                    const double pd = (double)pv;
-                    const double z2 = (double)zc.x * (double)zc.x + (double)zc.y * (double)zc.y;
-                    wreg[i] = (R)(pd * ((pd - 1.0) * z2 + nv));   // tau weight (src/vdamp.py:74-75)
+                    wreg[i] = tau_weight(pv, zc, nv, nvf);   // tau weight (src/vdamp.py:74-75)
                 } else {
                     v = mk<C>(R(0), R(0));
                 }
@@ -1247,14 +1257,14 @@ template <> __device__ __forceinline__ void ld4<double>(const double* q, double&
 // those 16 frequencies and runs the inverse FFT from them directly; outputs are
 // rows d + 16 n2.  Modes: COL_VDAMP, COL_FINAL, COL_NMSE.
 // bytes of col_pass256's first shared region: the transpose tile, later the
-// tau partials [np][256] and column sums [np][16] (doubles)
+// column sums [np][16] (doubles); the thread partials have their own region
 template <typename R>
 __host__ __device__ constexpr int col512_region0(int np) {
     return (4096 * 2 * (int)sizeof(R) > np * (256 + 8) * 8) ? 4096 * 2 * (int)sizeof(R) : np * (256 + 8) * 8;
 }
 template <typename R>
 __host__ __device__ constexpr int col256_region0(int np) {
-    return (4096 * 2 * (int)sizeof(R) > np * (256 + 16) * 8) ? 4096 * 2 * (int)sizeof(R) : np * (256 + 16) * 8;
+    return (4096 * 2 * (int)sizeof(R) > np * 16 * 8) ? 4096 * 2 * (int)sizeof(R) : np * 16 * 8;
 }
 template <typename R, int MODE>
 __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass256(Geo g, ColArgs<R> p) {
@@ -1296,6 +1306,17 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass256(Geo g
     C v[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = p.src[colbase + (long long)(16 * j) * W];
+    // the measurements (L2-prefetched before the wait) load under the forward FFT
+    R pvs[16];
+    C ys[16];
+    if (MODE != COL_NMSE) {
+#pragma unroll
+        for (int k2 = 0; k2 < 16; ++k2) {
+            const long long gi = colbase + (long long)(16 * k2) * W;
+            pvs[k2] = p.pinv[gi];
+            ys[k2] = p.yg[gi];
+        }
+    }
     fft256_stage_a<C, false>(v, d, p.tw);
 #pragma unroll
     for (int m = 0; m < 16; ++m) buf[(m * 16 + d) * 16 + c] = v[m];
@@ -1323,14 +1344,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass256(Geo g
     R wreg[16];
     {
         const double nv = (MODE == COL_VDAMP) ? p.noise_var[bi] : 0.0;
-        R pvs[16];
-        C ys[16];
-#pragma unroll
-        for (int k2 = 0; k2 < 16; ++k2) {                  // issue all measurement loads first
-            const long long gi = colbase + (long long)(16 * k2) * W;
-            pvs[k2] = p.pinv[gi];
-            ys[k2] = p.yg[gi];
-        }
+        const float nvf = (float)nv;
 #pragma unroll
         for (int k2 = 0; k2 < 16; ++k2) {
             const C X = cscale(v[k2], sc * cs);            // c * FFT2u, so (-1)^(k1+k2) X_centred
@@ -1340,9 +1354,7 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass256(Geo g
                 if (pv != R(0)) {
                     const C zc = csub(ys[k2], X);                  // (-1)^(k1+k2) z  (src/vdamp.py:112)
                     v[k2] = cscale(zc, pv);                        // P^-1 z           (src/vdamp.py:113)
-                    const double pd = (double)pv;
-                    const double z2 = (double)zc.x * (double)zc.x + (double)zc.y * (double)zc.y;
-                    wk = (R)(pd * ((pd - 1.0) * z2 + nv));         // tau weight (src/vdamp.py:74-75)
+                    wk = tau_weight(pv, zc, nv, nvf);              // tau weight (src/vdamp.py:74-75)
                 } else {
                     v[k2] = mk<C>(R(0), R(0));
                 }
@@ -1350,6 +1362,27 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass256(Geo g
                 v[k2] = (pv != R(0)) ? ys[k2] : X;
             }
             wreg[k2] = wk;
+        }
+    }
+    // tau partials (as col_pass) now, so the weights are dead before the
+    // inverse FFT: per row profile q, this thread's 16 rows d + 16 k2 against
+    // profiles staged row-major [row][npp] (float4 loads), into a dedicated
+    // shared region [np][PNT]
+    double* pearly = reinterpret_cast<double*>(smem_raw + A + 256 * npp * (int)sizeof(R) + np * 16 * 8);
+    if (MODE == COL_VDAMP) {
+        mbar_wait(&pbar, 0);                               // profiles landed
+        for (int q0 = 0; q0 < np; q0 += 4) {
+            R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
+#pragma unroll
+            for (int k2 = 0; k2 < 16; ++k2) {
+                R b0, b1, b2, b3;
+                ld4<R>(prs + (d + 16 * k2) * npp + q0, b0, b1, b2, b3);
+                const R wk = wreg[k2];
+                a0 += b0 * wk; a1 += b1 * wk; a2 += b2 * wk; a3 += b3 * wk;
+            }
+            pearly[q0 * PNT + tid] = (double)a0;
+            pearly[(q0 + 1) * PNT + tid] = (double)a1;
+            if (q0 + 2 < np) { pearly[(q0 + 2) * PNT + tid] = (double)a2; pearly[(q0 + 3) * PNT + tid] = (double)a3; }
         }
     }
     fft256_stage_a<C, true>(v, d, p.tw);
@@ -1364,28 +1397,11 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass256(Geo g
     for (int n2 = 0; n2 < 16; ++n2) p.dst[colbase + (long long)(16 * n2) * W] = cscale(v[n2], sc);
     if (MODE != COL_VDAMP) return;
 
-    // tau partials (as col_pass): per row profile q, this thread's 16 rows
-    // d + 16 k2 in registers against profiles staged row-major [row][npp]
-    // (float4 loads), then a fixed-order combination over the 16 threads of
-    // each column and the column profiles
+    // fixed-order combination over the 16 threads of each column, then the
+    // column profiles
     __syncthreads();                                       // inverse transpose reads done
-    mbar_wait(&pbar, 0);                                   // profiles landed
-    double* part = reinterpret_cast<double*>(buf);         // [np][PNT] thread partials
-    double* psum = part + np * PNT;                        // [np][16] column partials
-    for (int q0 = 0; q0 < np; q0 += 4) {
-        R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
-#pragma unroll
-        for (int k2 = 0; k2 < 16; ++k2) {
-            R b0, b1, b2, b3;
-            ld4<R>(prs + (d + 16 * k2) * npp + q0, b0, b1, b2, b3);
-            const R wk = wreg[k2];
-            a0 += b0 * wk; a1 += b1 * wk; a2 += b2 * wk; a3 += b3 * wk;
-        }
-        part[q0 * PNT + tid] = (double)a0;
-        part[(q0 + 1) * PNT + tid] = (double)a1;
-        if (q0 + 2 < np) { part[(q0 + 2) * PNT + tid] = (double)a2; part[(q0 + 3) * PNT + tid] = (double)a3; }
-    }
-    __syncthreads();
+    double* part = pearly;                                 // [np][PNT] thread partials
+    double* psum = reinterpret_cast<double*>(buf);         // [np][16] column partials
     for (int it = tid; it < np * 16; it += PNT) {
         const int q = it >> 4, cc = it & 15;
         double sacc = 0.0;
@@ -1485,6 +1501,7 @@ __global__ void __launch_bounds__(PNT, 2) col_pass512(Geo g, ColArgs<R> p) {   /
     R wreg[16];
     {
         const double nv = (MODE == COL_VDAMP) ? p.noise_var[bi] : 0.0;
+        const float nvf = (float)nv;
         R pvs[16];
         C ys[16];
 #pragma unroll
@@ -1502,9 +1519,7 @@ __global__ void __launch_bounds__(PNT, 2) col_pass512(Geo g, ColArgs<R> p) {   /
                 if (pv != R(0)) {
                     const C zc = csub(ys[m], X);                   // (-1)^(k1+k2) z  (src/vdamp.py:112)
                     v[m] = cscale(zc, pv);                         // P^-1 z           (src/vdamp.py:113)
-                    const double pd = (double)pv;
-                    const double z2 = (double)zc.x * (double)zc.x + (double)zc.y * (double)zc.y;
-                    wk = (R)(pd * ((pd - 1.0) * z2 + nv));         // tau weight (src/vdamp.py:74-75)
+                    wk = tau_weight(pv, zc, nv, nvf);              // tau weight (src/vdamp.py:74-75)
                 } else {
                     v[m] = mk<C>(R(0), R(0));
                 }
