@@ -58,8 +58,8 @@ template <typename R, typename C>
 __device__ __forceinline__ C onsager(C r, R t, R alpha, R gain) {
     R m = cmag(r);
     R sh = (m > t) ? (R(1) - sdiv(t, m)) : R(0);   // m > t >= 0, so m is normal
-    R wx = r.x * sh, wy = r.y * sh;
-    return mk<C>((wx - alpha * r.x) * gain, (wy - alpha * r.y) * gain);
+    const R f = (sh - alpha) * gain;                // (soft(r) - alpha r) / (1 - alpha) = r f
+    return mk<C>(r.x * f, r.y * f);
 }
 
 // ---------------------------------------------------------------------------
