@@ -94,6 +94,7 @@ struct Plan {
     cudaStream_t side = nullptr;    // fork/join stream for the small-subband SURE kernel
     // CUDA graph of the whole vdamp_run sequence, re-captured when its key changes
     bool graphs = true;
+    bool interleave = true;          // lanes launched iteration-major (VDAMP_INTERLEAVE=0: lane-major)
     cudaGraphExec_t gexec = nullptr;
     std::vector<const void*> gkey;
     long long g_launches = 0;
@@ -570,9 +571,12 @@ struct Seq {
         synth((const C*)p->what, nullptr, false, xhat, 4);                  // x_hat = idwt(w_hat)
     }
 
-    void run(int n_iters, C* xhat, double* trace, double* nmse_out, void* const* snaps) {
+    void begin() {
         CK(cudaMemsetAsync(p->r, 0, (size_t)p->B * p->N * sizeof(C), st));   // r~_0 = 0
         identity_params();
+    }
+    void run(int n_iters, C* xhat, double* trace, double* nmse_out, void* const* snaps) {
+        begin();
         const long long tstride = (long long)p->B * p->S * TRACE_F;
         if (nmse_out && p->parseval) {
             // per-run Parseval constants: sum_mask |y - F x0|^2 and |x0|^2
@@ -836,6 +840,7 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         p->graphs = (long long)batch * p->N <= 8LL * 65536;
         if (const char* pe = getenv("VDAMP_PARSEVAL")) p->parseval = atoi(pe) != 0;
         if (const char* ge = getenv("VDAMP_GRAPHS")) p->graphs = atoi(ge) != 0;
+        if (const char* ie = getenv("VDAMP_INTERLEAVE")) p->interleave = atoi(ie) != 0;
         CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
         set_lanes(p, default_lanes(batch));
@@ -1004,6 +1009,45 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
             CK(cudaSetDevice(p->dev));
             CK(cudaEventRecord(p->lane_start, caller));
             const int L = p->lanes;
+            if (p->interleave) {
+                // iteration-major launch order: every lane gets its iteration k before
+                // any lane gets k + 1, so the lanes start together instead of one
+                // host-submission time apart
+                std::vector<Plan> vs;
+                std::vector<long long> l0(L), c0((size_t)L * VDAMP_KERNEL_CLASSES);
+                vs.reserve(L);
+                for (int li = 0; li < L; ++li) {
+                    const int b0 = (int)((long long)p->B * li / L), b1 = (int)((long long)p->B * (li + 1) / L);
+                    CK(cudaStreamWaitEvent(p->lane[li].st, p->lane_start, 0));
+                    vs.push_back(lane_view(p, b0, b1 - b0, p->lane[li]));
+                    l0[li] = vs[li].launches;
+                    for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) c0[(size_t)li * VDAMP_KERNEL_CLASSES + c] = vs[li].cls_launches[c];
+                }
+                auto each = [&](auto&& fn) {
+                    for (int li = 0; li < L; ++li) dispatch(&vs[li], (void*)p->lane[li].st, fn);
+                };
+                try {
+                    each([&](auto& s) { s.begin(); });
+                    for (int it = 0; it < n_iters; ++it) each([&](auto& s) { s.iteration(nullptr, nullptr); });
+                    for (int li = 0; li < L; ++li) {
+                        const int b0 = (int)((long long)p->B * li / L);
+                        void* xo = (char*)x_hat + (size_t)b0 * p->N * p->csz;
+                        dispatch(&vs[li], (void*)p->lane[li].st, [&](auto& s) {
+                            typedef typename std::remove_reference<decltype(s)>::type S_;
+                            s.finalize_from_r(s.p->parf, (typename S_::C*)xo);
+                        });
+                    }
+                } catch (...) {
+                    for (int li = 0; li < L; ++li) lane_merge(p, vs[li], l0[li], &c0[(size_t)li * VDAMP_KERNEL_CLASSES]);
+                    throw;
+                }
+                for (int li = 0; li < L; ++li) {
+                    lane_merge(p, vs[li], l0[li], &c0[(size_t)li * VDAMP_KERNEL_CLASSES]);
+                    CK(cudaEventRecord(p->lane[li].done, p->lane[li].st));
+                    CK(cudaStreamWaitEvent(caller, p->lane[li].done, 0));
+                }
+                return;
+            }
             for (int li = 0; li < L; ++li) {
                 const int b0 = (int)((long long)p->B * li / L), b1 = (int)((long long)p->B * (li + 1) / L);
                 Plan::Lane& l = p->lane[li];
