@@ -1005,9 +1005,12 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
         if (!x_hat) throw Err{VDAMP_ERR_ARG, "null x_hat"};
         cudaStream_t caller = (cudaStream_t)stream;
         cudaStream_t st = caller;
-        if (!p->graphs && p->lanes > 1 && !trace && !nmse && !snapshots) {
+        // image lanes (throughput path: no trace, NMSE or snapshots), forked from and
+        // joined back into stream cs; also captured into the graph below
+        const bool use_lanes = p->lanes > 1 && !trace && !nmse && !snapshots;
+        auto run_lanes = [&](cudaStream_t cs) {
             CK(cudaSetDevice(p->dev));
-            CK(cudaEventRecord(p->lane_start, caller));
+            CK(cudaEventRecord(p->lane_start, cs));
             const int L = p->lanes;
             if (p->interleave) {
                 // iteration-major launch order: every lane gets its iteration k before
@@ -1044,7 +1047,7 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
                 for (int li = 0; li < L; ++li) {
                     lane_merge(p, vs[li], l0[li], &c0[(size_t)li * VDAMP_KERNEL_CLASSES]);
                     CK(cudaEventRecord(p->lane[li].done, p->lane[li].st));
-                    CK(cudaStreamWaitEvent(caller, p->lane[li].done, 0));
+                    CK(cudaStreamWaitEvent(cs, p->lane[li].done, 0));
                 }
                 return;
             }
@@ -1065,8 +1068,12 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
                 } catch (...) { lane_merge(p, v, l0, c0); throw; }
                 lane_merge(p, v, l0, c0);
                 CK(cudaEventRecord(l.done, l.st));
-                CK(cudaStreamWaitEvent(caller, l.done, 0));
+                CK(cudaStreamWaitEvent(cs, l.done, 0));
             }
+            return;
+        };
+        if (!p->graphs && use_lanes) {
+            run_lanes(caller);
             return;
         }
         if (!p->graphs) {
@@ -1087,7 +1094,8 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
         void* sarg = (void*)st;
         // key: everything baked into the captured launches
         std::vector<const void*> key{(const void*)(intptr_t)n_iters, x_hat, trace, nmse, (const void*)(intptr_t)p->have_gt,
-                                     (const void*)(intptr_t)p->timing, (const void*)st};
+                                     (const void*)(intptr_t)p->timing, (const void*)st,
+                                     (const void*)(intptr_t)(use_lanes ? p->lanes : 1), (const void*)(intptr_t)p->interleave};
         if (snapshots) for (int k = 0; k < n_iters; ++k) key.push_back(snapshots[k]);
         else key.push_back(nullptr);
         if (!p->gexec || key != p->gkey) {
@@ -1102,7 +1110,8 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
             CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
             bool ok = true;
             try {
-                dispatch(p, sarg, [&](auto& s) {
+                if (use_lanes) run_lanes(st);
+                else dispatch(p, sarg, [&](auto& s) {
                     typedef typename std::remove_reference<decltype(s)>::type S_;
                     s.run(n_iters, (typename S_::C*)x_hat, trace, nmse, snapshots);
                 });
@@ -1117,7 +1126,8 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
                 p->launches = l0;
                 for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) p->cls_launches[c] = c0[c];
                 cudaGetLastError();
-                dispatch(p, sarg, [&](auto& s) {
+                if (use_lanes) run_lanes(st);
+                else dispatch(p, sarg, [&](auto& s) {
                     typedef typename std::remove_reference<decltype(s)>::type S_;
                     s.run(n_iters, (typename S_::C*)x_hat, trace, nmse, snapshots);
                 });
@@ -1127,7 +1137,7 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
                 }
                 return;
             }
-            CK(cudaGraphInstantiate(&p->gexec, graph, 0));
+            CK(cudaGraphInstantiate(&p->gexec, graph, cudaGraphInstantiateFlagUseNodePriority));
             cudaGraphDestroy(graph);
             p->gkey = key;
             p->g_launches = p->launches - l0;
