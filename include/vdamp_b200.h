@@ -160,10 +160,12 @@ VDAMP_API int vdamp_kernel_times(vdamp_plan_t plan, double* ms, int64_t* launche
  * stream and flags are unchanged.  With timing enabled each graph run synchronises
  * once to accumulate the kernel times. */
 VDAMP_API int vdamp_set_graphs(vdamp_plan_t plan, int enable);
-/* Image lanes of vdamp_run's throughput path (no trace, NMSE or snapshots, no
- * graph): the batch runs as `lanes` contiguous image ranges on their own streams,
- * joined back into the caller's stream.  Results are identical for any lane count
- * (images are independent).  Default min(4, batch / 16) (1 from 256 images), env VDAMP_LANES overrides;
+/* Image lanes of vdamp_run's throughput path (no trace, NMSE or snapshots): the
+ * batch runs as `lanes` contiguous image ranges on their own streams, forked from
+ * and joined back into the caller's stream, launched iteration-major (every lane
+ * gets iteration k before any lane gets k+1; env VDAMP_INTERLEAVE=0: lane-major).
+ * When graphs are on, the fork/join is captured into the graph.  Results are
+ * identical for any lane count (images are independent).  Default min(4, batch / 16) (1 from 256 images), env VDAMP_LANES overrides;
  * lanes = 0 restores the default. */
 VDAMP_API int vdamp_set_lanes(vdamp_plan_t plan, int lanes);
 /* total kernel launches issued by this plan since creation or the last reset */
