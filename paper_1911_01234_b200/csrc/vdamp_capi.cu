@@ -575,31 +575,36 @@ struct Seq {
         CK(cudaMemsetAsync(p->r, 0, (size_t)p->B * p->N * sizeof(C), st));   // r~_0 = 0
         identity_params();
     }
+    // per-run Parseval constants: sum_mask |y - F x0|^2 and |x0|^2
+    void nmse_begin() {
+        if (!p->parseval) return;
+        Launch L(p, 5, st);
+        nmse_setup<R><<<p->B, SNT, 0, st>>>(p->geo, (const C*)p->yg, (const R*)p->pinv, (const C*)p->x0r,
+                                            (const C*)p->x0, p->nmconst);
+    }
+
+    // NMSE record of this iteration's estimate into rec[b * VDAMP_NMSE_FIELDS]
+    void nmse_iter(double* rec) {
+        if (p->parseval) {
+            // x_hat_k = finalize(soft(r_k)): F x_hat is y on the mask and
+            // F Psi^H w_hat elsewhere, so one forward FFT suffices
+            synth(r(), p->parf, true, nullptr, 4);
+            col(COL_NMSE, (const C*)p->T1, nullptr, 4);
+            Launch L(p, 5, st);
+            nmse_finish<<<(p->B + 127) / 128, 128, 0, st>>>(p->nmpart, p->ntiles, p->nmconst, rec, p->B);
+        } else {
+            finalize_from_r(p->parf, (C*)p->xtmp);
+            nmse((const C*)p->xtmp, rec);
+        }
+    }
+
     void run(int n_iters, C* xhat, double* trace, double* nmse_out, void* const* snaps) {
         begin();
         const long long tstride = (long long)p->B * p->S * TRACE_F;
-        if (nmse_out && p->parseval) {
-            // per-run Parseval constants: sum_mask |y - F x0|^2 and |x0|^2
-            Launch L(p, 5, st);
-            nmse_setup<R><<<p->B, SNT, 0, st>>>(p->geo, (const C*)p->yg, (const R*)p->pinv, (const C*)p->x0r,
-                                                (const C*)p->x0, p->nmconst);
-        }
+        if (nmse_out) nmse_begin();
         for (int it = 0; it < n_iters; ++it) {
             iteration(trace ? trace + it * tstride : nullptr, snaps ? snaps[it] : nullptr);
-            if (nmse_out) {
-                double* rec = nmse_out + (long long)it * p->B * VDAMP_NMSE_FIELDS;
-                if (p->parseval) {
-                    // x_hat_k = finalize(soft(r_k)): F x_hat is y on the mask and
-                    // F Psi^H w_hat elsewhere, so one forward FFT suffices
-                    synth(r(), p->parf, true, nullptr, 4);
-                    col(COL_NMSE, (const C*)p->T1, nullptr, 4);
-                    Launch L(p, 5, st);
-                    nmse_finish<<<(p->B + 127) / 128, 128, 0, st>>>(p->nmpart, p->ntiles, p->nmconst, rec, p->B);
-                } else {
-                    finalize_from_r(p->parf, (C*)p->xtmp);
-                    nmse((const C*)p->xtmp, rec);
-                }
-            }
+            if (nmse_out) nmse_iter(nmse_out + (long long)it * p->B * VDAMP_NMSE_FIELDS);
         }
         finalize_from_r(p->parf, xhat);
     }
@@ -973,6 +978,9 @@ Plan lane_view(const Plan* p, int b0, int nb, const Plan::Lane& l) {
     v.taupart = p->taupart + (size_t)b0 * p->ntiles * p->S;
     v.nvar = p->nvar + b0;
     v.trtmp = p->trtmp + (size_t)b0 * p->S * TRACE_F;
+    v.x0 = off(p->x0, ci); v.w0 = off(p->w0, ci); v.x0r = off(p->x0r, ci); v.xtmp = off(p->xtmp, ci);
+    if (p->nmconst) v.nmconst = p->nmconst + (size_t)b0 * 2;
+    if (p->nmpart) v.nmpart = p->nmpart + (size_t)b0 * p->ntiles;
     if (p->bigpath) {
         const size_t nl = p->large.size();
         v.bhist = p->bhist + (size_t)b0 * nl * BIGB;
@@ -1007,7 +1015,9 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
         cudaStream_t st = caller;
         // image lanes (throughput path: no trace, NMSE or snapshots), forked from and
         // joined back into stream cs; also captured into the graph below
-        const bool use_lanes = p->lanes > 1 && !trace && !nmse && !snapshots;
+        // diagnostics (trace, NMSE, snapshots) ride on the lanes in iteration-major order:
+        // each lane writes its image range of every per-iteration record
+        const bool use_lanes = p->lanes > 1 && (p->interleave || (!trace && !nmse && !snapshots));
         auto run_lanes = [&](cudaStream_t cs) {
             CK(cudaSetDevice(p->dev));
             CK(cudaEventRecord(p->lane_start, cs));
@@ -1029,9 +1039,20 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
                 auto each = [&](auto&& fn) {
                     for (int li = 0; li < L; ++li) dispatch(&vs[li], (void*)p->lane[li].st, fn);
                 };
+                const long long tstride = (long long)p->B * p->S * TRACE_F;
                 try {
                     each([&](auto& s) { s.begin(); });
-                    for (int it = 0; it < n_iters; ++it) each([&](auto& s) { s.iteration(nullptr, nullptr); });
+                    if (nmse) each([&](auto& s) { s.nmse_begin(); });
+                    for (int it = 0; it < n_iters; ++it)
+                        for (int li = 0; li < L; ++li) {
+                            const long long b0 = (long long)p->B * li / L;
+                            double* tr = trace ? trace + it * tstride + b0 * p->S * TRACE_F : nullptr;
+                            void* sn = (snapshots && snapshots[it]) ? (void*)((char*)snapshots[it] + (size_t)b0 * p->N * p->csz) : nullptr;
+                            dispatch(&vs[li], (void*)p->lane[li].st, [&](auto& s) {
+                                s.iteration(tr, sn);
+                                if (nmse) s.nmse_iter(nmse + ((long long)it * p->B + b0) * VDAMP_NMSE_FIELDS);
+                            });
+                        }
                     for (int li = 0; li < L; ++li) {
                         const int b0 = (int)((long long)p->B * li / L);
                         void* xo = (char*)x_hat + (size_t)b0 * p->N * p->csz;

@@ -306,3 +306,32 @@ def test_rectangular_geometries_fp64_vs_oracle(oracle, h, w, scales):
     assert rel2(x, ref.x_hat) <= 1e-8
     dn = np.abs(tr.nmse_curve() - np.array([r.nmse_db for r in ref.records])).max()
     assert dn <= 1e-6, dn
+
+
+def test_lanes_with_diagnostics_bitwise_equal(monkeypatch):
+    """Image lanes also carry the trace, the per-iteration NMSE and the r snapshots
+    (each lane writes its image range of every record): bitwise the same as one lane."""
+    import dataclasses
+    from paper_1911_01234_b200 import vdamp, workload
+    from paper_1911_01234_b200.plan import clear_plans
+    w = workload.make_workload("cfg1", batch=32)
+    res = {}
+    for lanes in ("1", "3"):
+        monkeypatch.setenv("VDAMP_LANES", lanes)
+        clear_plans()
+        res[lanes] = vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, 4, 5, ground_truths=w.x0,
+                                     keep_r_iters=(1, 4), precision="fp32", keep_device=True)
+    clear_plans()
+    (a, ta), (b, tb) = res["1"], res["3"]
+    assert np.array_equal(a, b) and np.isfinite(a).all()
+    assert len(ta) == len(tb) == 32
+    for x, y in zip(ta, tb):
+        assert len(x.records) == len(y.records) == 5
+        for rx, ry in zip(x.records, y.records):
+            dx, dy = dataclasses.asdict(rx), dataclasses.asdict(ry)
+            for k in dx:
+                if "time" in k:
+                    continue
+                assert np.array_equal(np.asarray(dx[k]), np.asarray(dy[k])), k
+    for k in (1, 4):
+        assert ta[0].device_snapshots[k].equal(tb[0].device_snapshots[k])
