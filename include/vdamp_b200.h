@@ -160,8 +160,8 @@ VDAMP_API int vdamp_kernel_times(vdamp_plan_t plan, double* ms, int64_t* launche
  * stream and flags are unchanged.  With timing enabled each graph run synchronises
  * once to accumulate the kernel times. */
 VDAMP_API int vdamp_set_graphs(vdamp_plan_t plan, int enable);
-/* Image lanes of vdamp_run's throughput path (no trace, NMSE or snapshots): the
- * batch runs as `lanes` contiguous image ranges on their own streams, forked from
+/* Image lanes of vdamp_run (with trace, NMSE or snapshots only when interleaved,
+ * each lane writing its image range of every record): the batch runs as `lanes` contiguous image ranges on their own streams, forked from
  * and joined back into the caller's stream, launched iteration-major (every lane
  * gets iteration k before any lane gets k+1; env VDAMP_INTERLEAVE=0: lane-major).
  * When graphs are on, the fork/join is captured into the graph.  Results are
