@@ -50,6 +50,17 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 # ----------------------------------------------------------------- CPU leg --
 _W = None
 
@@ -153,14 +164,66 @@ def class_bytes(cfg, N, n_mean, images, iters, b_c):
 
 
 def traffic_from_profiles(kernel_class):
-    """dram bytes per launch from the committed ncu summary (profiles/), if present."""
+    """(dram bytes per launch, source note) from the committed ncu summary (profiles/), if present."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(kernel_class)
+        return d.get(kernel_class), d.get("_note")
     except Exception:
-        return None
+        return None, None
+
+
+# ------------------------------------------------------- per-config lines --
+EXTRAS = [("cfg1", "fp64"), ("cfg0", "fp32"), ("cfg2", "fp32"), ("cfg2", "fp64"), ("cfg3", "fp32"),
+          ("cfg3", "fp64"), ("cfg4_r2", "fp32"), ("cfg4_r2", "fp64"), ("cfg4_r4", "fp32"),
+          ("cfg4_r8", "fp32"), ("cfg4_r8", "fp64"), ("cfg4_r16", "fp32"), ("cfg4_r16", "fp64")]
+
+
+def measure_config(name, precision, steps, warmup, local, procs, peak):
+    """Device-resident img-iter/s of one BASELINE config on this GPU (same timing rules as
+    the headline: CUDA events per step, L2 flushed between steps, all images of the config)."""
+    import torch
+    from paper_1911_01234_b200 import vdamp
+    from paper_1911_01234_b200.plan import clear_plans
+    cfg = workload.CONFIGS[name]
+    w = workload.make_workload(cfg, procs=procs)
+    inp = vdamp.prepare_batch(w.ys, w.masks, w.pmap, w.noise_vars)
+    dev = torch.device("cuda", local)
+    rec = vdamp.BatchReconstructor(cfg.size, cfg.size, cfg.scales, cfg.batch, precision=precision, device=local)
+    cd = rec.plan.cdtype
+    y = torch.from_numpy(inp.y).to(dev, cd)
+    idx = torch.from_numpy(inp.indices).to(dev)
+    probs = torch.from_numpy(inp.probs).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    step = lambda: rec(y, idx, inp.counts, probs, inp.noise_var, cfg.n_iters, shared_probs=True, sync=False)
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.fill_(float(i))
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    rec.plan.measurement_status(wait=True)
+    ms = [a.elapsed_time(b) for a, b in evs]
+    value = cfg.batch * cfg.n_iters * steps / (sum(ms) / 1e3)
+    n_mean = float(np.mean(inp.counts))
+    b_c = 8 if precision == "fp32" else 16
+    b_iter = workload.algorithmic_bytes_per_image_iter(cfg.size * cfg.size, n_mean, b_c)
+    out = {"value": value, "unit": UNIT, "precision": precision, "images": cfg.batch, "n_iters": cfg.n_iters,
+           "steps": steps, "ms_per_step": float(np.mean(ms)),
+           "workload": f"{cfg.batch} x {cfg.size}^2, Haar s={cfg.scales}, R={cfg.undersampling:g}, "
+                       f"{cfg.snr_db:g} dB, {cfg.n_iters} iterations",
+           "iteration_roofline": {"B_iter_bytes": b_iter, "achieved_GBps": value * b_iter / 1e9,
+                                  "frac": value * b_iter / 1e9 / peak}}
+    del rec, y, idx, probs, flush
+    clear_plans()
+    torch.cuda.empty_cache()
+    return out
 
 
 # ------------------------------------------------------------------- main --
@@ -176,6 +239,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="print a short human summary instead of JSON")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the per-config lines (cfg0/2/3/4 and fp64) of a 1-GPU run")
+    ap.add_argument("--extras-steps", type=int, default=5)
     ap.add_argument("--with-trace", action="store_true",
                     help="time the production trace path: ground truth set, per-iteration NMSE + trace records")
     args = ap.parse_args()
@@ -191,8 +257,8 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        ns = max(4, min(cores, 64))
-        w = workload.make_workload(cfg, batch=min(ns, B))
+        ns = min(B, 64)                                  # the same slices as our arm (cfg1: all 64)
+        w = workload.make_workload(cfg, batch=ns, procs=cores)
         rates = []
         t_all = []
         rate, _ = cpu_oracle_rate(w, ns, cores, repeats=args.warmup)    # warm-up steps
@@ -208,8 +274,9 @@ def main():
             "data": "synthetic (seeded BASELINE workload generator)",
             "config": {"workload": f"{cfg.name}: {cfg.size}^2 complex, Haar s={cfg.scales}, R={cfg.undersampling:g}, "
                                    f"{cfg.snr_db:g} dB, {cfg.n_iters} iterations", "images_per_step": ns},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{ns} slices x {cfg.n_iters} iterations per step, one slice per process "
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
+                             "sample": f"{ns} slices x {cfg.n_iters} iterations per step (the first {ns} slices of "
+                                       f"our arm's batch), one slice per process "
                                        f"(oracle/vdamp_oracle.py, numpy float64)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }
@@ -222,9 +289,13 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ns = max(8, min(2 * cores, B))                     # ~0.55 s of CPU per slice: 10-30 s of work
         rate, ts = cpu_oracle_rate(w, ns, cores, repeats=1)
-        cpu_base = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+        n1 = 2
+        rate1, ts1 = cpu_oracle_rate(w, n1, 1, repeats=1)
+        cpu_base = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
                     "sample": f"{ns} of the {B} slices x {cfg.n_iters} iterations, one slice per process, "
-                              f"{cores} processes (oracle/vdamp_oracle.py, numpy float64), {ts[0]:.1f} s wall"}
+                              f"{cores} processes (oracle/vdamp_oracle.py, numpy float64), {ts[0]:.1f} s wall",
+                    "one_core": {"value": rate1, "unit": UNIT, "cores": 1,
+                                 "sample": f"{n1} slices x {cfg.n_iters} iterations in one process, {ts1[0]:.1f} s"}}
 
     import torch
     import torch.distributed as dist
@@ -264,7 +335,7 @@ def main():
     def step():
         if args.with_trace:
             plan.set_measurements(dev_in["y"], dev_in["indices"], dev_in["counts"], dev_in["probs"],
-                                  dev_in["noise_var"], True)
+                                  dev_in["noise_var"], True, sync_validation=False)
             return plan.run(cfg.n_iters, x_hat=rec._x, trace=trace_buf, nmse=nmse_buf)
         return rec(dev_in["y"], dev_in["indices"], dev_in["counts"], dev_in["probs"], dev_in["noise_var"],
                    cfg.n_iters, shared_probs=True, sync=False)
@@ -344,10 +415,69 @@ def main():
                "api": "StreamingReconstructor.submit (copies overlap the previous/next batch)",
                "sync_call_value": images_all * cfg.n_iters * args.steps / t_sync}
 
+    # ---- fixed batch sharded across the ranks (BASELINE cfg1/cfg4 wording) ----
+    # the config's batch (cfg1: 64 slices) split into contiguous slices, one per rank;
+    # each timed step reconstructs the rank's slice and gathers x_hat to rank 0
+    # (dist.gather over NCCL, the only collective) inside the timed region
+    fixed = None
+    if not args.with_trace:
+        from paper_1911_01234_b200.dist import gather_images, shard_range
+        Bf = cfg.batch
+        if world == 1 and B == Bf:
+            fixed = {"value": value, "ms_per_step": ms_per_step, "images": Bf,
+                     "note": "N=1: the headline steps themselves (no gather)"}
+        else:
+            lo, hi = shard_range(Bf, rank, world)
+            if hi > lo:
+                wf = workload.make_workload(cfg, batch=hi - lo, first=lo)
+                inf = vdamp.prepare_batch(wf.ys, wf.masks, wf.pmap, wf.noise_vars)
+                recf = vdamp.BatchReconstructor(cfg.size, cfg.size, cfg.scales, hi - lo, precision=args.precision,
+                                                device=local)
+                fin = dict(y=torch.from_numpy(inf.y).to(dev, cd), indices=torch.from_numpy(inf.indices).to(dev),
+                           probs=torch.from_numpy(inf.probs).to(dev))
+                fstep = lambda: recf(fin["y"], fin["indices"], inf.counts, fin["probs"], inf.noise_var, cfg.n_iters,
+                                     shared_probs=True, sync=False)
+            else:
+                fstep = lambda: torch.empty((0, cfg.size, cfg.size), dtype=cd, device=dev)
+
+            def fstep_gather():
+                x = fstep()
+                return gather_images(x, Bf) if world > 1 else x
+            for _ in range(args.warmup):
+                fstep_gather()
+            torch.cuda.synchronize(dev)
+            fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+            barrier()
+            for i in range(args.steps):
+                flush.fill_(float(i))
+                fev[i][0].record(stream)
+                fstep_gather()
+                fev[i][1].record(stream)
+            torch.cuda.synchronize(dev)
+            barrier()
+            tf = max_over_ranks(sum(a.elapsed_time(b) for a, b in fev) / 1e3)
+            fixed = {"value": Bf * cfg.n_iters * args.steps / tf, "ms_per_step": 1e3 * tf / args.steps, "images": Bf,
+                     "gather": "dist.gather of x_hat to rank 0 inside the timed region" if world > 1 else "none (N=1)"}
+        fixed.update(unit=UNIT, scaling="strong",
+                     workload=f"{cfg.name}: {Bf} x {cfg.size}^2 slices in total, contiguous slice per rank")
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
+
+    # ---- the other BASELINE configs and the fp64 parity mode (1 GPU) ----
+    peak, peak_src = measured_peak()
+    extras = None
+    if world == 1 and not args.no_extras and not args.with_trace and args.config == "cfg1" and args.batch is None:
+        extras = {}
+        for name, prec in EXTRAS:
+            if name == cfg.name and prec == args.precision:
+                continue
+            try:
+                extras[f"{name}_{prec}"] = measure_config(name, prec, args.extras_steps, 3, local, cores, peak)
+            except Exception as e:          # report, never hide a failure
+                extras[f"{name}_{prec}"] = {"error": f"{type(e).__name__}: {e}"}
 
     # ---- roofline of the dominant kernel class -----------------------
     N = cfg.size * cfg.size
@@ -355,11 +485,10 @@ def main():
     b_c = 8 if args.precision == "fp32" else 16
     cb = class_bytes(cfg, N, n_mean, B, cfg.n_iters * args.steps, b_c)
     cb["finalize"] *= args.steps
-    peak, peak_src = measured_peak()
     dom = max((k for k in cb), key=lambda k: ktimes[k][0])
     kms, kl = ktimes[dom]
     achieved = cb[dom] / (kms / 1e3) / 1e9
-    traffic = traffic_from_profiles(dom)
+    traffic, traffic_src = traffic_from_profiles(dom)
     kernels = {k: {"ms_per_step": ktimes[k][0] / args.steps, "launches_per_step": ktimes[k][1] / args.steps,
                    "GBps": (cb[k] / (ktimes[k][0] / 1e3) / 1e9) if ktimes[k][0] > 0 and k in cb else None}
                for k in ktimes}
@@ -376,7 +505,8 @@ def main():
                    "trace": "ground truth + per-iteration NMSE/trace records" if args.with_trace else "off (as the CPU timing)",
                    "parallelism": f"images sharded, {world} process(es), 1 GPU each, no collective"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": cb[dom] / max(kl, 1),
                      "avg_launch_ms": kms / max(kl, 1)},
         "iteration_roofline": {"B_iter_bytes": b_iter, "achieved_GBps": value / world * b_iter / 1e9,
@@ -387,6 +517,10 @@ def main():
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if fixed is not None:
+        line["fixed_batch"] = fixed
+    if extras is not None:
+        line["configs"] = extras
     if cpu_base is not None:
         line["cpu_baseline"] = cpu_base
     if args.quick:

@@ -95,6 +95,24 @@ VDAMP_API int vdamp_plan_workspace_bytes(vdamp_plan_t plan, size_t* bytes);
 VDAMP_API int vdamp_set_measurements(vdamp_plan_t plan, const void* y, const int64_t* indices,
                            const int64_t* counts, const double* probs,
                            int64_t probs_batch_stride, const double* noise_var, void* stream);
+/* Validation of the measurements (the reference raises ValueError for a bad
+ * mask or density: src/fourier.py:65-74, src/sampling.py:45-46).  The
+ * scatter kernel skips an index outside [0, H*W) and flags it, a repeated
+ * index and a probability outside (0, 1] at a sampled point; the flags are
+ * reported as VDAMP_ERR_ARG.  synchronous = 1 (default): vdamp_set_measurements
+ * waits for the check and returns the error itself.  synchronous = 0 (the
+ * pipelined serving path): the flags are read back asynchronously and
+ * reported by the first later call on the plan that finds them landed, or by
+ * vdamp_measurement_status. */
+VDAMP_API int vdamp_set_validation(vdamp_plan_t plan, int synchronous);
+/* VDAMP_ERR_ARG if any measurements set so far were flagged; wait = 1 blocks
+ * until the last check has landed, wait = 0 reports only what has. */
+VDAMP_API int vdamp_measurement_status(vdamp_plan_t plan, int wait);
+/* Host-side check of HOST arrays before any upload (no device needed): the same
+ * rules as the kernel plus counts in [1, H*W] and noise_var >= 0. */
+VDAMP_API int vdamp_check_measurements(int height, int width, int batch, const int64_t* indices,
+                                       const int64_t* counts, const double* probs,
+                                       int64_t probs_batch_stride, const double* noise_var);
 /* Ground truth images (complex, batch x H x W): enables the per-iteration
  * NMSE / subband NMSE records (src/vdamp.py:189-193). NULL disables. */
 VDAMP_API int vdamp_set_ground_truth(vdamp_plan_t plan, const void* x0, void* stream);

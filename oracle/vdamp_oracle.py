@@ -408,9 +408,19 @@ class Result:
     steps: list = field(default_factory=list)
 
 
+def _round_c64(v):
+    return v.astype(np.complex64).astype(np.complex128)
+
+
 def run(y, idx, probs, noise_var, scales, n_iters, ground_truth=None,
-        keep_r_iters=(), keep_steps=False) -> Result:
-    """The reconstruction loop (src/vdamp.py:153-197)."""
+        keep_r_iters=(), keep_steps=False, c64_state=False) -> Result:
+    """The reconstruction loop (src/vdamp.py:153-197).
+
+    ``c64_state=True`` is the complex64 floor of SURVEY A.3 (not a reference
+    mode): the iteration state r~_{k+1} and w_hat_k are rounded to complex64
+    after every iteration, everything else stays float64.  The distance of
+    this run from the plain run is the deviation that storing the state in
+    complex64 alone causes; the fp32 CUDA path is judged against it."""
     if n_iters < 1:
         raise ValueError(f"need at least one iteration, got {n_iters}")
     p = Problem(np.asarray(y, dtype=np.complex128), np.asarray(idx), np.asarray(probs, float),
@@ -421,6 +431,9 @@ def run(y, idx, probs, noise_var, scales, n_iters, ground_truth=None,
     st = None
     for k in range(n_iters):
         st = step(p, rt)
+        if c64_state:
+            st.r_tilde = _round_c64(st.r_tilde)
+            st.w_hat = _round_c64(st.w_hat)
         rec = Record(k, st.tau.copy(), st.thresholds.copy(), st.lambdas.copy(),
                      st.alpha.copy(), st.clamped)
         if ground_truth is not None:

@@ -57,6 +57,9 @@ SIGNATURES = {
     "vdamp_mc_accumulate": (_I, [_P, _P, _P, _P, _P, _P, _P]),
     "vdamp_baseline_run": (_I, [_P, _I, _I, _P, _P, _P, _P, _P]),
     "vdamp_launch_count": (_I, [_P, _I64P, _I]),
+    "vdamp_set_validation": (_I, [_P, _I]),
+    "vdamp_measurement_status": (_I, [_P, _I]),
+    "vdamp_check_measurements": (_I, [_I, _I, _I, _I64P, _I64P, _DP, ctypes.c_int64, _DP]),
 }
 
 _lib = None

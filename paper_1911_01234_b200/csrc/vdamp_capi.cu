@@ -103,15 +103,28 @@ struct Plan {
     cudaStream_t gstream = nullptr; // capture/launch stream when the caller passes the legacy default stream
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    // image lanes: vdamp_run (throughput path: no trace / NMSE / snapshots) runs
-    // the batch as `lanes` contiguous image ranges on their own streams, so one
-    // lane's latency-bound SURE tail overlaps the FFT kernels of the others
+    // image lanes: vdamp_run runs the batch as `lanes` contiguous image ranges on
+    // their own streams, so one lane's latency-bound SURE tail overlaps the FFT
+    // kernels of the others; diagnostics ride on the lanes when interleaved
     int lanes = 1;
     struct Lane { cudaStream_t st = nullptr, side = nullptr; cudaEvent_t fork = nullptr, join = nullptr, done = nullptr; };
     std::vector<Lane> lane;
     cudaEvent_t lane_start = nullptr;
     bool have_meas = false;
     bool have_gt = false;
+    // measurement validation (scatter_measurements flags, sticky until reported):
+    // device word, its pinned host copy and the event after the copy
+    unsigned* d_merr = nullptr;
+    unsigned* h_merr = nullptr;     // mapped pinned host word
+    unsigned* h_merr_dev = nullptr; // its device alias
+    cudaEvent_t ev_meas = nullptr;
+    bool meas_pending = false;
+    bool validate_sync = true;      // vdamp_set_validation
+    // pinned staging of the per-call host arrays (noise variances, offsets), two
+    // slots so a call never overwrites a slot whose copy may still be queued
+    double* h_stage[2] = {nullptr, nullptr};
+    cudaEvent_t ev_stage[2] = {nullptr, nullptr};
+    int stage_k = 0;
     size_t bytes = 0;
     long long launches = 0;
     // timing
@@ -695,7 +708,43 @@ void free_plan(Plan* p) {
     }
     if (p->lane_start) cudaEventDestroy(p->lane_start);
     if (p->ev_join) cudaEventDestroy(p->ev_join);
+    if (p->d_merr) cudaFree(p->d_merr);
+    if (p->h_merr) cudaFreeHost(p->h_merr);
+    if (p->ev_meas) cudaEventDestroy(p->ev_meas);
+    for (int i = 0; i < 2; ++i) {
+        if (p->h_stage[i]) cudaFreeHost(p->h_stage[i]);
+        if (p->ev_stage[i]) cudaEventDestroy(p->ev_stage[i]);
+    }
     delete p;
+}
+
+std::string meas_message(unsigned f) {
+    std::string m;
+    if (f & MEAS_RANGE) m += "sampled index outside [0, height*width)";
+    if (f & MEAS_DUP) m += std::string(m.empty() ? "" : "; ") + "repeated sampled index";
+    if (f & MEAS_PROB) m += std::string(m.empty() ? "" : "; ") + "sampling probability outside (0, 1] at a sampled point";
+    return m;
+}
+
+// Report the flags of the measurements set so far (VDAMP_ERR_ARG).  wait = false
+// only looks if the last check has already landed (never blocks the host).
+void check_meas(Plan* p, bool wait) {
+    if (!p->meas_pending) return;
+    if (wait) {
+        CK(cudaEventSynchronize(p->ev_meas));
+    } else {
+        const cudaError_t q = cudaEventQuery(p->ev_meas);
+        if (q == cudaErrorNotReady) return;
+        CK(q);
+    }
+    p->meas_pending = false;
+    const unsigned f = *(volatile unsigned*)p->h_merr;
+    if (f) {
+        *(volatile unsigned*)p->h_merr = 0;
+        CK(cudaMemset(p->d_merr, 0, sizeof(unsigned)));
+        p->have_meas = false;
+        throw Err{VDAMP_ERR_ARG, meas_message(f)};
+    }
 }
 
 }  // namespace
@@ -849,6 +898,16 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
         set_lanes(p, default_lanes(batch));
+        p->d_merr = (unsigned*)dalloc(p, sizeof(unsigned));
+        CK(cudaMemset(p->d_merr, 0, sizeof(unsigned)));
+        CK(cudaHostAlloc((void**)&p->h_merr, sizeof(unsigned), cudaHostAllocMapped));
+        *p->h_merr = 0;
+        CK(cudaHostGetDevicePointer((void**)&p->h_merr_dev, p->h_merr, 0));
+        CK(cudaEventCreateWithFlags(&p->ev_meas, cudaEventDisableTiming));
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaHostAlloc((void**)&p->h_stage[i], (size_t)(2 * batch + 1) * sizeof(double), cudaHostAllocDefault));
+            CK(cudaEventCreateWithFlags(&p->ev_stage[i], cudaEventDisableTiming));
+        }
         CK(cudaMemset(p->yg, 0, img * cs));
         CK(cudaMemset(p->pinv, 0, img * rs));
         if (precision == VDAMP_FP32) {
@@ -897,42 +956,97 @@ int vdamp_set_measurements(vdamp_plan_t plan, const void* y, const int64_t* indi
     return guard([&] {
         Plan* p = P(plan);
         if (!y || !indices || !counts || !probs || !noise_var) throw Err{VDAMP_ERR_ARG, "null measurement pointer"};
-        std::vector<long long> offs(p->B + 1, 0);
+        if (probs_batch_stride != 0 && probs_batch_stride != p->N)
+            throw Err{VDAMP_ERR_ARG, "probs_batch_stride must be 0 (shared map) or height*width"};
+        check_meas(p, false);                          // flags of an earlier call that have landed
         long long maxn = 0;
         for (int b = 0; b < p->B; ++b) {
             if (counts[b] < 1 || counts[b] > p->N) throw Err{VDAMP_ERR_ARG, "mask selects no samples or too many"};
-            if (noise_var[b] < 0) throw Err{VDAMP_ERR_ARG, "noise variance must be >= 0"};
-            offs[b + 1] = offs[b] + counts[b];
+            if (!(noise_var[b] >= 0)) throw Err{VDAMP_ERR_ARG, "noise variance must be >= 0"};
             maxn = std::max(maxn, (long long)counts[b]);
         }
         CK(cudaSetDevice(p->dev));
         cudaStream_t st = (cudaStream_t)stream;
+        // pinned staging slot (its previous copies must have left the host buffer)
+        const int slot = p->stage_k++ & 1;
+        CK(cudaEventSynchronize(p->ev_stage[slot]));
+        double* nv = p->h_stage[slot];
+        long long* offs = reinterpret_cast<long long*>(nv + p->B);
+        offs[0] = 0;
+        for (int b = 0; b < p->B; ++b) { nv[b] = noise_var[b]; offs[b + 1] = offs[b] + counts[b]; }
         const size_t img = (size_t)p->B * p->N;
         const size_t rs = p->prec == VDAMP_FP32 ? sizeof(float) : sizeof(double);
         CK(cudaMemsetAsync(p->yg, 0, img * p->csz, st));
         CK(cudaMemsetAsync(p->pinv, 0, img * rs, st));
-        // pageable host sources are staged before cudaMemcpyAsync returns, so the
-        // locals above may die right after; no stream synchronisation needed
-        CK(cudaMemcpyAsync(p->nvar, noise_var, p->B * sizeof(double), cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(p->offs, offs.data(), (p->B + 1) * sizeof(long long), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(p->nvar, nv, p->B * sizeof(double), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(p->offs, offs, (p->B + 1) * sizeof(long long), cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(p->ev_stage[slot], st));
         dim3 grid((unsigned)std::min<long long>((maxn + 255) / 256, 1024), p->B);
         {
             Launch L(p, 5, st);
             if (p->prec == VDAMP_FP32)
                 scatter_measurements<float><<<grid, 256, 0, st>>>(p->geo, (const float2*)y, (const long long*)indices,
                                                                   p->offs, probs, probs_batch_stride, (float2*)p->yg,
-                                                                  (float*)p->pinv);
+                                                                  (float*)p->pinv, p->d_merr);
             else
                 scatter_measurements<double><<<grid, 256, 0, st>>>(p->geo, (const double2*)y, (const long long*)indices,
                                                                    p->offs, probs, probs_batch_stride, (double2*)p->yg,
-                                                                   (double*)p->pinv);
+                                                                   (double*)p->pinv, p->d_merr);
         }
         if (p->pend != cudaSuccess) {
             cudaError_t e = p->pend;
             p->pend = cudaSuccess;
             throw Err{VDAMP_ERR_CUDA, std::string("scatter_measurements: ") + cudaGetErrorString(e)};
         }
+        {
+            Launch L(p, 5, st);
+            publish_flags<<<1, 1, 0, st>>>(p->d_merr, p->h_merr_dev);
+        }
+        CK(cudaEventRecord(p->ev_meas, st));
+        p->meas_pending = true;
         p->have_meas = true;
+        if (p->validate_sync) check_meas(p, true);
+    });
+}
+
+int vdamp_set_validation(vdamp_plan_t plan, int synchronous) {
+    return guard([&] { P(plan)->validate_sync = synchronous != 0; });
+}
+
+int vdamp_measurement_status(vdamp_plan_t plan, int wait) {
+    return guard([&] {
+        Plan* p = P(plan);
+        CK(cudaSetDevice(p->dev));
+        check_meas(p, wait != 0);
+    });
+}
+
+int vdamp_check_measurements(int height, int width, int batch, const int64_t* indices, const int64_t* counts,
+                             const double* probs, int64_t probs_batch_stride, const double* noise_var) {
+    return guard([&] {
+        if (height < 1 || width < 1 || batch < 1) throw Err{VDAMP_ERR_ARG, "height, width and batch must be >= 1"};
+        if (!indices || !counts || !probs || !noise_var) throw Err{VDAMP_ERR_ARG, "null measurement pointer"};
+        const long long N = (long long)height * width;
+        if (probs_batch_stride != 0 && probs_batch_stride != N)
+            throw Err{VDAMP_ERR_ARG, "probs_batch_stride must be 0 (shared map) or height*width"};
+        std::vector<unsigned char> seen((size_t)N);
+        long long o = 0;
+        unsigned f = 0;
+        for (int b = 0; b < batch; ++b) {
+            if (counts[b] < 1 || counts[b] > N) throw Err{VDAMP_ERR_ARG, "mask selects no samples or too many"};
+            if (!(noise_var[b] >= 0)) throw Err{VDAMP_ERR_ARG, "noise variance must be >= 0"};
+            std::fill(seen.begin(), seen.end(), 0);
+            for (long long e = 0; e < counts[b]; ++e) {
+                const long long gi = indices[o + e];
+                if (gi < 0 || gi >= N) { f |= MEAS_RANGE; continue; }
+                if (seen[(size_t)gi]) f |= MEAS_DUP;
+                seen[(size_t)gi] = 1;
+                const double pr = probs[(long long)b * probs_batch_stride + gi];
+                if (!(pr > 0.0 && pr <= 1.0)) f |= MEAS_PROB;
+            }
+            o += counts[b];
+        }
+        if (f) throw Err{VDAMP_ERR_ARG, meas_message(f)};
     });
 }
 
@@ -1008,15 +1122,16 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
     return guard([&] {
         Plan* p = P(plan);
         if (n_iters < 1) throw Err{VDAMP_ERR_ARG, "need at least one iteration, got " + std::to_string(n_iters)};
+        check_meas(p, false);
         if (!p->have_meas) throw Err{VDAMP_ERR_STATE, "vdamp_set_measurements must be called first"};
         if (nmse && !p->have_gt) throw Err{VDAMP_ERR_STATE, "NMSE trace requested without ground truth"};
         if (!x_hat) throw Err{VDAMP_ERR_ARG, "null x_hat"};
         cudaStream_t caller = (cudaStream_t)stream;
         cudaStream_t st = caller;
-        // image lanes (throughput path: no trace, NMSE or snapshots), forked from and
-        // joined back into stream cs; also captured into the graph below
-        // diagnostics (trace, NMSE, snapshots) ride on the lanes in iteration-major order:
-        // each lane writes its image range of every per-iteration record
+        // image lanes, forked from and joined back into stream cs (also captured into
+        // the graph below); diagnostics (trace, NMSE, snapshots) ride on the lanes when
+        // they are interleaved (iteration-major): each lane writes its image range of
+        // every per-iteration record
         const bool use_lanes = p->lanes > 1 && (p->interleave || (!trace && !nmse && !snapshots));
         auto run_lanes = [&](cudaStream_t cs) {
             CK(cudaSetDevice(p->dev));
@@ -1180,6 +1295,7 @@ int vdamp_iterate(vdamp_plan_t plan, const void* r_tilde, void* r, void* r_tilde
                   void* stream) {
     return guard([&] {
         Plan* p = P(plan);
+        check_meas(p, false);
         if (!p->have_meas) throw Err{VDAMP_ERR_STATE, "vdamp_set_measurements must be called first"};
         if (!r_tilde) throw Err{VDAMP_ERR_ARG, "null r_tilde"};
         dispatch(p, stream, [&](auto& s) {
@@ -1238,6 +1354,7 @@ int vdamp_fft2c(vdamp_plan_t plan, const void* in, void* out, int inverse, void*
 int vdamp_finalize(vdamp_plan_t plan, const void* w_hat, void* x_hat, void* stream) {
     return guard([&] {
         Plan* p = P(plan);
+        check_meas(p, false);
         if (!p->have_meas) throw Err{VDAMP_ERR_STATE, "vdamp_set_measurements must be called first"};
         dispatch(p, stream, [&](auto& s) {
             typedef typename std::remove_reference<decltype(s)>::type S_;
@@ -1304,6 +1421,7 @@ int vdamp_baseline_run(vdamp_plan_t plan, int algorithm, int n_iters, const doub
         Plan* p = P(plan);
         if (algorithm != 0 && algorithm != 1) throw Err{VDAMP_ERR_ARG, "algorithm must be 0 (fista) or 1 (sure_it)"};
         if (n_iters < 1) throw Err{VDAMP_ERR_ARG, "need at least one iteration"};
+        check_meas(p, false);
         if (!p->have_meas) throw Err{VDAMP_ERR_STATE, "vdamp_set_measurements must be called first"};
         if (algorithm == 0 && !lam) throw Err{VDAMP_ERR_ARG, "fista requires lam"};
         if ((algorithm == 1 || nmse || trace) && !p->have_gt)

@@ -3096,21 +3096,45 @@ __global__ void apply_params(Geo g, const typename CT<R>::T* in, typename CT<R>:
 }
 
 // y on the grid with the centred-FFT sign folded in, and 1/p (0 off mask).
+// Guards for raw C callers (the reference raises ValueError for these,
+// src/fourier.py:65-74, src/sampling.py:45-46): an index outside [0, N) is
+// skipped, a repeated index or a probability outside (0, 1] at a sampled
+// point is flagged; the flags (MEAS_*) are OR-ed into *err and reported by
+// the host as VDAMP_ERR_ARG.  pinv is zero before the scatter, so a
+// non-zero previous value marks a duplicate.
+constexpr unsigned MEAS_RANGE = 1u, MEAS_DUP = 2u, MEAS_PROB = 4u;
+
+__device__ __forceinline__ float xchg_pinv(float* a, float v) { return atomicExch(a, v); }
+__device__ __forceinline__ double xchg_pinv(double* a, double v) {
+    return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long*>(a),
+                                                      (unsigned long long)__double_as_longlong(v)));
+}
+
 template <typename R>
 __global__ void scatter_measurements(Geo g, const typename CT<R>::T* y, const long long* idx,
                                      const long long* offs, const double* probs, long long pstride,
-                                     typename CT<R>::T* yg, R* pinv) {
+                                     typename CT<R>::T* yg, R* pinv, unsigned* err) {
     const int bi = blockIdx.y;
     const long long o0 = offs[bi], n = offs[bi + 1] - o0;
+    unsigned bad = 0;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
         const long long gi = idx[o0 + e];
+        if (gi < 0 || gi >= g.N) { bad |= MEAS_RANGE; continue; }
         const int k1 = (int)(gi >> g.logW), k2 = (int)(gi & (g.W - 1));
         typename CT<R>::T v = y[o0 + e];
         if ((k1 + k2) & 1) { v.x = -v.x; v.y = -v.y; }
+        const double pr = probs[(long long)bi * pstride + gi];
+        if (!(pr > 0.0 && pr <= 1.0)) bad |= MEAS_PROB;
         yg[(long long)bi * g.N + gi] = v;
-        pinv[(long long)bi * g.N + gi] = (R)(1.0 / probs[(long long)bi * pstride + gi]);
+        if (xchg_pinv(pinv + (long long)bi * g.N + gi, (R)(1.0 / pr)) != (R)0) bad |= MEAS_DUP;
     }
+    if (bad) atomicOr(err, bad);
 }
+
+// copy the sticky measurement flags into mapped pinned host memory: a kernel store,
+// not a DMA copy, so the compute stream never queues behind a large device-to-host
+// transfer on the copy engine (the pipelined serving path overlaps those)
+__global__ void publish_flags(const unsigned* d, volatile unsigned* h) { *h = *d; }
 
 template <typename R>
 __global__ void fill_identity_params(double* par, int count) {

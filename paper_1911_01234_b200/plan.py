@@ -103,10 +103,19 @@ class Plan:
             t = torch.from_numpy(np.ascontiguousarray(a))
         return t.to(device=self.device, dtype=dtype, non_blocking=True).contiguous()
 
-    def set_measurements(self, y, indices, counts, probs, noise_var, shared_probs=False, stream=None):
+    def set_measurements(self, y, indices, counts, probs, noise_var, shared_probs=False, stream=None,
+                         sync_validation=True):
         """y: concatenated (sum n_b,) complex; indices int64 same length;
-        counts (B,); probs (B,H,W) or (H,W) when shared_probs; noise_var (B,)."""
+        counts (B,); probs (B,H,W) or (H,W) when shared_probs; noise_var (B,).
+
+        The device checks every index (range, repeats) and the probability at it;
+        a flagged batch raises ValueError here (``sync_validation``) or, on the
+        pipelined path (``sync_validation=False``), from the first later call that
+        finds the check landed, or from :meth:`measurement_status`."""
         torch = _torch()
+        if sync_validation != getattr(self, "_sync_val", True):
+            _lib.check(_lib.load().vdamp_set_validation(self.handle, int(bool(sync_validation))))
+        self._sync_val = bool(sync_validation)
         y_d = self.to_device(y, self.cdtype)
         i_d = self.to_device(indices, torch.int64)
         p_d = self.to_device(probs, torch.float64)
@@ -125,6 +134,10 @@ class Plan:
             nv.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _lib.stream_ptr(stream)))
         self._keep = (y_d, i_d, p_d)
         self.has_measurements = True
+
+    def measurement_status(self, wait=True):
+        """Raise ValueError if any measurements set so far were flagged by the device check."""
+        _lib.check(_lib.load().vdamp_measurement_status(self.handle, int(bool(wait))))
 
     def set_ground_truth(self, x0, stream=None):
         if x0 is None:
@@ -188,7 +201,9 @@ class Plan:
         _lib.check(_lib.load().vdamp_set_graphs(self.handle, int(bool(enable))))
 
     def set_lanes(self, lanes: int):
-        """Run the batch as `lanes` image ranges on their own streams (throughput path; 0 = default)."""
+        """Run the batch as `lanes` image ranges on their own streams (0 = default).  With the
+        default iteration-major launch order the trace, NMSE records and snapshots ride on
+        the lanes too (each lane writes its image range)."""
         _lib.check(_lib.load().vdamp_set_lanes(self.handle, int(lanes)))
 
     def launch_count(self, reset=False) -> int:

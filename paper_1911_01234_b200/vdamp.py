@@ -288,7 +288,8 @@ class BatchReconstructor:
         if n_iters < 1:
             raise ValueError(f"need at least one iteration, got {n_iters}")
         p = self.plan
-        p.set_measurements(y, indices, counts, probs, noise_var, shared_probs, stream=stream)
+        p.set_measurements(y, indices, counts, probs, noise_var, shared_probs, stream=stream,
+                           sync_validation=False)
         x = p.run(n_iters, x_hat=self._x, stream=stream)
         if out is not None:
             out.copy_(x, non_blocking=True)
@@ -296,6 +297,7 @@ class BatchReconstructor:
         if sync:
             import torch
             torch.cuda.current_stream(p.device).synchronize() if stream is None else stream.synchronize()
+            p.measurement_status(wait=True)
         return x
 
 
@@ -345,7 +347,7 @@ class StreamingReconstructor:
         self.compute.wait_event(ev_in)
         with torch.cuda.stream(self.compute):
             p.set_measurements(st["y"], st["indices"], host["counts"], st["probs"], host["noise_var"],
-                               host.get("shared_probs", True), stream=self.compute)
+                               host.get("shared_probs", True), stream=self.compute, sync_validation=False)
             p.run(n_iters, x_hat=self._x[s], stream=self.compute)
             ev_done = torch.cuda.Event()
             ev_done.record(self.compute)
@@ -358,6 +360,9 @@ class StreamingReconstructor:
         return out
 
     def wait(self):
+        """Block until every submitted batch has landed; raises ValueError if the
+        device flagged the measurements of any of them."""
         for e in self._ev_out:
             if e is not None:
                 e.synchronize()
+        self.plan.measurement_status(wait=True)

@@ -76,15 +76,31 @@ def make_slice(cfg: Config, pmap: ProbabilityMap, b: int, seed: int = DEFAULT_SE
     return x0, mask, k.values.astype(np.complex64), float(k.noise_var)
 
 
-def make_workload(name_or_cfg, batch: int | None = None, seed: int = DEFAULT_SEED, first: int = 0) -> Workload:
-    """Slices [first, first + batch) of a configuration (default: the whole batch)."""
+_JOB = None          # (cfg, pmap, seed) of the pool in flight (inherited by the forked workers)
+
+
+def _slice_job(b):
+    cfg, pmap, seed = _JOB
+    return make_slice(cfg, pmap, b, seed)
+
+
+def make_workload(name_or_cfg, batch: int | None = None, seed: int = DEFAULT_SEED, first: int = 0,
+                  procs: int = 1) -> Workload:
+    """Slices [first, first + batch) of a configuration (default: the whole batch).
+    ``procs`` > 1 generates the slices in that many forked processes (same result)."""
     cfg = CONFIGS[name_or_cfg] if isinstance(name_or_cfg, str) else name_or_cfg
     n = cfg.batch if batch is None else int(batch)
     pmap = density(cfg)
-    xs, masks, ys, nvs = [], [], [], []
-    for b in range(first, first + n):
-        x0, m, y, nv = make_slice(cfg, pmap, b, seed)
-        xs.append(x0); masks.append(m); ys.append(y); nvs.append(nv)
+    global _JOB
+    _JOB = (cfg, pmap, seed)
+    jobs = list(range(first, first + n))
+    if procs > 1 and n > 8:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(min(procs, n)) as pool:
+            res = pool.map(_slice_job, jobs, chunksize=max(1, n // (4 * procs)))
+    else:
+        res = [_slice_job(j) for j in jobs]
+    xs, masks, ys, nvs = (list(v) for v in zip(*res))
     return Workload(cfg, pmap, masks, ys, np.array(nvs), np.stack(xs), list(range(first, first + n)))
 
 

@@ -230,8 +230,45 @@ def cli_golden():
     np.savez_compressed(os.path.join(OUT, "cli.npz"), **d)
 
 
+def bench512_golden():
+    """The reference's own benchmark fixture (tests/conftest.py:101-132 of the
+    reference): Shepp-Logan 512^2, Haar s=4, polynomial density (d=8, centre
+    0.02, R=8), mask seed 3, noise seed 103, 40 dB, 30 iterations with ground
+    truth.  Its recorded result is -35.5 dB at iteration 30 (test_output.txt).
+    The inputs are regenerated at test time by paper_1911_01234_b200.sampling
+    (pinned bit-exact here through the mask bits, y checksums and noise_var);
+    x_hat is stored on a stride-8 grid plus 16 random projections."""
+    sys.path.insert(0, REF)
+    from csmri import vdamp
+    from csmri.sampling import draw_mask, polynomial_pmap, shepp_logan, synthesize
+    size, scales, n_iters = 512, 4, 30
+    x0 = shepp_logan(size, size)
+    pmap = polynomial_pmap(size, size, 8, 0.02, 8.0)
+    mask = draw_mask(pmap, 3)
+    kd = synthesize(x0, mask, 40.0, 103)
+    x_hat, trace = vdamp.run(kd.values, mask, pmap, kd.noise_var, scales, n_iters, ground_truth=x0)
+    proj = np.random.default_rng(512).normal(size=(16, size * size))
+    np.savez_compressed(
+        os.path.join(OUT, "bench512.npz"),
+        mask_bits=np.packbits(mask.sampled.ravel()), n=np.array(mask.n),
+        y_sum=np.array([kd.values.real.sum(), kd.values.imag.sum()]), y_norm=np.array(np.linalg.norm(kd.values)),
+        noise_var=np.array(kd.noise_var), scales=np.array(scales), n_iters=np.array(n_iters),
+        x_hat_grid=x_hat[::8, ::8], x_hat_norm=np.array(np.linalg.norm(x_hat)),
+        x_hat_proj=proj @ x_hat.ravel(), proj_seed=np.array(512),
+        nmse_db=trace.nmse_curve(),
+        tau=np.array([r.tau for r in trace.records]),
+        thresholds=np.array([r.thresholds for r in trace.records]),
+        alphas=np.array([r.alphas for r in trace.records]),
+        clamped=np.array([r.alpha_clamped for r in trace.records]),
+        subband_nmse_db=np.array([r.subband_nmse_db for r in trace.records]),
+    )
+    print("bench512: nmse at iteration 30 =", trace.nmse_curve()[-1])
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["cli"]:
         cli_golden()
+    elif sys.argv[1:] == ["bench512"]:
+        bench512_golden()
     else:
         main()

@@ -87,11 +87,12 @@ def _tricky_coeffs(rng, n, kind):
     return r
 
 
-@pytest.mark.parametrize("shape", [(64, 64, 3), (256, 256, 4), (512, 512, 2)])
+@pytest.mark.parametrize("shape", [(64, 64, 3), (256, 256, 4), (512, 512, 2), (1024, 1024, 1), (1024, 1024, 6)])
 @pytest.mark.parametrize("kind", ["gauss", "ties", "zeros", "sparse", "diverged"])
 def test_sure_select_vs_oracle(oracle, shape, kind):
-    """Exact SURE argmin incl. ties, zeros, interior points; 512x512 s=2 has 65,536-entry
-    subbands (multi-tile merge path)."""
+    """Exact SURE argmin (fp64 path) incl. ties, zeros, interior points; 512x512 s=2 has
+    65,536-entry subbands (multi-tile merge path), 1024x1024 s=1 / s=6 262,144-entry ones
+    (cfg3 geometry: the global counting sort over 64-bit keys)."""
     from paper_1911_01234_b200 import denoise, wavelet
     h, w, s = shape
     rng = np.random.default_rng(hash((shape, kind)) % 2**32)
@@ -237,3 +238,18 @@ def test_sure_select_fp32_large_subbands(oracle, shape, kind, monkeypatch):
             assert r_g <= r_o + 1e-10 * abs(r_o), (env, jb, t_g[jb], t_o[jb])
         if kind != "diverged":
             assert same.all(), env
+
+
+def test_reference_benchmark_512():
+    """The reference's own 512^2 benchmark (Shepp-Logan, s=4, R=8, 40 dB, 30 iterations,
+    mask seed 3 / noise seed 103): fp64 tracks the reference run to round-off; fp32 within
+    the north-star NMSE bar at every iteration."""
+    from conftest import bench512_check, bench512_inputs
+    from paper_1911_01234_b200 import vdamp
+    g, x0, pmap, mask, kd = bench512_inputs()
+    x, tr = vdamp.run(kd.values, mask, pmap, kd.noise_var, 4, 30, ground_truth=x0, precision="fp64")
+    nm = bench512_check(g, x, tr.records, 1e-8, 1e-6, 1e-8)
+    assert round(nm[-1], 1) == -35.5
+    x32, tr32 = vdamp.run(kd.values, mask, pmap, kd.noise_var, 4, 30, ground_truth=x0, precision="fp32")
+    assert np.abs(tr32.nmse_curve() - g["nmse_db"]).max() <= 0.05
+    assert rel2(x32, x) <= 1e-2

@@ -308,19 +308,25 @@ def test_rectangular_geometries_fp64_vs_oracle(oracle, h, w, scales):
     assert dn <= 1e-6, dn
 
 
-def test_lanes_with_diagnostics_bitwise_equal(monkeypatch):
+@pytest.mark.parametrize("precision,parseval,graphs", [("fp32", "1", "0"), ("fp32", "0", "0"), ("fp32", "1", "1"),
+                                                      ("fp32", "0", "1"), ("fp64", "1", "0"), ("fp64", "0", "1")])
+def test_lanes_with_diagnostics_bitwise_equal(monkeypatch, precision, parseval, graphs):
     """Image lanes also carry the trace, the per-iteration NMSE and the r snapshots
-    (each lane writes its image range of every record): bitwise the same as one lane."""
+    (each lane writes its image range of every record): bitwise the same as one lane,
+    with the Parseval NMSE pass or the finalize path (VDAMP_PARSEVAL=0, per-lane xtmp / x0
+    offsets), and with the lane fork/join captured into a CUDA graph (VDAMP_GRAPHS=1)."""
     import dataclasses
     from paper_1911_01234_b200 import vdamp, workload
     from paper_1911_01234_b200.plan import clear_plans
     w = workload.make_workload("cfg1", batch=32)
+    monkeypatch.setenv("VDAMP_PARSEVAL", parseval)
+    monkeypatch.setenv("VDAMP_GRAPHS", graphs)
     res = {}
     for lanes in ("1", "3"):
         monkeypatch.setenv("VDAMP_LANES", lanes)
         clear_plans()
         res[lanes] = vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, 4, 5, ground_truths=w.x0,
-                                     keep_r_iters=(1, 4), precision="fp32", keep_device=True)
+                                     keep_r_iters=(1, 4), precision=precision, keep_device=True)
     clear_plans()
     (a, ta), (b, tb) = res["1"], res["3"]
     assert np.array_equal(a, b) and np.isfinite(a).all()
@@ -335,3 +341,91 @@ def test_lanes_with_diagnostics_bitwise_equal(monkeypatch):
                 assert np.array_equal(np.asarray(dx[k]), np.asarray(dy[k])), k
     for k in (1, 4):
         assert ta[0].device_snapshots[k].equal(tb[0].device_snapshots[k])
+
+
+def test_device_measurement_validation():
+    """Raw C-ABI inputs the Python layer would reject: an out-of-range index is skipped by the
+    scatter kernel (no out-of-bounds write) and reported as ValueError, synchronously on the
+    functional path and at StreamingReconstructor.wait() on the pipelined one; a repeated
+    index and a probability outside (0, 1] likewise.  The plan stays usable afterwards."""
+    import torch
+    from paper_1911_01234_b200 import vdamp, workload
+    w = workload.make_workload("cfg1", batch=2)
+    inp = vdamp.prepare_batch(w.ys, w.masks, w.pmap, w.noise_vars)
+    rec = vdamp.BatchReconstructor(256, 256, 4, 2, precision="fp32")
+    p = rec.plan
+    good = rec.upload(inp, pin=False)
+    ref = rec(good["y"], good["indices"], good["counts"], good["probs"], good["noise_var"], 3).cpu().clone()
+
+    def variant(kind):
+        d = dict(good)
+        if kind == "range":
+            d["indices"] = good["indices"].clone(); d["indices"][5] = 65536 * 7
+        elif kind == "neg":
+            d["indices"] = good["indices"].clone(); d["indices"][0] = -3
+        elif kind == "dup":
+            d["indices"] = good["indices"].clone(); d["indices"][9] = d["indices"][8]
+        else:
+            d["probs"] = good["probs"].clone().reshape(-1); d["probs"][int(good["indices"][4])] = 0.0
+        return d
+
+    for kind in ("range", "neg", "dup", "prob"):
+        d = variant(kind)
+        with pytest.raises(ValueError):            # synchronous check (functional API default)
+            p.set_measurements(d["y"], d["indices"], d["counts"], d["probs"], d["noise_var"], True)
+        with pytest.raises(ValueError):            # BatchReconstructor: reported after its sync
+            rec(d["y"], d["indices"], d["counts"], d["probs"], d["noise_var"], 3)
+        out = rec(good["y"], good["indices"], good["counts"], good["probs"], good["noise_var"], 3).cpu()
+        assert torch.equal(out, ref), kind          # plan usable again, same result
+    srec = vdamp.StreamingReconstructor(256, 256, 4, 2, precision="fp32")
+    host = srec.upload(inp, pin=True)
+    badh = dict(host)
+    badh["indices"] = host["indices"].clone(); badh["indices"][3] = 1 << 40
+    outs = [torch.empty((2, 256, 256), dtype=torch.complex64).pin_memory() for _ in range(2)]
+    srec.submit(host, 3, outs[0])
+    with pytest.raises(ValueError):                # deferred: at the first later call that sees it
+        srec.submit(badh, 3, outs[1])
+        srec.wait()
+    srec.submit(host, 3, outs[0])
+    srec.wait()
+    assert torch.equal(outs[0], ref)
+
+
+def _gpu_keys_f32(r):
+    """|r| as the fp32 SURE kernel forms it: sqrtf(fmaf(x, x, y*y)) of the complex64 value."""
+    c = np.asarray(r).astype(np.complex64)
+    x = c.real.astype(np.float64)
+    yy = (c.imag * c.imag).astype(np.float32).astype(np.float64)
+    return np.sqrt((x * x + yy).astype(np.float32)).astype(np.float64)
+
+
+@pytest.mark.parametrize("name,steps", [("cfg1", 10), ("cfg2", 8), ("cfg4_r2", 8)])
+def test_fp32_threshold_is_exact_argmin_of_its_data(oracle, name, steps):
+    """fp32 mode, teacher-forced along the oracle's trajectory: in every (iteration, subband)
+    selection the GPU threshold is the exact SURE argmin (src/denoise.py:62-118, float64 sums)
+    of the GPU's own float32 magnitudes and tau -- so a threshold that differs from the
+    float64 oracle's does so only because r differs by float32 round-off (~5e-7), i.e. a
+    near-tie flip of SURVEY A.5, never because the selection is inexact."""
+    from paper_1911_01234_b200 import vdamp, wavelet, workload
+    w = workload.make_workload(name, batch=1)
+    c = w.config
+    p = oracle.Problem(w.ys[0].astype(np.complex128), w.masks[0].indices, w.pmap.probs, w.noise_vars[0], c.scales)
+    lay = wavelet.SubbandLayout.create(c.size, c.size, c.scales)
+    rt = np.zeros(c.size * c.size, dtype=np.complex128)
+    for k in range(steps):
+        st = oracle.step(p, rt)
+        g = vdamp.iterate(vdamp.VdampState(wavelet.WaveletCoeffs(rt, lay), k=k), w.ys[0], w.masks[0], w.pmap,
+                          w.noise_vars[0], precision="fp32")
+        assert rel2(g.r.values, st.r) <= 2e-6
+        assert np.allclose(g.tau.values, st.tau, rtol=5e-6)
+        for j, bd in enumerate(p.bands):
+            m = np.sort(_gpu_keys_f32(g.r.values[bd.offset:bd.offset + bd.length]))
+            tau = max(float(g.tau.values[j]), 1e-300)
+            t_own = oracle.threshold_scan(m, tau)[0]
+            tg = float(g.thresholds[j])
+            if abs(tg - t_own) > 1e-9 * max(t_own, 1e-30):
+                # only an exact near-tie of the risk may pick the other candidate
+                risk = lambda t: (np.sum(np.minimum(m, t) ** 2) - m.size * tau
+                                  + tau * np.sum(2.0 - t / m[m > t]))
+                assert risk(tg) <= risk(t_own) * (1 + 1e-12) + 1e-300, (k, j, tg, t_own)
+        rt = st.r_tilde

@@ -107,3 +107,45 @@ def test_algorithmic_bytes_formula():
     # 256^2 R4 -> 3,874,816 B (n = N/4)
     assert workload.algorithmic_bytes_per_image_iter(65536, 16384) == 3874816
     assert workload.algorithmic_bytes_per_image_iter(512 * 512, 512 * 512 // 8) == 15106048
+
+
+def test_check_measurements_c_abi_without_gpu():
+    """vdamp_check_measurements (host arrays, no device): a bad index, a repeated index or a
+    probability outside (0, 1] is VDAMP_ERR_ARG, as the reference raises ValueError
+    (src/fourier.py:65-74, src/sampling.py:45-46); valid inputs pass."""
+    from paper_1911_01234_b200 import _lib
+    lib = _lib.load()
+    H = W = 8
+    probs = np.full(H * W, 0.5)
+    nv = np.array([0.1, 0.2])
+
+    def call(idx, counts, pr=probs, stride=0, noise=nv):
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        counts = np.ascontiguousarray(counts, dtype=np.int64)
+        pr = np.ascontiguousarray(pr, dtype=np.float64)
+        noise = np.ascontiguousarray(noise, dtype=np.float64)
+        P = lambda a, t: a.ctypes.data_as(ctypes.POINTER(t))
+        return lib.vdamp_check_measurements(H, W, len(counts), P(idx, ctypes.c_int64), P(counts, ctypes.c_int64),
+                                            P(pr, ctypes.c_double), stride, P(noise, ctypes.c_double))
+
+    good = [0, 5, 63, 0, 7]
+    assert call(good, [3, 2]) == _lib.VDAMP_OK
+    assert call([0, 64, 3, 1, 2], [3, 2]) == _lib.VDAMP_ERR_ARG
+    assert b"outside [0" in lib.vdamp_last_error()
+    assert call([0, -1, 3, 1, 2], [3, 2]) == _lib.VDAMP_ERR_ARG
+    assert call([0, 5, 5, 1, 2], [3, 2]) == _lib.VDAMP_ERR_ARG
+    assert b"repeated" in lib.vdamp_last_error()
+    bad = probs.copy()
+    bad[63] = 0.0
+    assert call(good, [3, 2], bad) == _lib.VDAMP_ERR_ARG
+    assert b"probability" in lib.vdamp_last_error()
+    bad[63] = 1.5
+    assert call(good, [3, 2], bad) == _lib.VDAMP_ERR_ARG
+    bad[63] = np.nan
+    assert call(good, [3, 2], bad) == _lib.VDAMP_ERR_ARG
+    assert call(good, [3, 2], np.tile(probs, 2), stride=H * W) == _lib.VDAMP_OK
+    assert call(good, [3, 2], stride=5) == _lib.VDAMP_ERR_ARG
+    assert call(good, [0, 5]) == _lib.VDAMP_ERR_ARG
+    assert call(good, [3, 2], noise=np.array([0.1, -1.0])) == _lib.VDAMP_ERR_ARG
+    with pytest.raises(ValueError):
+        _lib.check(call([0, 64, 3, 1, 2], [3, 2]))
