@@ -87,6 +87,11 @@ struct Plan {
     double* nmconst = nullptr;      // [B][2]: mask error constant, |x0|^2
     double* nmpart = nullptr;       // [B][ntiles]
     bool parseval = true;           // per-iteration NMSE by Parseval (one forward FFT)
+    // bound-pruned exact SURE selection (vdamp_prune.cuh) for 4,096..16,384-key subbands:
+    // on for fp64 keys (2x faster than their bitonic full sort), off for fp32 keys (the
+    // counting-sort full path measured faster there: 3.46 vs 3.89 ms/step cfg1);
+    // VDAMP_PRUNE=0/1 forces it off/on for both
+    int prune = -1;
     void* what = nullptr;           // baselines: w_hat state [B][N]
     double* btau = nullptr;         // baselines: [B][S] oracle tau
     double* berr = nullptr;         // baselines: [B][S][2] coefficient errors
@@ -431,6 +436,7 @@ struct Seq {
         a.par = onsager_par ? p->par : nullptr; a.parf = p->parf; a.trace = trace;
         a.w0 = use_w0 ? (const C*)p->w0 : nullptr;
         a.kA = (R*)p->kA; a.kB = (R*)p->kB;
+        a.prune = p->prune ? 1 : 0;
         // big subbands: 1024-thread CTAs with the full sort workspace; small ones:
         // 128-thread CTAs with little shared memory, many per SM
         // the small-subband kernel runs on a side stream, concurrently with the
@@ -490,8 +496,12 @@ struct Seq {
                 // large subbands: global counting sort counters + ranking tile
                 const size_t gcs = sizeof(R) == 4 ? 32768 * 4 + 16384 * sizeof(R) : 8192 * 4 + 8192 * sizeof(R);
                 if (sm < gcs) sm = gcs;
+                // fp64 pruned path: keys | counters | reduction scratch + list (vdamp_prune.cuh)
+                const size_t smp = slot16 * sizeof(R) + (PR_NC + PR_NF + 32) * 4 + (size_t)PR_BIDN * 2 +
+                                   (5 * 32 + 8) * 8 + ((size_t)pr_lmax<R>() + pr_lmax<R>() / 32 + 8) * sizeof(R);
+                if (sizeof(R) == 8 && p->prune && sm < smp) sm = smp;
                 constexpr int BNT = sizeof(R) == 4 ? BNT32 : BNT64;
-                auto k = sure_select<R, BNT>;
+                auto k = p->prune ? sure_select<R, BNT, true> : sure_select<R, BNT, false>;
                 set_smem(k, sm);
                 launch(k, grid, BNT, sm, ls, p->geo, a);
             } else {
@@ -893,6 +903,8 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         // GPU-bound and measured slightly faster with direct launches (round 1, cfg1)
         p->graphs = (long long)batch * p->N <= 8LL * 65536;
         if (const char* pe = getenv("VDAMP_PARSEVAL")) p->parseval = atoi(pe) != 0;
+        p->prune = precision == VDAMP_FP64 ? 1 : 0;
+        if (const char* pe = getenv("VDAMP_PRUNE")) p->prune = atoi(pe) != 0;
         if (const char* ge = getenv("VDAMP_GRAPHS")) p->graphs = atoi(ge) != 0;
         if (const char* ie = getenv("VDAMP_INTERLEAVE")) p->interleave = atoi(ie) != 0;
         CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
@@ -1412,6 +1424,9 @@ extern "C" VDAMP_API int vdamp_debug_scan_times(long long* out, int images) {
 }
 extern "C" VDAMP_API int vdamp_debug_csort_times(long long* out, int images) {
     return guard([&] { CK(cudaMemcpyFromSymbol(out, g_csort, (size_t)images * 64 * 8 * sizeof(long long))); });
+}
+extern "C" VDAMP_API int vdamp_debug_prune_times(long long* out, int images) {
+    return guard([&] { CK(cudaMemcpyFromSymbol(out, g_prune, (size_t)images * 64 * 10 * sizeof(long long))); });
 }
 #endif
 

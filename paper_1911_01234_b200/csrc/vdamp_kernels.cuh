@@ -1628,6 +1628,7 @@ struct SelArgs {
     const typename CT<R>::T* w0;     // [B][N] ground-truth coefficients or null
     R* kA;                           // [B][N] key scratch (subbands > SCAP)
     R* kB;
+    int prune;                       // bound-pruned exact selection (vdamp_prune.cuh) for 4096..SCAP keys
     int item_start[MAXS + 1];        // work items: subbands item_list[item_start[i] .. item_start[i+1])
     int item_list[MAXS];
 };
@@ -2468,6 +2469,8 @@ __device__ __forceinline__ void scan_keys(const R* keys, int T, int tilebase, in
     }
 }
 
+#include "vdamp_prune.cuh"
+
 #ifdef VDAMP_PHASE_TIMING
 // [image][subband][phase]: clock64 deltas of thread 0 (debug builds only)
 __device__ long long g_phase[4096][64][4];
@@ -2489,6 +2492,45 @@ struct SelShared {
     Best run;                        // running argmin over the tiles
     double err, ref;                 // subband |r - w0|^2, |w0|^2 (trace)
 };
+
+// The t = 0 candidates (src/denoise.py:84: when no magnitude is zero; m0 = the
+// smallest key, or 0 to skip them), the argmin over all tiles and candidates
+// (ties -> smaller t) in S_.run, alpha (src/denoise.py:169), the clamp
+// (src/vdamp.py:121-124) and the outputs.
+template <typename R, int NT>
+__device__ __forceinline__ void select_finish(const Geo& g, const SelArgs<R>& a, int j, int bi, int n, double tau,
+                                              double m0, bool have_w0, SelShared<NT>& S_) {
+    const int tid = threadIdx.x;
+    __syncthreads();
+    __syncthreads();
+    if (tid == 0) {
+        if (m0 > 0) {
+            const double totinv = S_.totinv;
+            const double nn = (double)n;
+            Best bb = S_.run;
+            const double base0 = fma(2.0 * tau, nn, -(nn * tau));   // scan_keys' grouping at t = 0
+            consider(bb, base0, 0.0, nn, totinv);
+            const double ts = tau * totinv / (2.0 * nn);
+            if (ts > 0.0 && ts < m0) {
+                const double rsk = fma(ts, ts * nn - tau * totinv, base0);
+                consider(bb, rsk, ts, nn, totinv);
+            }
+            S_.run = bb;
+        }
+        const Best bb = S_.run;
+        const double alpha = (bb.cnt - 0.5 * bb.t * bb.inv) / (double)n;   // src/denoise.py:169
+        const bool clamped = alpha >= ALPHA_CLAMP;                         // src/vdamp.py:121-124
+        const double ac = clamped ? ALPHA_CLAMP : alpha;
+        const long long pj = ((long long)bi * g.S + j);
+        if (a.par) { a.par[3 * pj] = bb.t; a.par[3 * pj + 1] = ac; a.par[3 * pj + 2] = 1.0 / (1.0 - ac); }
+        if (a.parf) { a.parf[3 * pj] = bb.t; a.parf[3 * pj + 1] = 0.0; a.parf[3 * pj + 2] = 1.0; }
+        if (a.trace) {
+            double* tr = a.trace + pj * TRACE_F;
+            tr[0] = S_.tau; tr[1] = bb.t; tr[2] = bb.t / tau; tr[3] = ac; tr[4] = alpha;
+            tr[5] = clamped ? 1.0 : 0.0; tr[6] = have_w0 ? S_.err : 0.0; tr[7] = have_w0 ? S_.ref : 0.0;
+        }
+    }
+}
 
 // Exact SURE selection for subband j of image bi (src/denoise.py:62-118,
 // 165-173; clamp src/vdamp.py:121-124).
@@ -2738,46 +2780,140 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             scan_tile<R, NT, EMAXS, SMEMSUF>(tk, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, s_best, &S_.run,
                                              &s_totinv, slo, shi, sdbg);
     }
-    // candidate t = 0 when no magnitude is zero (src/denoise.py:84)
-    __syncthreads();
-    __syncthreads();
-    if (tid == 0) {
-        const double m0 = large ? (double)sorted[0] : (double)skeys[0];
-        if (m0 > 0) {
-            const double totinv = s_totinv;
-            const double nn = (double)n;
-            Best bb = S_.run;
-            const double base0 = fma(2.0 * tau, nn, -(nn * tau));   // scan_keys' grouping at t = 0
-            consider(bb, base0, 0.0, nn, totinv);
-            const double ts = tau * totinv / (2.0 * nn);
-            if (ts > 0.0 && ts < m0) {
-                const double rsk = fma(ts, ts * nn - tau * totinv, base0);
-                consider(bb, rsk, ts, nn, totinv);
-            }
-            S_.run = bb;
-        }
-    }
-    PHASE_MARK(1);                                   // scans + candidates
-    // the argmin over all tiles and candidates (ties -> smaller t) is S_.run
-    if (tid == 0) {
-        const Best bb = S_.run;
-        const double alpha = (bb.cnt - 0.5 * bb.t * bb.inv) / (double)n;   // src/denoise.py:169
-        const bool clamped = alpha >= ALPHA_CLAMP;                         // src/vdamp.py:121-124
-        const double ac = clamped ? ALPHA_CLAMP : alpha;
-        const long long pj = ((long long)bi * g.S + j);
-        if (a.par) { a.par[3 * pj] = bb.t; a.par[3 * pj + 1] = ac; a.par[3 * pj + 2] = 1.0 / (1.0 - ac); }
-        if (a.parf) { a.parf[3 * pj] = bb.t; a.parf[3 * pj + 1] = 0.0; a.parf[3 * pj + 2] = 1.0; }
-        if (a.trace) {
-            double* tr = a.trace + pj * TRACE_F;
-            tr[0] = s_tau; tr[1] = bb.t; tr[2] = bb.t / tau; tr[3] = ac; tr[4] = alpha;
-            tr[5] = clamped ? 1.0 : 0.0; tr[6] = w0 ? S_.err : 0.0; tr[7] = w0 ? S_.ref : 0.0;
-        }
-    }
+    select_finish<R, NT>(g, a, j, bi, n, tau, large ? (double)sorted[0] : (double)skeys[0], w0 != nullptr, S_);
     PHASE_MARK(2);                                   // argmin + outputs
 }
 
+// Bound-pruned selection of one subband of n = EF * NT keys (4,096 <= n <= SCAP):
+// load, |r| keys (+ trace error sums), tau, select_pruned (vdamp_prune.cuh), outputs.
+// Returns false when the bounds leave too many keys; the caller then runs the
+// full sort (select_band) on the subband from scratch.
+// Shared memory: fp32 -- keys | stage | counters as in select_band (the subband
+// lands in stage + counters by TMA); fp64 -- keys (doubles) | counters | scratch + list.
 template <typename R, int NT>
-__global__ void __launch_bounds__(NT, NT >= BNT32 ? 1 : 4) sure_select(Geo g, SelArgs<R> a) {
+__device__ __forceinline__ bool prune_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R* keys, SelShared<NT>& S_) {
+    typedef typename CT<R>::T C;
+    typedef typename PrT<R>::U U;
+    constexpr int CAPK = Scap<R>::v;
+    constexpr int SLOT = (CAPK + CAPK / 32 + 2 + 3) & ~3;
+    const int tid = threadIdx.x;
+    const int n = g.len[j];
+    const int ef = n / NT;
+    const long long base = (long long)bi * g.N + g.off[j];
+    if (a.tau_in) {
+        if (tid == 0) S_.tau = a.tau_in[(long long)bi * g.S + j];
+    } else {
+        for (int i = tid; i < a.ntiles; i += NT) S_.tpart[i] = a.taupart[((long long)bi * a.ntiles + i) * g.S + j];
+    }
+    const C* rs = a.r + base;
+    const C* w0 = a.w0 ? a.w0 + base : nullptr;
+    double err = 0.0, ref = 0.0;
+    U kmn = ~(U)0, kmx = 0;
+    unsigned* cnt;
+    double* rsh;
+    unsigned short* bid;
+    if constexpr (sizeof(R) == 4) {
+        R* stage = keys + SLOT;
+        cnt = reinterpret_cast<unsigned*>(stage + SLOT);
+        rsh = reinterpret_cast<double*>(stage);
+        // stage: reduction scratch | list | bucket ids (free once the keys are built)
+        bid = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(stage) + PR_STAGE_BID);
+        C* cz = reinterpret_cast<C*>(stage);
+        const unsigned bytes = (unsigned)n * (unsigned)sizeof(C);
+        __syncthreads();                                       // previous users of the region are done
+        if (tid == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(&S_.mbar, bytes);
+            for (unsigned o = 0; o < bytes; o += 32768u)
+                bulk_g2s(reinterpret_cast<char*>(cz) + o, reinterpret_cast<const char*>(rs) + o,
+                         bytes - o < 32768u ? bytes - o : 32768u, &S_.mbar);
+        }
+        mbar_wait(&S_.mbar, S_.mphase);
+        for (int q = 0; q < ef; ++q) {
+            const int e = tid + q * NT;
+            const C v = cz[e];
+            const float kf = (float)cmag(v);
+            keys[KI(e)] = (R)kf;
+            const U u = __float_as_uint(kf);
+            if (u) kmn = min(kmn, u);
+            kmx = max(kmx, u);
+            if (w0) {
+                const C w = w0[e];
+                const double dx = (double)v.x - (double)w.x, dy = (double)v.y - (double)w.y;
+                err += dx * dx + dy * dy;
+                ref += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) S_.mphase ^= 1u;
+    } else {
+        cnt = reinterpret_cast<unsigned*>(keys + SLOT);
+        bid = reinterpret_cast<unsigned short*>(cnt + PR_NC + PR_NF + 32);
+        rsh = reinterpret_cast<double*>(bid + PR_BIDN);
+        constexpr int LB = 8;                                  // loads in flight per thread
+        for (int e0 = tid; e0 < n; e0 += LB * NT) {
+            C v[LB];
+#pragma unroll
+            for (int u = 0; u < LB; ++u) if (e0 + u * NT < n) v[u] = rs[e0 + u * NT];
+#pragma unroll
+            for (int u = 0; u < LB; ++u) {
+                const int e = e0 + u * NT;
+                if (e < n) {
+                    const R m = cmag(v[u]);
+                    keys[KI(e)] = m;
+                    const U k = PrT<R>::bits(m);
+                    if (k) kmn = k < kmn ? k : kmn;
+                    kmx = k > kmx ? k : kmx;
+                    if (w0) {
+                        const C w = w0[e];
+                        const double dx = (double)v[u].x - (double)w.x, dy = (double)v[u].y - (double)w.y;
+                        err += dx * dx + dy * dy;
+                        ref += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (!a.tau_in && tid == 0) {
+        double t = 0.0;
+        for (int i = 0; i < a.ntiles; ++i) t += S_.tpart[i];
+        S_.tau = t;
+    }
+    if (w0) {
+        const double e2 = block_sum<NT>(err, S_.sh), r2 = block_sum<NT>(ref, S_.sh);
+        if (tid == 0) { S_.err = e2; S_.ref = r2; }
+    }
+    __syncthreads();
+    const double tau = fmax(S_.tau, TAU_FLOOR);
+    R* plist = reinterpret_cast<R*>(rsh + 5 * (NT / 32) + 8);
+#ifdef VDAMP_PHASE_TIMING
+    long long* pdbg = bi < 4096 ? &g_prune[bi][j][0] : nullptr;
+#else
+    long long* pdbg = nullptr;
+#endif
+    PrOut po{0, 0.0};
+    bool ok;
+    if (ef == 16) ok = select_pruned<R, NT, 16>(n, tau, keys, cnt, bid, plist, rsh, kmn, kmx, S_, po, pdbg);
+    else if (ef == 8) ok = select_pruned<R, NT, 8>(n, tau, keys, cnt, bid, plist, rsh, kmn, kmx, S_, po, pdbg);
+    else ok = select_pruned<R, NT, 4>(n, tau, keys, cnt, bid, plist, rsh, kmn, kmx, S_, po, pdbg);
+    if (!ok) return false;
+    select_finish<R, NT>(g, a, j, bi, n, tau, po.nbelow == 0 ? po.m0 : 0.0, w0 != nullptr, S_);
+    return true;
+}
+
+// the full sort path as a call: its code stays out of the pruned path's instruction stream
+template <typename R, int NT>
+__device__ __noinline__ void select_band_call(const Geo& g, const SelArgs<R>& a, int j, int bi, R* keys,
+                                              SelShared<NT>& S_) {
+    select_band<R, NT>(g, a, j, bi, keys, S_);
+}
+
+// PRUNE: the bound-pruned path first (vdamp_prune.cuh), the full sort as an out-of-line
+// fallback; otherwise the full sort inline (the code the fp32 default runs)
+template <typename R, int NT, bool PRUNE = false>
+__global__ void __launch_bounds__(NT, NT >= BNT32 ? 1 : 4) sure_select(const __grid_constant__ Geo g,
+                                                                       const __grid_constant__ SelArgs<R> a) {
     pdl_enter();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     R* keys = reinterpret_cast<R*>(smem_raw);
@@ -2787,7 +2923,16 @@ __global__ void __launch_bounds__(NT, NT >= BNT32 ? 1 : 4) sure_select(Geo g, Se
     __syncthreads();
     // one work item = one large subband, or several small ones packed to ~SCAP keys
     for (int q = a.item_start[it]; q < a.item_start[it + 1]; ++q) {
-        select_band<R, NT>(g, a, a.item_list[q], bi, keys, S_);
+        const int j = a.item_list[q];
+        if constexpr (PRUNE && NT >= BNT32) {
+            const int n = g.len[j];
+            bool done = false;
+            if (n >= 4096 && n <= Scap<R>::v && n % NT == 0 && (n / NT) % 4 == 0)
+                done = prune_band<R, NT>(g, a, j, bi, keys, S_);
+            if (!done) select_band_call<R, NT>(g, a, j, bi, keys, S_);
+        } else {
+            select_band<R, NT>(g, a, j, bi, keys, S_);
+        }
         __syncthreads();
     }
 }

@@ -9,7 +9,7 @@ Tolerances:
 import numpy as np
 import pytest
 
-from conftest import golden
+from conftest import exact_or_tie, golden, gpu_keys_f32
 
 pytestmark = pytest.mark.gpu
 
@@ -84,6 +84,14 @@ def _tricky_coeffs(rng, n, kind):
         r = r * 0.05
         idx = rng.choice(n, n // 20, replace=False)
         r[idx] += rng.exponential(3.0, idx.size)
+    elif kind == "wide":
+        # magnitudes log-uniform over 40 octaves: keys below the pruned path's linear range
+        r = np.exp2(rng.uniform(-30, 10, n)) * np.exp(1j * rng.uniform(0, 6.28, n))
+    elif kind == "heavy":
+        r = rng.standard_cauchy(n) + 1j * rng.standard_cauchy(n)
+    elif kind == "onehot":
+        r = r * 1e-3
+        r[rng.integers(0, n)] = 1e6
     return r
 
 
@@ -253,3 +261,30 @@ def test_reference_benchmark_512():
     x32, tr32 = vdamp.run(kd.values, mask, pmap, kd.noise_var, 4, 30, ground_truth=x0, precision="fp32")
     assert np.abs(tr32.nmse_curve() - g["nmse_db"]).max() <= 0.05
     assert rel2(x32, x) <= 1e-2
+
+
+@pytest.mark.parametrize("shape", [(256, 256, 4), (128, 128, 1), (256, 256, 1), (64, 64, 1)])
+@pytest.mark.parametrize("kind", ["gauss", "ties", "zeros", "sparse", "diverged", "wide", "heavy", "onehot"])
+def test_sure_select_fp32_vs_exact_scan(oracle, shape, kind):
+    """fp32 SURE selection (the bound-pruned path for 4,096..16,384-key subbands, the
+    counting sort when it falls back, the small-subband kernel below) against the exact
+    reference scan (src/denoise.py:62-118, float64 sums) of the same float32 magnitudes:
+    the threshold is the argmin or an exact tie of it, alpha follows
+    (src/denoise.py:169)."""
+    from paper_1911_01234_b200 import denoise, wavelet
+    h, w, s = shape
+    rng = np.random.default_rng([h, w, s, len(kind), ord(kind[0]), ord(kind[-1])])
+    lay = wavelet.SubbandLayout.create(h, w, s)
+    r = _tricky_coeffs(rng, h * w, kind).astype(np.complex64).astype(np.complex128)
+    tau = rng.uniform(0.2, 2.0, lay.n_subbands)
+    if kind in ("wide", "heavy"):
+        tau = tau * 1e-4
+    _, al, lam = denoise.denoise_colored(wavelet.WaveletCoeffs(r, lay), denoise.SubbandVector(tau),
+                                         precision="fp32")
+    t_gpu = lam.values * tau
+    for j, b in enumerate(oracle.band_table(h, w, s)):
+        m = np.sort(gpu_keys_f32(r[b.offset:b.offset + b.length]))
+        assert exact_or_tie(oracle, m, float(tau[j]), float(t_gpu[j])), (j, t_gpu[j])
+        t, cnt, inv = oracle.threshold_scan(m, float(tau[j]))
+        if abs(t - t_gpu[j]) <= 1e-9 * max(t, 1e-30):
+            assert np.isclose(al.values[j], (cnt - 0.5 * t * inv) / b.length, rtol=1e-9, atol=1e-12)

@@ -9,6 +9,8 @@ VDAMP's SURE-argmin bifurcation under float32 rounding.
 import numpy as np
 import pytest
 
+from conftest import exact_or_tie, gpu_keys_f32
+
 pytestmark = pytest.mark.gpu
 
 
@@ -391,14 +393,6 @@ def test_device_measurement_validation():
     assert torch.equal(outs[0], ref)
 
 
-def _gpu_keys_f32(r):
-    """|r| as the fp32 SURE kernel forms it: sqrtf(fmaf(x, x, y*y)) of the complex64 value."""
-    c = np.asarray(r).astype(np.complex64)
-    x = c.real.astype(np.float64)
-    yy = (c.imag * c.imag).astype(np.float32).astype(np.float64)
-    return np.sqrt((x * x + yy).astype(np.float32)).astype(np.float64)
-
-
 @pytest.mark.parametrize("name,steps", [("cfg1", 10), ("cfg2", 8), ("cfg4_r2", 8)])
 def test_fp32_threshold_is_exact_argmin_of_its_data(oracle, name, steps):
     """fp32 mode, teacher-forced along the oracle's trajectory: in every (iteration, subband)
@@ -419,13 +413,8 @@ def test_fp32_threshold_is_exact_argmin_of_its_data(oracle, name, steps):
         assert rel2(g.r.values, st.r) <= 2e-6
         assert np.allclose(g.tau.values, st.tau, rtol=5e-6)
         for j, bd in enumerate(p.bands):
-            m = np.sort(_gpu_keys_f32(g.r.values[bd.offset:bd.offset + bd.length]))
+            m = np.sort(gpu_keys_f32(g.r.values[bd.offset:bd.offset + bd.length]))
             tau = max(float(g.tau.values[j]), 1e-300)
-            t_own = oracle.threshold_scan(m, tau)[0]
-            tg = float(g.thresholds[j])
-            if abs(tg - t_own) > 1e-9 * max(t_own, 1e-30):
-                # only an exact near-tie of the risk may pick the other candidate
-                risk = lambda t: (np.sum(np.minimum(m, t) ** 2) - m.size * tau
-                                  + tau * np.sum(2.0 - t / m[m > t]))
-                assert risk(tg) <= risk(t_own) * (1 + 1e-12) + 1e-300, (k, j, tg, t_own)
+            # only an exact near-tie of the risk may pick another candidate
+            assert exact_or_tie(oracle, m, tau, float(g.thresholds[j])), (k, j)
         rt = st.r_tilde
