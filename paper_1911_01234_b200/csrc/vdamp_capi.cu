@@ -87,11 +87,11 @@ struct Plan {
     double* nmconst = nullptr;      // [B][2]: mask error constant, |x0|^2
     double* nmpart = nullptr;       // [B][ntiles]
     bool parseval = true;           // per-iteration NMSE by Parseval (one forward FFT)
-    // bound-pruned exact SURE selection (vdamp_prune.cuh) for 4,096..16,384-key subbands:
-    // on for fp64 keys (2x faster than their bitonic full sort), off for fp32 keys (the
-    // counting-sort full path measured faster there: 3.46 vs 3.89 ms/step cfg1);
-    // VDAMP_PRUNE=0/1 forces it off/on for both
-    int prune = -1;
+    // bound-pruned exact SURE selection (vdamp_prune.cuh), bit 0: subbands of 4,096..16,384
+    // keys, bit 1: larger ones (keys in global scratch).  fp64 keys: both (2x faster than
+    // their bitonic / global sorts); fp32 keys: large only (the shared-memory counting sort
+    // measured faster for <= 16,384 keys: 3.46 vs 3.89 ms/step cfg1).  VDAMP_PRUNE=mask
+    int prune = 0;
     void* what = nullptr;           // baselines: w_hat state [B][N]
     double* btau = nullptr;         // baselines: [B][S] oracle tau
     double* berr = nullptr;         // baselines: [B][S][2] coefficient errors
@@ -436,7 +436,7 @@ struct Seq {
         a.par = onsager_par ? p->par : nullptr; a.parf = p->parf; a.trace = trace;
         a.w0 = use_w0 ? (const C*)p->w0 : nullptr;
         a.kA = (R*)p->kA; a.kB = (R*)p->kB;
-        a.prune = p->prune ? 1 : 0;
+        a.prune = p->prune;
         // big subbands: 1024-thread CTAs with the full sort workspace; small ones:
         // 128-thread CTAs with little shared memory, many per SM
         // the small-subband kernel runs on a side stream, concurrently with the
@@ -903,8 +903,16 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         // GPU-bound and measured slightly faster with direct launches (round 1, cfg1)
         p->graphs = (long long)batch * p->N <= 8LL * 65536;
         if (const char* pe = getenv("VDAMP_PARSEVAL")) p->parseval = atoi(pe) != 0;
-        p->prune = precision == VDAMP_FP64 ? 1 : 0;
-        if (const char* pe = getenv("VDAMP_PRUNE")) p->prune = atoi(pe) != 0;
+        p->prune = precision == VDAMP_FP64 ? 3 : 2;
+        {
+            // one CTA per large subband: with few of them (cfg3: 1 image x 6) the pruned
+            // single-CTA passes measured slower than the fp64 global sort (120 vs 165
+            // img-iter/s); fp32 splits those subbands by value (big_keys / big_range)
+            int nlarge = 0;
+            for (int j = 0; j < p->S; ++j) nlarge += g.len[j] > capk;
+            if ((long long)batch * nlarge * 4 <= (long long)p->nsm) p->prune &= 1;
+        }
+        if (const char* pe = getenv("VDAMP_PRUNE")) p->prune = atoi(pe) & 3;
         if (const char* ge = getenv("VDAMP_GRAPHS")) p->graphs = atoi(ge) != 0;
         if (const char* ie = getenv("VDAMP_INTERLEAVE")) p->interleave = atoi(ie) != 0;
         CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));

@@ -1628,7 +1628,7 @@ struct SelArgs {
     const typename CT<R>::T* w0;     // [B][N] ground-truth coefficients or null
     R* kA;                           // [B][N] key scratch (subbands > SCAP)
     R* kB;
-    int prune;                       // bound-pruned exact selection (vdamp_prune.cuh) for 4096..SCAP keys
+    int prune;                       // bound-pruned exact selection (vdamp_prune.cuh): bit 0 4096..SCAP keys, bit 1 larger
     int item_start[MAXS + 1];        // work items: subbands item_list[item_start[i] .. item_start[i+1])
     int item_list[MAXS];
 };
@@ -2812,7 +2812,43 @@ __device__ __forceinline__ bool prune_band(const Geo& g, const SelArgs<R>& a, in
     unsigned* cnt;
     double* rsh;
     unsigned short* bid;
-    if constexpr (sizeof(R) == 4) {
+    const bool large = n > CAPK;
+    if (large) {
+        // keys to global scratch (L2-resident); the shared key region holds the list
+        R* ka = a.kA + base;
+        if constexpr (sizeof(R) == 4) {
+            cnt = reinterpret_cast<unsigned*>(keys + 2 * SLOT);
+            rsh = reinterpret_cast<double*>(keys + SLOT);
+        } else {
+            cnt = reinterpret_cast<unsigned*>(keys + SLOT);
+            rsh = reinterpret_cast<double*>(cnt + PR_NC + PR_NF + 32);
+        }
+        bid = nullptr;
+        constexpr int LB = 8;                                  // loads in flight per thread
+        for (int e0 = tid; e0 < n; e0 += LB * NT) {
+            C v[LB];
+#pragma unroll
+            for (int u = 0; u < LB; ++u) if (e0 + u * NT < n) v[u] = rs[e0 + u * NT];
+#pragma unroll
+            for (int u = 0; u < LB; ++u) {
+                const int e = e0 + u * NT;
+                if (e < n) {
+                    const R m = cmag(v[u]);
+                    ka[e] = m;
+                    const U k = PrT<R>::bits(m);
+                    if (k) kmn = k < kmn ? k : kmn;
+                    kmx = k > kmx ? k : kmx;
+                    if (w0) {
+                        const C w = w0[e];
+                        const double dx = (double)v[u].x - (double)w.x, dy = (double)v[u].y - (double)w.y;
+                        err += dx * dx + dy * dy;
+                        ref += (double)w.x * (double)w.x + (double)w.y * (double)w.y;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    } else if constexpr (sizeof(R) == 4) {
         R* stage = keys + SLOT;
         cnt = reinterpret_cast<unsigned*>(stage + SLOT);
         rsh = reinterpret_cast<double*>(stage);
@@ -2886,7 +2922,7 @@ __device__ __forceinline__ bool prune_band(const Geo& g, const SelArgs<R>& a, in
     }
     __syncthreads();
     const double tau = fmax(S_.tau, TAU_FLOOR);
-    R* plist = reinterpret_cast<R*>(rsh + 5 * (NT / 32) + 8);
+    R* plist = large ? keys : reinterpret_cast<R*>(rsh + 5 * (NT / 32) + 8);
 #ifdef VDAMP_PHASE_TIMING
     long long* pdbg = bi < 4096 ? &g_prune[bi][j][0] : nullptr;
 #else
@@ -2894,7 +2930,9 @@ __device__ __forceinline__ bool prune_band(const Geo& g, const SelArgs<R>& a, in
 #endif
     PrOut po{0, 0.0};
     bool ok;
-    if (ef == 16) ok = select_pruned<R, NT, 16>(n, tau, keys, cnt, bid, plist, rsh, kmn, kmx, S_, po, pdbg);
+    if (large) ok = select_pruned<R, NT, 0, SelShared<NT>, true>(n, tau, a.kA + base, cnt, bid, plist, rsh, kmn, kmx,
+                                                                 S_, po, pdbg);
+    else if (ef == 16) ok = select_pruned<R, NT, 16>(n, tau, keys, cnt, bid, plist, rsh, kmn, kmx, S_, po, pdbg);
     else if (ef == 8) ok = select_pruned<R, NT, 8>(n, tau, keys, cnt, bid, plist, rsh, kmn, kmx, S_, po, pdbg);
     else ok = select_pruned<R, NT, 4>(n, tau, keys, cnt, bid, plist, rsh, kmn, kmx, S_, po, pdbg);
     if (!ok) return false;
@@ -2927,7 +2965,8 @@ __global__ void __launch_bounds__(NT, NT >= BNT32 ? 1 : 4) sure_select(const __g
         if constexpr (PRUNE && NT >= BNT32) {
             const int n = g.len[j];
             bool done = false;
-            if (n >= 4096 && n <= Scap<R>::v && n % NT == 0 && (n / NT) % 4 == 0)
+            // a.prune: bit 0 subbands of 4,096..SCAP keys, bit 1 larger ones
+            if (n >= 4096 && n % NT == 0 && (n / NT) % 4 == 0 && (a.prune & (n > Scap<R>::v ? 2 : 1)))
                 done = prune_band<R, NT>(g, a, j, bi, keys, S_);
             if (!done) select_band_call<R, NT>(g, a, j, bi, keys, S_);
         } else {

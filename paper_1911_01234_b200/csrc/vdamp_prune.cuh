@@ -350,10 +350,16 @@ __device__ __forceinline__ double pr_ub(double pu, double cge, double A, double 
 // all squares plus 2 n tau in magnitude (keys above t satisfy m > t, so
 // c t^2 <= their squares and tau t sum(1/m) <= n tau), and float rounding of the
 // sums and products stays far below the 1e-5 relative margin added to U.
-template <typename R, int NT, int EF, typename SS>
+// GLOBAL: the keys are n = ef * NT keys in (L2-resident) global scratch at keys[e]
+// (subbands larger than the shared-memory sort), bucket ids are recomputed, the
+// list holds up to SCAP keys; EF is then 0 and ef a runtime count.
+template <typename R, int NT, int EF, typename SS, bool GLOBAL = false>
 __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, unsigned short* bid, R* list,
                               double* sh, typename PrT<R>::U kmn, typename PrT<R>::U kmx, SS& S_, PrOut& out,
                               long long* dbg = nullptr) {
+    const int ef = GLOBAL ? n / NT : EF;
+    constexpr int LMAXK = GLOBAL ? SCAP : pr_lmax<R>();
+    auto key = [&](int e) -> R { if constexpr (GLOBAL) return __ldcg(keys + e); else return keys[KI(e)]; };
     static_assert(NT == PR_NC && PR_NF == 4 * NT, "one coarse bucket and four fine buckets per thread");
     typedef typename PrT<R>::U U;
 #ifdef VDAMP_PHASE_TIMING
@@ -409,11 +415,11 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
         C.ls = ls;
         C.top = PR_NC;
     }
-#pragma unroll
-    for (int q = 0; q < EF; ++q) {
+#pragma unroll (GLOBAL ? 4 : EF)
+    for (int q = 0; q < ef; ++q) {
         const int e = tid + q * NT;
-        const int b = C.bucket(PrT<R>::bits(keys[KI(e)]));
-        bid[KI(e)] = (unsigned short)b;
+        const int b = C.bucket(PrT<R>::bits(key(e)));
+        if constexpr (!GLOBAL) bid[KI(e)] = (unsigned short)b;
         atomicAdd(&cc[b], 1u);
     }
     __syncthreads();
@@ -472,15 +478,16 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
     }
     const int flo = g0 >= 2 ? 2 : g0;            // first fine bucket that belongs to the span
     float pbf = 0.0f, iaf = 0.0f, cblf = 0.0f, zz = INFINITY;
-#pragma unroll
-    for (int q = 0; q < EF; ++q) {
+#pragma unroll (GLOBAL ? 4 : EF)
+    for (int q = 0; q < ef; ++q) {
         const int e = tid + q * NT;
-        const int b = bid[KI(e)];
-        const float mf = (float)keys[KI(e)];
+        const R m = key(e);
+        const int b = GLOBAL ? C.bucket(PrT<R>::bits(m)) : bid[KI(e)];
+        const float mf = (float)m;
         pbf = b < g0 ? fmaf(mf, mf, pbf) : pbf;
         cblf += b < g0 ? 1.0f : 0.0f;
         iaf += b > g1 ? __frcp_ru(mf) : 0.0f;
-        if (b >= g0 && b <= g1) atomicAdd(&cf[F.bucket(PrT<R>::bits(keys[KI(e)]))], 1u);
+        if (b >= g0 && b <= g1) atomicAdd(&cf[F.bucket(PrT<R>::bits(m))], 1u);
     }
     pr_reducef<NT>(pbf, iaf, cblf, zz, shf);
     PR_MARK(2);
@@ -548,18 +555,18 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
 
     // ---- 5. exact float64 offsets (all keys), list gather, sort, scan ---------
     double pre = 0.0, suf = 0.0, nbl = 0.0, nxt = INFINITY, mprev = -INFINITY;
-#pragma unroll
-    for (int q = 0; q < EF; ++q) {
+#pragma unroll (GLOBAL ? 4 : EF)
+    for (int q = 0; q < ef; ++q) {
         const int e = tid + q * NT;
-        const int b = bid[KI(e)];
-        const R m = keys[KI(e)];
+        const R m = key(e);
+        const int b = GLOBAL ? C.bucket(PrT<R>::bits(m)) : bid[KI(e)];
         const int fb = (b < g0) ? -1 : (b > g1) ? 0x7fffffff : F.bucket(PrT<R>::bits(m));
         const double md = (double)m;
         if (fb < f0) { pre = fma(md, md, pre); nbl += 1.0; mprev = fmax(mprev, md); }
         else if (fb > f1) { suf += PrT<R>::rcp(md); nxt = fmin(nxt, md); }
         else {
             const unsigned pos = atomicAdd(lc, 1u);
-            if (pos < (unsigned)pr_lmax<R>()) list[KI(pos)] = m;
+            if (pos < (unsigned)LMAXK) list[KI(pos)] = m;
         }
     }
     pr_reduce5<NT>(pre, suf, nbl, nxt, mprev, sh);
@@ -568,7 +575,7 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
     PR_MARK(4);
     PR_NOTE(7, Lw);
     // the padded list (a power of two >= Lw + 1) must fit the list buffer
-    if (Lw + 1 > pr_lmax<R>() || Lw + (prev ? 1 : 0) < 1) return false;
+    if (Lw + 1 > LMAXK || Lw + (prev ? 1 : 0) < 1) return false;
     // offsets: squares below the list (all keys below but one instance of mprev, the
     // list's first element; its ties stay below), inverses above it
     const double pre_list = prev ? pre - mprev * mprev : 0.0;
@@ -583,8 +590,12 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
     PR_MARK(5);
     if (tid == 0) S_.run = Best{INFINITY, INFINITY, 0.0, 0.0};
     const int Lr = Lw + (prev ? 1 : 0);          // real keys
-    scan_tile<R, NT, 4, false, 4, true>(list, Lr, nb, n, tau, pre_list, suf, nxt, S_.sh, S_.best, &S_.run,
-                                        &S_.totinv, nullptr, nullptr);
+    if (!GLOBAL || Lp <= 4 * NT)
+        scan_tile<R, NT, 4, false, 4, true>(list, Lr, nb, n, tau, pre_list, suf, nxt, S_.sh, S_.best, &S_.run,
+                                            &S_.totinv, nullptr, nullptr);
+    else
+        scan_tile<R, NT, 16, false, 16, true>(list, Lr, nb, n, tau, pre_list, suf, nxt, S_.sh, S_.best, &S_.run,
+                                              &S_.totinv, nullptr, nullptr);
     PR_MARK(6);
     PR_NOTE(8, 1);
     out.nbelow = nb;
