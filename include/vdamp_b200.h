@@ -186,6 +186,13 @@ VDAMP_API int vdamp_set_graphs(vdamp_plan_t plan, int enable);
  * identical for any lane count (images are independent).  Default min(4, batch / 16) (1 from 256 images), env VDAMP_LANES overrides;
  * lanes = 0 restores the default. */
 VDAMP_API int vdamp_set_lanes(vdamp_plan_t plan, int lanes);
+/* Per-iteration device time of vdamp_run (the reference records each iteration's own
+ * wall time, src/vdamp.py:176-179): when enabled, CUDA events bracket K1..K4 of every
+ * iteration on the stream of the first image lane.  vdamp_iteration_times (after the
+ * run; synchronises) returns ms[k] for k < n_iters and *images = the images sharing
+ * that stream (the per-image share of an iteration is ms[k] / *images). */
+VDAMP_API int vdamp_set_iteration_timing(vdamp_plan_t plan, int enable);
+VDAMP_API int vdamp_iteration_times(vdamp_plan_t plan, int n_iters, double* ms, int* images);
 /* total kernel launches issued by this plan since creation or the last reset */
 VDAMP_API int vdamp_launch_count(vdamp_plan_t plan, int64_t* count, int reset);
 

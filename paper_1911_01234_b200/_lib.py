@@ -60,6 +60,8 @@ SIGNATURES = {
     "vdamp_set_validation": (_I, [_P, _I]),
     "vdamp_measurement_status": (_I, [_P, _I]),
     "vdamp_check_measurements": (_I, [_I, _I, _I, _I64P, _I64P, _DP, ctypes.c_int64, _DP]),
+    "vdamp_set_iteration_timing": (_I, [_P, _I]),
+    "vdamp_iteration_times": (_I, [_P, _I, _DP, ctypes.POINTER(_I)]),
 }
 
 _lib = None

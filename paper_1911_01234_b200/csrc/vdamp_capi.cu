@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "vdamp_b200.h"
 #include "vdamp_kernels.cuh"
 
@@ -96,6 +98,12 @@ struct Plan {
     double* btau = nullptr;         // baselines: [B][S] oracle tau
     double* berr = nullptr;         // baselines: [B][S][2] coefficient errors
     double* trtmp = nullptr;        // [B][S][TRACE_F]
+    unsigned* pflag = nullptr;      // [B][S] sure_prune32 fallback flags
+    // per-iteration device times (vdamp_set_iteration_timing): events around K1..K4 of
+    // every iteration on the first lane's stream; images sharing that stream
+    bool iter_timing = false;
+    std::vector<cudaEvent_t> itev;
+    int it_images = 0, it_count = 0;
     cudaStream_t side = nullptr;    // fork/join stream for the small-subband SURE kernel
     // CUDA graph of the whole vdamp_run sequence, re-captured when its key changes
     bool graphs = true;
@@ -163,12 +171,28 @@ inline cudaError_t record(cudaEvent_t e, cudaStream_t s) {
                                                : cudaEventRecord(e, s);
 }
 
+// NVTX ranges (env VDAMP_NVTX=1): one per kernel launch, named by kernel class, and
+// one per vdamp_run / iteration -- host-side launch ranges for nsys/ncu timelines
+static bool nvtx_enabled() {
+    static const bool on = [] { const char* e = getenv("VDAMP_NVTX"); return e && atoi(e) != 0; }();
+    return on;
+}
+static const char* const kClassNames[VDAMP_KERNEL_CLASSES] = {
+    "K1 synthesis+row FFT", "K2 column FFT/residual/tau", "K3 row IFFT+analysis", "K4 SURE select",
+    "finalize", "other"};
+struct NvtxRange {
+    bool on;
+    explicit NvtxRange(const char* name) : on(nvtx_enabled()) { if (on) nvtxRangePushA(name); }
+    ~NvtxRange() { if (on) nvtxRangePop(); }
+};
+
 struct Launch {
     Plan* p;
     int cls;
     cudaStream_t st;
     cudaEvent_t e0 = nullptr;
-    Launch(Plan* p_, int c, cudaStream_t s) : p(p_), cls(c), st(s) {
+    NvtxRange nv;
+    Launch(Plan* p_, int c, cudaStream_t s) : p(p_), cls(c), st(s), nv(kClassNames[c]) {
         if (p->timing) {
             cudaEvent_t e1;
             CK(cudaEventCreate(&e0));
@@ -468,17 +492,19 @@ struct Seq {
         // the small-subband kernel is launched first (on the side stream) so its CTAs take
         // SMs before the big kernel's 200 KB CTAs do: 411k vs 399k img-iter/s (cfg1).  With
         // per-launch timing on, both run on the caller's stream (clean per-kernel times).
+        a.pflag = p->pflag;
+        a.only = nullptr;
+        auto set_items = [&](const std::vector<int>& li) {
+            a.item_start[0] = 0;
+            for (size_t i = 0; i < li.size(); ++i) { a.item_start[i + 1] = (int)i + 1; a.item_list[i] = li[i]; }
+        };
         for (int big = 0; big < 2; ++big) {
-            std::vector<int> st{0}, li;
+            std::vector<int> li;
             for (int j = 0; j < p->S; ++j)
                 if ((p->geo.len[j] > SMALL_N) == (big == 1) && !(p->bigpath && p->geo.len[j] > SCAP)) li.push_back(j);
             // longest items first (grid is image-fastest, so they are all scheduled first)
             std::stable_sort(li.begin(), li.end(), [&](int x, int y) { return p->geo.len[x] > p->geo.len[y]; });
-            for (size_t i = 0; i < li.size(); ++i) st.push_back((int)i + 1);
             if (li.empty()) continue;
-            for (size_t i = 0; i < st.size(); ++i) a.item_start[i] = st[i];
-            for (size_t i = 0; i < li.size(); ++i) a.item_list[i] = li[i];
-            dim3 grid(p->B, (unsigned)li.size());
             cudaStream_t ls = st_;
             if (!big && p->side && !p->timing && p->B * li.size() >= 64) {
                 CK(cudaEventRecord(p->ev_fork, st_));
@@ -486,30 +512,69 @@ struct Seq {
                 ls = p->side;
                 forked = true;
             }
-            Launch L(p, 3, ls);
-            if (big) {
-                const int cap = Scap<R>::v;
-                const size_t slots = (size_t)(cap + cap / 32 + 1) + 1;
-                const size_t slot16 = ((size_t)cap + cap / 32 + 2 + 3) & ~(size_t)3;   // kernel's SLOT
-                size_t sm = sizeof(R) == 4 ? 2 * slot16 * sizeof(R) + CS_WORDS * sizeof(unsigned)
-                                           : slots * sizeof(R);
-                // large subbands: global counting sort counters + ranking tile
-                const size_t gcs = sizeof(R) == 4 ? 32768 * 4 + 16384 * sizeof(R) : 8192 * 4 + 8192 * sizeof(R);
-                if (sm < gcs) sm = gcs;
-                // fp64 pruned path: keys | counters | reduction scratch + list (vdamp_prune.cuh)
-                const size_t smp = slot16 * sizeof(R) + (PR_NC + PR_NF + 32) * 4 + (size_t)PR_BIDN * 2 +
-                                   (5 * 32 + 8) * 8 + ((size_t)pr_lmax<R>() + pr_lmax<R>() / 32 + 8) * sizeof(R);
-                if (sizeof(R) == 8 && p->prune && sm < smp) sm = smp;
-                constexpr int BNT = sizeof(R) == 4 ? BNT32 : BNT64;
-                auto k = p->prune ? sure_select<R, BNT, true> : sure_select<R, BNT, false>;
-                set_smem(k, sm);
-                launch(k, grid, BNT, sm, ls, p->geo, a);
-            } else {
+            if (!big) {
+                set_items(li);
+                Launch L(p, 3, ls);
                 const size_t sm = (size_t)(SMALL_N + SMALL_N / 32 + 2) * sizeof(R);
                 auto k = sure_select<R, SNT_SMALL>;
                 set_smem(k, sm);
-                launch(k, grid, SNT_SMALL, sm, ls, p->geo, a);
+                launch(k, dim3(p->B, (unsigned)li.size()), SNT_SMALL, sm, ls, p->geo, a);
+                continue;
             }
+            const int cap = Scap<R>::v;
+            const size_t slot16 = ((size_t)cap + cap / 32 + 2 + 3) & ~(size_t)3;   // kernel's SLOT
+            int pm = p->prune;
+            // fp32 subbands of 4,096..SCAP keys (multiples of 2,048): the two-CTA-per-SM pruned
+            // kernel, then the full sort for the subbands it flagged
+            if constexpr (std::is_same<R, float>::value) {
+                if ((pm & 1) && p->ntiles <= PR_MAXT) {
+                    std::vector<int> lp, lr;
+                    for (int j : li) {
+                        const int n = p->geo.len[j];
+                        (n >= 4096 && n <= cap && n % 2048 == 0 ? lp : lr).push_back(j);
+                    }
+                    if (!lp.empty()) {
+                        set_items(lp);
+                        {
+                            Launch L(p, 3, ls);
+                            const size_t sm = slot16 * 4 + (PR_NC + PR_NF + 32) * 4 + (5 * 16 + 8) * 8 +
+                                              ((size_t)PR_LMAX / 2 + PR_LMAX / 64 + 8) * 4;
+                            auto k = sure_prune32<PR_NT32>;
+                            set_smem(k, sm);
+                            launch(k, dim3(p->B, (unsigned)lp.size()), PR_NT32, sm, ls, p->geo, a);
+                        }
+                        a.only = p->pflag;
+                        {
+                            Launch L(p, 3, ls);
+                            const size_t sm = 2 * slot16 * sizeof(R) + CS_WORDS * sizeof(unsigned);
+                            auto k = sure_select<R, BNT32, 0>;
+                            set_smem(k, sm);
+                            launch(k, dim3(p->B, (unsigned)lp.size()), BNT32, sm, ls, p->geo, a);
+                        }
+                        a.only = nullptr;
+                    }
+                    li = lr;
+                    pm &= 2;
+                    if (li.empty()) continue;
+                }
+            }
+            set_items(li);
+            Launch L(p, 3, ls);
+            const size_t slots = (size_t)(cap + cap / 32 + 1) + 1;
+            size_t sm = sizeof(R) == 4 ? 2 * slot16 * sizeof(R) + CS_WORDS * sizeof(unsigned) : slots * sizeof(R);
+            // large subbands: global counting sort counters + ranking tile
+            const size_t gcs = sizeof(R) == 4 ? 32768 * 4 + 16384 * sizeof(R) : 8192 * 4 + 8192 * sizeof(R);
+            if (sm < gcs) sm = gcs;
+            // fp64 pruned path: keys | counters | bucket ids | reduction scratch + list (vdamp_prune.cuh)
+            const size_t smp = slot16 * sizeof(R) + (PR_NC + PR_NF + 32) * 4 + (size_t)PR_BIDN * 2 +
+                               (5 * 32 + 8) * 8 + ((size_t)pr_lmax<R>() + pr_lmax<R>() / 32 + 8) * sizeof(R);
+            if (sizeof(R) == 8 && pm && sm < smp) sm = smp;
+            constexpr int BNT = sizeof(R) == 4 ? BNT32 : BNT64;
+            auto k = pm == 0 ? sure_select<R, BNT, 0>
+                   : pm == 1 ? sure_select<R, BNT, 1>
+                   : pm == 2 ? sure_select<R, BNT, 2> : sure_select<R, BNT, 3>;
+            set_smem(k, sm);
+            launch(k, dim3(p->B, (unsigned)li.size()), BNT, sm, ls, p->geo, a);
         }
         if (forked) {
             CK(cudaEventRecord(p->ev_join, p->side));
@@ -530,12 +595,16 @@ struct Seq {
     }
 
     // one VDAMP iteration from (r, par) -> (r, par)   (src/vdamp.py:99-144)
-    void iteration(double* trace, void* snapshot) {
+    void iteration(double* trace, void* snapshot, int k = -1) {
+        NvtxRange nv("vdamp iteration");
+        const bool tm = p->iter_timing && k >= 0 && 2 * k + 1 < (int)p->itev.size();
+        if (tm) CK(record(p->itev[2 * k], st));
         synth(r(), p->par, true, nullptr, 0, true);        // r: written by K3 two kernels back
         col(COL_VDAMP, (const C*)p->T1, (C*)p->T2, 1);
         analysis(nullptr, true, r(), p->par, true, 2);
         if (snapshot) CK(cudaMemcpyAsync(snapshot, p->r, (size_t)p->B * p->N * sizeof(C), cudaMemcpyDeviceToDevice, st));
         select(r(), nullptr, trace, p->have_gt);
+        if (tm) CK(record(p->itev[2 * k + 1], st));
     }
 
     // x_hat = finalize(soft(r; parf))   (src/vdamp.py:147-150)
@@ -626,7 +695,7 @@ struct Seq {
         const long long tstride = (long long)p->B * p->S * TRACE_F;
         if (nmse_out) nmse_begin();
         for (int it = 0; it < n_iters; ++it) {
-            iteration(trace ? trace + it * tstride : nullptr, snaps ? snaps[it] : nullptr);
+            iteration(trace ? trace + it * tstride : nullptr, snaps ? snaps[it] : nullptr, it);
             if (nmse_out) nmse_iter(nmse_out + (long long)it * p->B * VDAMP_NMSE_FIELDS);
         }
         finalize_from_r(p->parf, xhat);
@@ -702,7 +771,7 @@ void free_plan(Plan* p) {
     if (!p) return;
     cudaSetDevice(p->dev);
     void* bufs[] = {p->what, p->btau, p->berr, p->x0r, p->nmconst, p->nmpart, p->r, p->T1, p->T2, p->yg, p->pinv, p->par, p->parf, p->taupart, p->prow, p->pcol, p->prs256,
-                    p->nvar, p->offs, p->twH, p->twW, p->kA, p->kB, p->bhist, p->btick, p->bbest, p->baux, p->berrp, p->x0, p->w0, p->xtmp, p->trtmp};
+                    p->nvar, p->offs, p->twH, p->twW, p->kA, p->kB, p->bhist, p->btick, p->bbest, p->baux, p->berrp, p->x0, p->w0, p->xtmp, p->trtmp, p->pflag};
     for (void* b : bufs) if (b) cudaFree(b);
     for (void* b : p->scratch) if (b) cudaFree(b);
     for (auto& e : p->ev) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
@@ -718,6 +787,7 @@ void free_plan(Plan* p) {
     }
     if (p->lane_start) cudaEventDestroy(p->lane_start);
     if (p->ev_join) cudaEventDestroy(p->ev_join);
+    for (cudaEvent_t e : p->itev) cudaEventDestroy(e);
     if (p->d_merr) cudaFree(p->d_merr);
     if (p->h_merr) cudaFreeHost(p->h_merr);
     if (p->ev_meas) cudaEventDestroy(p->ev_meas);
@@ -864,6 +934,7 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         p->twH = dalloc(p, (size_t)height * cs);
         p->twW = dalloc(p, (size_t)width * cs);
         p->trtmp = (double*)dalloc(p, (size_t)batch * p->S * TRACE_F * sizeof(double));
+        p->pflag = (unsigned*)dalloc(p, (size_t)batch * p->S * sizeof(unsigned));
         const int maxlen = *std::max_element(g.len, g.len + p->S);
         const int capk = precision == VDAMP_FP32 ? Scap<float>::v : Scap<double>::v;
         if (maxlen > capk) {
@@ -1029,6 +1100,30 @@ int vdamp_set_measurements(vdamp_plan_t plan, const void* y, const int64_t* indi
     });
 }
 
+int vdamp_set_iteration_timing(vdamp_plan_t plan, int enable) {
+    return guard([&] {
+        Plan* p = P(plan);
+        if (p->iter_timing != (enable != 0)) drop_graph(p);
+        p->iter_timing = enable != 0;
+    });
+}
+
+int vdamp_iteration_times(vdamp_plan_t plan, int n_iters, double* ms, int* images) {
+    return guard([&] {
+        Plan* p = P(plan);
+        if (!p->iter_timing || n_iters > p->it_count || 2 * n_iters > (int)p->itev.size())
+            throw Err{VDAMP_ERR_STATE, "no iteration times recorded for that many iterations"};
+        CK(cudaSetDevice(p->dev));
+        for (int k = 0; k < n_iters; ++k) {
+            CK(cudaEventSynchronize(p->itev[2 * k + 1]));
+            float t = 0.0f;
+            CK(cudaEventElapsedTime(&t, p->itev[2 * k], p->itev[2 * k + 1]));
+            ms[k] = t;
+        }
+        if (images) *images = p->it_images;
+    });
+}
+
 int vdamp_set_validation(vdamp_plan_t plan, int synchronous) {
     return guard([&] { P(plan)->validate_sync = synchronous != 0; });
 }
@@ -1112,6 +1207,7 @@ Plan lane_view(const Plan* p, int b0, int nb, const Plan::Lane& l) {
     v.taupart = p->taupart + (size_t)b0 * p->ntiles * p->S;
     v.nvar = p->nvar + b0;
     v.trtmp = p->trtmp + (size_t)b0 * p->S * TRACE_F;
+    v.pflag = p->pflag + (size_t)b0 * p->S;
     v.x0 = off(p->x0, ci); v.w0 = off(p->w0, ci); v.x0r = off(p->x0r, ci); v.xtmp = off(p->xtmp, ci);
     if (p->nmconst) v.nmconst = p->nmconst + (size_t)b0 * 2;
     if (p->nmpart) v.nmpart = p->nmpart + (size_t)b0 * p->ntiles;
@@ -1139,6 +1235,7 @@ void lane_merge(Plan* p, Plan& v, long long l0, const long long* c0) {
 
 int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double* nmse, void* const* snapshots,
               void* stream) {
+    NvtxRange nv("vdamp_run");
     return guard([&] {
         Plan* p = P(plan);
         if (n_iters < 1) throw Err{VDAMP_ERR_ARG, "need at least one iteration, got " + std::to_string(n_iters)};
@@ -1148,11 +1245,22 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
         if (!x_hat) throw Err{VDAMP_ERR_ARG, "null x_hat"};
         cudaStream_t caller = (cudaStream_t)stream;
         cudaStream_t st = caller;
+        if (p->iter_timing) {
+            CK(cudaSetDevice(p->dev));
+            if ((int)p->itev.size() < 2 * n_iters) drop_graph(p);     // captured event nodes change
+            while ((int)p->itev.size() < 2 * n_iters) {
+                cudaEvent_t e;
+                CK(cudaEventCreate(&e));
+                p->itev.push_back(e);
+            }
+            p->it_count = n_iters;
+        }
         // image lanes, forked from and joined back into stream cs (also captured into
         // the graph below); diagnostics (trace, NMSE, snapshots) ride on the lanes when
         // they are interleaved (iteration-major): each lane writes its image range of
         // every per-iteration record
         const bool use_lanes = p->lanes > 1 && (p->interleave || (!trace && !nmse && !snapshots));
+        p->it_images = use_lanes ? (int)((long long)p->B / p->lanes) : p->B;
         auto run_lanes = [&](cudaStream_t cs) {
             CK(cudaSetDevice(p->dev));
             CK(cudaEventRecord(p->lane_start, cs));
@@ -1184,7 +1292,7 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
                             double* tr = trace ? trace + it * tstride + b0 * p->S * TRACE_F : nullptr;
                             void* sn = (snapshots && snapshots[it]) ? (void*)((char*)snapshots[it] + (size_t)b0 * p->N * p->csz) : nullptr;
                             dispatch(&vs[li], (void*)p->lane[li].st, [&](auto& s) {
-                                s.iteration(tr, sn);
+                                s.iteration(tr, sn, li == 0 ? it : -1);
                                 if (nmse) s.nmse_iter(nmse + ((long long)it * p->B + b0) * VDAMP_NMSE_FIELDS);
                             });
                         }
@@ -1212,6 +1320,7 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
                 Plan::Lane& l = p->lane[li];
                 CK(cudaStreamWaitEvent(l.st, p->lane_start, 0));
                 Plan v = lane_view(p, b0, b1 - b0, l);
+                v.iter_timing = p->iter_timing && li == 0;
                 long long c0[VDAMP_KERNEL_CLASSES];
                 for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) c0[c] = v.cls_launches[c];
                 const long long l0 = v.launches;
@@ -1251,7 +1360,8 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
         // key: everything baked into the captured launches
         std::vector<const void*> key{(const void*)(intptr_t)n_iters, x_hat, trace, nmse, (const void*)(intptr_t)p->have_gt,
                                      (const void*)(intptr_t)p->timing, (const void*)st,
-                                     (const void*)(intptr_t)(use_lanes ? p->lanes : 1), (const void*)(intptr_t)p->interleave};
+                                     (const void*)(intptr_t)(use_lanes ? p->lanes : 1), (const void*)(intptr_t)p->interleave,
+                                     (const void*)(intptr_t)p->iter_timing};
         if (snapshots) for (int k = 0; k < n_iters; ++k) key.push_back(snapshots[k]);
         else key.push_back(nullptr);
         if (!p->gexec || key != p->gkey) {

@@ -1629,6 +1629,8 @@ struct SelArgs {
     R* kA;                           // [B][N] key scratch (subbands > SCAP)
     R* kB;
     int prune;                       // bound-pruned exact selection (vdamp_prune.cuh): bit 0 4096..SCAP keys, bit 1 larger
+    unsigned* pflag;                 // [B][S] fallback flags of sure_prune32 (1 = sort fully)
+    const unsigned* only;            // non-null: process only the items flagged here
     int item_start[MAXS + 1];        // work items: subbands item_list[item_start[i] .. item_start[i+1])
     int item_list[MAXS];
 };
@@ -2497,9 +2499,9 @@ struct SelShared {
 // smallest key, or 0 to skip them), the argmin over all tiles and candidates
 // (ties -> smaller t) in S_.run, alpha (src/denoise.py:169), the clamp
 // (src/vdamp.py:121-124) and the outputs.
-template <typename R, int NT>
+template <typename R, int NT, typename SS>
 __device__ __forceinline__ void select_finish(const Geo& g, const SelArgs<R>& a, int j, int bi, int n, double tau,
-                                              double m0, bool have_w0, SelShared<NT>& S_) {
+                                              double m0, bool have_w0, SS& S_) {
     const int tid = threadIdx.x;
     __syncthreads();
     __syncthreads();
@@ -2780,7 +2782,7 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
             scan_tile<R, NT, EMAXS, SMEMSUF>(tk, T, t * T, n, tau, tpre[t], tsuf[t], nf, sh, s_best, &S_.run,
                                              &s_totinv, slo, shi, sdbg);
     }
-    select_finish<R, NT>(g, a, j, bi, n, tau, large ? (double)sorted[0] : (double)skeys[0], w0 != nullptr, S_);
+    select_finish<R, NT, SelShared<NT>>(g, a, j, bi, n, tau, large ? (double)sorted[0] : (double)skeys[0], w0 != nullptr, S_);
     PHASE_MARK(2);                                   // argmin + outputs
 }
 
@@ -2790,8 +2792,10 @@ __device__ void select_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R*
 // full sort (select_band) on the subband from scratch.
 // Shared memory: fp32 -- keys | stage | counters as in select_band (the subband
 // lands in stage + counters by TMA); fp64 -- keys (doubles) | counters | scratch + list.
-template <typename R, int NT>
-__device__ __forceinline__ bool prune_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R* keys, SelShared<NT>& S_) {
+// NT < BNT32 (fp32 only, sure_prune32): keys by LDG into shared memory (no TMA landing
+// zone), bucket ids recomputed, a PR_LMAX/2 list -- about 100 KB, two CTAs per SM.
+template <typename R, int NT, typename SS>
+__device__ __forceinline__ bool prune_band(const Geo& g, const SelArgs<R>& a, int j, int bi, R* keys, SS& S_) {
     typedef typename CT<R>::T C;
     typedef typename PrT<R>::U U;
     constexpr int CAPK = Scap<R>::v;
@@ -2812,7 +2816,7 @@ __device__ __forceinline__ bool prune_band(const Geo& g, const SelArgs<R>& a, in
     unsigned* cnt;
     double* rsh;
     unsigned short* bid;
-    const bool large = n > CAPK;
+    const bool large = NT >= BNT32 && n > CAPK;
     if (large) {
         // keys to global scratch (L2-resident); the shared key region holds the list
         R* ka = a.kA + base;
@@ -2848,7 +2852,7 @@ __device__ __forceinline__ bool prune_band(const Geo& g, const SelArgs<R>& a, in
             }
         }
         __syncthreads();
-    } else if constexpr (sizeof(R) == 4) {
+    } else if constexpr (sizeof(R) == 4 && NT >= BNT32) {
         R* stage = keys + SLOT;
         cnt = reinterpret_cast<unsigned*>(stage + SLOT);
         rsh = reinterpret_cast<double*>(stage);
@@ -2884,8 +2888,13 @@ __device__ __forceinline__ bool prune_band(const Geo& g, const SelArgs<R>& a, in
         if (tid == 0) S_.mphase ^= 1u;
     } else {
         cnt = reinterpret_cast<unsigned*>(keys + SLOT);
-        bid = reinterpret_cast<unsigned short*>(cnt + PR_NC + PR_NF + 32);
-        rsh = reinterpret_cast<double*>(bid + PR_BIDN);
+        if constexpr (NT >= BNT32) {
+            bid = reinterpret_cast<unsigned short*>(cnt + PR_NC + PR_NF + 32);
+            rsh = reinterpret_cast<double*>(bid + PR_BIDN);
+        } else {
+            bid = nullptr;
+            rsh = reinterpret_cast<double*>(cnt + PR_NC + PR_NF + 32);
+        }
         constexpr int LB = 8;                                  // loads in flight per thread
         for (int e0 = tid; e0 < n; e0 += LB * NT) {
             C v[LB];
@@ -2930,13 +2939,20 @@ __device__ __forceinline__ bool prune_band(const Geo& g, const SelArgs<R>& a, in
 #endif
     PrOut po{0, 0.0};
     bool ok;
-    if (large) ok = select_pruned<R, NT, 0, SelShared<NT>, true>(n, tau, a.kA + base, cnt, bid, plist, rsh, kmn, kmx,
-                                                                 S_, po, pdbg);
-    else if (ef == 16) ok = select_pruned<R, NT, 16>(n, tau, keys, cnt, bid, plist, rsh, kmn, kmx, S_, po, pdbg);
-    else if (ef == 8) ok = select_pruned<R, NT, 8>(n, tau, keys, cnt, bid, plist, rsh, kmn, kmx, S_, po, pdbg);
-    else ok = select_pruned<R, NT, 4>(n, tau, keys, cnt, bid, plist, rsh, kmn, kmx, S_, po, pdbg);
+    const int lmax = large ? SCAP : NT >= BNT32 ? pr_lmax<R>() : PR_LMAX / 2;
+    if constexpr (NT >= BNT32) {
+        if (large) ok = select_pruned<R, NT, 0, SS, true>(n, tau, a.kA + base, cnt, bid, plist, lmax, rsh, kmn, kmx,
+                                                          S_, po, pdbg);
+        else if (ef == 16) ok = select_pruned<R, NT, 16>(n, tau, keys, cnt, bid, plist, lmax, rsh, kmn, kmx, S_, po, pdbg);
+        else if (ef == 8) ok = select_pruned<R, NT, 8>(n, tau, keys, cnt, bid, plist, lmax, rsh, kmn, kmx, S_, po, pdbg);
+        else ok = select_pruned<R, NT, 4>(n, tau, keys, cnt, bid, plist, lmax, rsh, kmn, kmx, S_, po, pdbg);
+    } else {
+        if (ef == 32) ok = select_pruned<R, NT, 32>(n, tau, keys, cnt, bid, plist, lmax, rsh, kmn, kmx, S_, po, pdbg);
+        else if (ef == 16) ok = select_pruned<R, NT, 16>(n, tau, keys, cnt, bid, plist, lmax, rsh, kmn, kmx, S_, po, pdbg);
+        else ok = select_pruned<R, NT, 8>(n, tau, keys, cnt, bid, plist, lmax, rsh, kmn, kmx, S_, po, pdbg);
+    }
     if (!ok) return false;
-    select_finish<R, NT>(g, a, j, bi, n, tau, po.nbelow == 0 ? po.m0 : 0.0, w0 != nullptr, S_);
+    select_finish<R, NT, SS>(g, a, j, bi, n, tau, po.nbelow == 0 ? po.m0 : 0.0, w0 != nullptr, S_);
     return true;
 }
 
@@ -2947,9 +2963,45 @@ __device__ __noinline__ void select_band_call(const Geo& g, const SelArgs<R>& a,
     select_band<R, NT>(g, a, j, bi, keys, S_);
 }
 
-// PRUNE: the bound-pruned path first (vdamp_prune.cuh), the full sort as an out-of-line
-// fallback; otherwise the full sort inline (the code the fp32 default runs)
-template <typename R, int NT, bool PRUNE = false>
+// Shared state of sure_prune32 (the fields prune_band / select_finish / scan_tile use)
+template <int NT>
+struct PrShared {
+    unsigned long long mbar;
+    unsigned mphase;
+    double sh[66 + NT / 32 + 2];
+    double tpart[PR_MAXT];
+    double tau, totinv;
+    Best best[NT / 32];
+    Best run;
+    double err, ref;
+};
+
+// Bound-pruned selection of fp32 subbands of 4,096..SCAP keys in 512-thread CTAs with
+// ~100 KB of shared memory: two CTAs (two subbands) per SM, so one CTA's barrier and
+// reduction latency overlaps the other's work.  A subband the bounds cannot settle is
+// flagged in a.pflag and sorted fully by the sure_select launch that follows (a.only).
+template <int NT>
+__global__ void __launch_bounds__(NT, 2) sure_prune32(const __grid_constant__ Geo g,
+                                                      const __grid_constant__ SelArgs<float> a) {
+    pdl_enter();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* keys = reinterpret_cast<float*>(smem_raw);
+    __shared__ PrShared<NT> S_;
+    const int bi = blockIdx.x, it = blockIdx.y;
+    if (threadIdx.x == 0) { mbar_init(&S_.mbar, 1); S_.mphase = 0; }
+    __syncthreads();
+    for (int q = a.item_start[it]; q < a.item_start[it + 1]; ++q) {
+        const int j = a.item_list[q];
+        const bool ok = prune_band<float, NT>(g, a, j, bi, keys, S_);
+        if (threadIdx.x == 0) a.pflag[(long long)bi * g.S + j] = ok ? 0u : 1u;
+        __syncthreads();
+    }
+}
+
+// PM (prune mask, bit 0: subbands of 4,096..SCAP keys, bit 1: larger ones): those take
+// the bound-pruned path first (vdamp_prune.cuh) with the full sort as an out-of-line
+// fallback; the others run the full sort inline (PM = 0: the fp32 default kernel)
+template <typename R, int NT, int PM = 0>
 __global__ void __launch_bounds__(NT, NT >= BNT32 ? 1 : 4) sure_select(const __grid_constant__ Geo g,
                                                                        const __grid_constant__ SelArgs<R> a) {
     pdl_enter();
@@ -2962,13 +3014,17 @@ __global__ void __launch_bounds__(NT, NT >= BNT32 ? 1 : 4) sure_select(const __g
     // one work item = one large subband, or several small ones packed to ~SCAP keys
     for (int q = a.item_start[it]; q < a.item_start[it + 1]; ++q) {
         const int j = a.item_list[q];
-        if constexpr (PRUNE && NT >= BNT32) {
+        if (a.only && !a.only[(long long)bi * g.S + j]) continue;   // pruned already (uniform per CTA)
+        if constexpr (PM != 0 && NT >= BNT32) {
             const int n = g.len[j];
-            bool done = false;
-            // a.prune: bit 0 subbands of 4,096..SCAP keys, bit 1 larger ones
-            if (n >= 4096 && n % NT == 0 && (n / NT) % 4 == 0 && (a.prune & (n > Scap<R>::v ? 2 : 1)))
-                done = prune_band<R, NT>(g, a, j, bi, keys, S_);
-            if (!done) select_band_call<R, NT>(g, a, j, bi, keys, S_);
+            const int bit = n > Scap<R>::v ? 2 : 1;
+            if ((PM & bit) && n >= 4096 && n % NT == 0 && (n / NT) % 4 == 0) {
+                if (!prune_band<R, NT>(g, a, j, bi, keys, S_)) select_band_call<R, NT>(g, a, j, bi, keys, S_);
+            } else if (PM == 2 && bit == 1) {
+                select_band<R, NT>(g, a, j, bi, keys, S_);        // small subbands inline (fp32 cfg2)
+            } else {
+                select_band_call<R, NT>(g, a, j, bi, keys, S_);
+            }
         } else {
             select_band<R, NT>(g, a, j, bi, keys, S_);
         }

@@ -54,6 +54,8 @@ constexpr int PR_LMAX = 4096;     // keys evaluated exactly at most (else the fu
 template <typename R> __host__ __device__ constexpr int pr_lmax() { return sizeof(R) == 4 ? PR_LMAX : PR_LMAX / 2; }
 constexpr int PR_NC = 1024;       // coarse buckets (one per thread)
 constexpr int PR_NF = 4096;       // fine buckets over the coarse span (four per thread)
+constexpr int PR_NT32 = 512;      // threads of sure_prune32 (two CTAs per SM)
+constexpr int PR_MAXT = 256;      // tau column-tile partials sure_prune32 holds (more: the 1024-thread path)
 constexpr int PR_BIDN = 16384 + 16384 / 32 + 8;   // bucket-id slots (KI layout, n <= 16384)
 // fp32 layout of the stage region: reduction scratch (168 doubles) | list | bucket ids
 constexpr int PR_STAGE_BID = (5 * 32 + 8) * 8 + ((PR_LMAX + PR_LMAX / 32 + 8) * 4 + 15) / 16 * 16;
@@ -340,27 +342,100 @@ __device__ __forceinline__ double pr_ub(double pu, double cge, double A, double 
     return pu + cge * A * A + 2.0 * tau * cge - tau * A * il;
 }
 
-// keys: n keys of this subband at keys[KI(tid + q * NT)], q < EF (n == EF * NT).
-// cnt: >= PR_NC + PR_NF + 32 words.  bid: n + n/32 shorts (coarse bucket per key).
-// list: PR_LMAX + 1 + pad keys.  sh: >= 5 * NT/32 + 8 doubles.  Runs scan_tile
-// over the list (S_.run, S_.totinv).  Returns false (scratch regions clobbered,
-// keys intact) when the caller must sort all keys.
+// One bounds level over buckets [0, K*NT) of map M (K per thread, counts in cnt, only
+// buckets [flo, ftop) belong to the range): exclusive scans of the edge sums, upper
+// bounds of the risk at every lower edge (t = 0 exact when flo == 0; beyond the largest
+// key when `top`), U = their minimum (never above Uprev), then the buckets whose lower
+// bound is <= U + margin -> [w0, w1].  pbf / iaf / cblf: squares below the range,
+// inverses above it, keys below it.  Returns the margin-widened U.
+template <int NT, int K, typename MapT>
+__device__ __forceinline__ float pr_stage(const unsigned* cnt, const MapT& M, int flo, int ftop, bool top, float pbf,
+                                          float iaf, float cblf, int n, float tauf, float ntauf, float Uprev,
+                                          float* shf, int& w0, int& w1) {
+    const int tid = threadIdx.x;
+    const int b0 = K * tid;
+    float cv[K], A[K + 1], ivs[K], ibs[K];
+#pragma unroll
+    for (int i = 0; i <= K; ++i) A[i] = (float)M.edge(b0 + i);
+    float f[3] = {0.0f, 0.0f, 0.0f}, r[2] = {0.0f, 0.0f};
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        const int b = b0 + i;
+        const float c = (b >= flo && b < ftop) ? (float)cnt[b] : 0.0f;
+        cv[i] = c;
+        f[0] = fmaf(c * A[i], A[i], f[0]);
+        f[1] = fmaf(c * A[i + 1], A[i + 1], f[1]);
+        ivs[i] = (b >= 1 && c > 0.0f) ? c * __frcp_ru(A[i]) : 0.0f;
+        ibs[i] = (b >= 1 && c > 0.0f && A[i + 1] < INFINITY) ? c * __frcp_rd(A[i + 1]) : 0.0f;
+        r[0] += ivs[i];
+        r[1] += ibs[i];
+        f[2] += c;
+    }
+    const float own_b2 = f[1];
+    pr_scanf<NT, 3, 2>(f, r, shf);
+    float sufa[K], sufb[K];
+    {
+        float s2 = iaf + r[0], s3 = iaf + r[1];
+#pragma unroll
+        for (int i = K - 1; i >= 0; --i) { sufa[i] = s2; s2 += ivs[i]; s3 += ibs[i]; sufb[i] = s3; }
+    }
+    float ub = INFINITY;
+    {
+        float p = pbf + f[1], cbelow = cblf + f[2];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const int b = b0 + i;
+            if (b >= flo && b < ftop && b >= 1)
+                ub = fminf(ub, pr_ubf(p, (float)n - cbelow, A[i], sufb[i], tauf) - ntauf);
+            p = fmaf(cv[i] * A[i + 1], A[i + 1], p);
+            cbelow += cv[i];
+        }
+    }
+    if (flo == 0 && tid == 0) ub = fminf(ub, 2.0f * tauf * ((float)n - cv[0]) - ntauf);   // t = 0, exact
+    float scale = 0.0f, z0 = 0.0f, z1 = 0.0f;
+    if (tid == NT - 1) {
+        scale = pbf + f[1] + own_b2;                   // all squares below the range top, upper edges
+        if (top) ub = fminf(ub, scale - ntauf);          // t beyond the largest key
+    }
+    pr_reducef<NT>(scale, z0, z1, ub, shf);
+    const float Ulim = fminf(Uprev, ub + 1e-5f * (fabsf(ub) + 2.0f * ntauf + scale));
+    w0 = 0x7fffffff;
+    w1 = -1;
+    {
+        float p = pbf + f[0], cbelow = cblf + f[2];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const int b = b0 + i;
+            const float cu = (float)n - cbelow - cv[i];
+            const float lb = pr_lbf(p, cv[i], A[i], A[i + 1], cu, sufa[i], tauf) - ntauf;
+            if (b >= flo && b < ftop && lb <= Ulim) { w0 = min(w0, b); w1 = max(w1, b); }
+            p = fmaf(cv[i] * A[i], A[i], p);
+            cbelow += cv[i];
+        }
+    }
+    pr_minmax<NT>(w0, w1, reinterpret_cast<int*>(shf));
+    return Ulim;
+}
+
+// keys: n keys of this subband at keys[KI(tid + q * NT)], q < EF (n == EF * NT), or
+// (GLOBAL) at keys[e] in L2-resident global scratch with ef = n / NT at run time.
+// cnt: >= PR_NC + PR_NF + 32 words.  bid: n + n/32 shorts (coarse bucket per key), or
+// null (recomputed).  list: lmax + pad keys.  sh: >= 5 * NT/32 + 8 doubles.  Runs
+// scan_tile over the list (S_.run, S_.totinv).  Returns false (scratch regions
+// clobbered, keys intact) when the caller must sort all keys.
 //
 // Bounds are evaluated in float: every term of a bound is at most the sum of
 // all squares plus 2 n tau in magnitude (keys above t satisfy m > t, so
 // c t^2 <= their squares and tau t sum(1/m) <= n tau), and float rounding of the
 // sums and products stays far below the 1e-5 relative margin added to U.
-// GLOBAL: the keys are n = ef * NT keys in (L2-resident) global scratch at keys[e]
-// (subbands larger than the shared-memory sort), bucket ids are recomputed, the
-// list holds up to SCAP keys; EF is then 0 and ef a runtime count.
 template <typename R, int NT, int EF, typename SS, bool GLOBAL = false>
 __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, unsigned short* bid, R* list,
-                              double* sh, typename PrT<R>::U kmn, typename PrT<R>::U kmx, SS& S_, PrOut& out,
-                              long long* dbg = nullptr) {
+                              int lmax, double* sh, typename PrT<R>::U kmn, typename PrT<R>::U kmx, SS& S_,
+                              PrOut& out, long long* dbg = nullptr) {
+    static_assert(PR_NC % NT == 0 && PR_NF % NT == 0, "whole buckets per thread");
+    constexpr int KC = PR_NC / NT, KF = PR_NF / NT;
     const int ef = GLOBAL ? n / NT : EF;
-    constexpr int LMAXK = GLOBAL ? SCAP : pr_lmax<R>();
     auto key = [&](int e) -> R { if constexpr (GLOBAL) return __ldcg(keys + e); else return keys[KI(e)]; };
-    static_assert(NT == PR_NC && PR_NF == 4 * NT, "one coarse bucket and four fine buckets per thread");
     typedef typename PrT<R>::U U;
 #ifdef VDAMP_PHASE_TIMING
     long long pc0_ = clock64();
@@ -384,9 +459,7 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
     U* ur = reinterpret_cast<U*>(sh);
     __syncthreads();
     if ((tid & 31) == 0) { ur[tid >> 5] = kmn; ur[NW + (tid >> 5)] = kmx; }
-    cc[tid] = 0u;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) cf[tid + i * NT] = 0u;
+    for (int i = tid; i < PR_NC + PR_NF; i += NT) cnt[i] = 0u;
     if (tid == 0) *lc = 1u;                      // list slot 0: the largest key below the window
     __syncthreads();
     U mn, mx;
@@ -419,49 +492,17 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
     for (int q = 0; q < ef; ++q) {
         const int e = tid + q * NT;
         const int b = C.bucket(PrT<R>::bits(key(e)));
-        if constexpr (!GLOBAL) bid[KI(e)] = (unsigned short)b;
+        if (bid) bid[KI(e)] = (unsigned short)b;
         atomicAdd(&cc[b], 1u);
     }
     __syncthreads();
     PR_MARK(0);
 
-    // ---- 2. coarse bounds (thread t = bucket t) -> span [g0, g1] ----------------
-    // upper-edge sums are bounded by lower-edge ones: within a linear bucket the upper
-    // edge is at most 2^ls units in the last place of A above A (twice that across an
-    // exponent boundary), so B <= rho A with rho = 1 + 2^(ls - MB + 1), rho^2 <= 1 + 3x
+    // ---- 2. coarse bounds -> span [g0, g1] -------------------------------------
     int g0, g1;
-    float Ulim;
-    {
-        const unsigned ci = cc[tid];
-        const float c = (float)ci;
-        const float A = (float)C.edge(tid), B = (float)C.edge(tid + 1);
-        const float rho2 = 1.0f + 3.0f * ldexpf(1.0f, C.ls - PrT<R>::MB + 1);
-        // zeros / below-range buckets: bounded by their own upper edges
-        const float c0 = (float)cc[0], c1 = (float)cc[1];
-        const float e1 = (float)C.edge(1), e2 = (float)C.edge(2);
-        const float low = c0 * e1 * e1 + c1 * e2 * e2;
-        const float cA = (tid >= 1 && ci) ? c * __frcp_ru(A) : 0.0f;     // c / A, rounded up (margin)
-        float f[2] = {c * A * A, c}, r[1] = {cA};
-        pr_scanf<NT, 2, 1>(f, r, shf);
-        const float pl = f[0], cb = f[1], iu = r[0];
-        const float cu = (float)n - cb - c;
-        const float lb = pr_lbf(pl, c, A, B, cu, iu, tauf) - ntauf;
-        // upper bound at t = A (linear buckets): squares below <= rho^2 pl + low,
-        // inverses of the keys at or above A >= (iu + c/A) / rho^2
-        float ub = INFINITY;
-        if (tid >= 2) ub = pr_ubf(rho2 * pl + low, (float)n - cb, A, (iu + cA) / rho2, tauf) - ntauf;
-        if (tid == 0) ub = fminf(ub, 2.0f * tauf * ((float)n - c) - ntauf);   // t = 0
-        float scale = 0.0f, z0 = 0.0f, z1 = 0.0f;
-        if (tid == NT - 1) { scale = rho2 * (pl + c * A * A) + low; ub = fminf(ub, scale - ntauf); }
-        pr_reducef<NT>(scale, z0, z1, ub, shf);
-        Ulim = ub + 1e-5f * (fabsf(ub) + 2.0f * ntauf + scale);
-        g0 = lb <= Ulim ? tid : 0x7fffffff;
-        g1 = lb <= Ulim ? tid : -1;
-        pr_minmax<NT>(g0, g1, reinterpret_cast<int*>(sh));
-        if (g1 < 0) return false;
-    }
+    const float Ulim = pr_stage<NT, KC>(cc, C, 0, PR_NC, true, 0.0f, 0.0f, 0.0f, n, tauf, ntauf, INFINITY, shf, g0, g1);
+    if (g1 < 0) return false;
     PR_MARK(1);
-    
 
     // ---- 3. float sums outside the span, fine histogram inside ----------------
     PrMap<R> F;
@@ -482,7 +523,7 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
     for (int q = 0; q < ef; ++q) {
         const int e = tid + q * NT;
         const R m = key(e);
-        const int b = GLOBAL ? C.bucket(PrT<R>::bits(m)) : bid[KI(e)];
+        const int b = bid ? (int)bid[KI(e)] : C.bucket(PrT<R>::bits(m));
         const float mf = (float)m;
         pbf = b < g0 ? fmaf(mf, mf, pbf) : pbf;
         cblf += b < g0 ? 1.0f : 0.0f;
@@ -492,65 +533,10 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
     pr_reducef<NT>(pbf, iaf, cblf, zz, shf);
     PR_MARK(2);
 
-    // ---- 4. fine bounds (thread t: fine buckets 4t .. 4t+3) -> window [f0, f1] --
+    // ---- 4. fine bounds -> window [f0, f1] ---------------------------------------
     int f0, f1;
-    {
-        const int fb0 = 4 * tid;
-        float cv[4], A[5], ivs[4];
-#pragma unroll
-        for (int i = 0; i < 5; ++i) A[i] = (float)F.edge(fb0 + i);
-        float f[3] = {0.0f, 0.0f, 0.0f}, r[2] = {0.0f, 0.0f};
-        float ibs[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int fb = fb0 + i;
-            const float c = (fb >= flo && fb < F.top) ? (float)cf[fb] : 0.0f;
-            cv[i] = c;
-            f[0] = fmaf(c * A[i], A[i], f[0]);
-            f[1] = fmaf(c * A[i + 1], A[i + 1], f[1]);
-            ivs[i] = (fb >= 1 && c > 0.0f) ? c * __frcp_ru(A[i]) : 0.0f;
-            ibs[i] = (fb >= 1 && c > 0.0f && A[i + 1] < INFINITY) ? c * __frcp_rd(A[i + 1]) : 0.0f;
-            r[0] += ivs[i];
-            r[1] += ibs[i];
-            f[2] += c;
-        }
-        pr_scanf<NT, 3, 2>(f, r, shf);
-        float sufa[4], sufb[4];
-        {
-            float s2 = iaf + r[0], s3 = iaf + r[1];
-#pragma unroll
-            for (int i = 3; i >= 0; --i) { sufa[i] = s2; s2 += ivs[i]; s3 += ibs[i]; sufb[i] = s3; }
-        }
-        float ub = INFINITY;
-        {
-            float p = pbf + f[1], cbelow = cblf + f[2];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int fb = fb0 + i;
-                if (fb >= flo && fb < F.top && fb >= 2)
-                    ub = fminf(ub, pr_ubf(p, (float)n - cbelow, A[i], sufb[i], tauf) - ntauf);
-                p = fmaf(cv[i] * A[i + 1], A[i + 1], p);
-                cbelow += cv[i];
-            }
-        }
-        float z3 = 0.0f, z4 = 0.0f, z5 = 0.0f;
-        pr_reducef<NT>(z3, z4, z5, ub, shf);
-        const float ul2 = fminf(Ulim, ub + 1e-5f * (fabsf(ub) + 2.0f * ntauf + pbf + f[1]));
-        float p = pbf + f[0], cbelow = cblf + f[2];
-        f0 = 0x7fffffff;
-        f1 = -1;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int fb = fb0 + i;
-            const float cu = (float)n - cbelow - cv[i];
-            const float lb = pr_lbf(p, cv[i], A[i], A[i + 1], cu, sufa[i], tauf) - ntauf;
-            if (fb >= flo && fb < F.top && lb <= ul2) { f0 = min(f0, fb); f1 = max(f1, fb); }
-            p = fmaf(cv[i] * A[i], A[i], p);
-            cbelow += cv[i];
-        }
-        pr_minmax<NT>(f0, f1, reinterpret_cast<int*>(sh));
-        if (f1 < 0) return false;
-    }
+    pr_stage<NT, KF>(cf, F, flo, F.top, false, pbf, iaf, cblf, n, tauf, ntauf, Ulim, shf, f0, f1);
+    if (f1 < 0) return false;
     PR_MARK(3);
 
     // ---- 5. exact float64 offsets (all keys), list gather, sort, scan ---------
@@ -559,14 +545,14 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
     for (int q = 0; q < ef; ++q) {
         const int e = tid + q * NT;
         const R m = key(e);
-        const int b = GLOBAL ? C.bucket(PrT<R>::bits(m)) : bid[KI(e)];
+        const int b = bid ? (int)bid[KI(e)] : C.bucket(PrT<R>::bits(m));
         const int fb = (b < g0) ? -1 : (b > g1) ? 0x7fffffff : F.bucket(PrT<R>::bits(m));
         const double md = (double)m;
         if (fb < f0) { pre = fma(md, md, pre); nbl += 1.0; mprev = fmax(mprev, md); }
         else if (fb > f1) { suf += PrT<R>::rcp(md); nxt = fmin(nxt, md); }
         else {
             const unsigned pos = atomicAdd(lc, 1u);
-            if (pos < (unsigned)LMAXK) list[KI(pos)] = m;
+            if (pos < (unsigned)lmax) list[KI(pos)] = m;
         }
     }
     pr_reduce5<NT>(pre, suf, nbl, nxt, mprev, sh);
@@ -575,7 +561,7 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
     PR_MARK(4);
     PR_NOTE(7, Lw);
     // the padded list (a power of two >= Lw + 1) must fit the list buffer
-    if (Lw + 1 > LMAXK || Lw + (prev ? 1 : 0) < 1) return false;
+    if (Lw + 1 > lmax || Lw + (prev ? 1 : 0) < 1) return false;
     // offsets: squares below the list (all keys below but one instance of mprev, the
     // list's first element; its ties stay below), inverses above it
     const double pre_list = prev ? pre - mprev * mprev : 0.0;
@@ -590,7 +576,7 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
     PR_MARK(5);
     if (tid == 0) S_.run = Best{INFINITY, INFINITY, 0.0, 0.0};
     const int Lr = Lw + (prev ? 1 : 0);          // real keys
-    if (!GLOBAL || Lp <= 4 * NT)
+    if (Lp <= 4 * NT)
         scan_tile<R, NT, 4, false, 4, true>(list, Lr, nb, n, tau, pre_list, suf, nxt, S_.sh, S_.best, &S_.run,
                                             &S_.totinv, nullptr, nullptr);
     else

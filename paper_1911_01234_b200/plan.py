@@ -206,6 +206,16 @@ class Plan:
         the lanes too (each lane writes its image range)."""
         _lib.check(_lib.load().vdamp_set_lanes(self.handle, int(lanes)))
 
+    def set_iteration_timing(self, enable: bool):
+        _lib.check(_lib.load().vdamp_set_iteration_timing(self.handle, int(bool(enable))))
+
+    def iteration_times(self, n_iters):
+        """(ms per iteration, images sharing each timed stream) of the last vdamp_run."""
+        ms = (ctypes.c_double * n_iters)()
+        im = ctypes.c_int()
+        _lib.check(_lib.load().vdamp_iteration_times(self.handle, int(n_iters), ms, ctypes.byref(im)))
+        return np.array(ms[:], dtype=np.float64), int(im.value)
+
     def launch_count(self, reset=False) -> int:
         v = ctypes.c_int64()
         _lib.check(_lib.load().vdamp_launch_count(self.handle, ctypes.byref(v), int(bool(reset))))

@@ -116,7 +116,8 @@ def _records(trace_np, nmse_np, b, n_iters, wall):
         tau = tr[:, 0].copy()
         lam = tr[:, 2].copy()
         rec = IterationRecord(
-            k=k, wall_time=wall, tau=tau, thresholds=lam * tau, lambdas=lam,
+            k=k, wall_time=float(wall[k]) if np.ndim(wall) else float(wall), tau=tau, thresholds=lam * tau,
+            lambdas=lam,
             alphas=tr[:, 3].copy(), alpha_clamped=bool(np.any(tr[:, 5] != 0)))
         if nmse_np is not None:
             rec.nmse_db = _nmse_db(float(nmse_np[k, b, 0]), float(nmse_np[k, b, 1]))
@@ -158,13 +159,12 @@ def run_batch(ys, masks, pmaps, noise_vars, scales, n_iters, ground_truths=None,
     nmse = (torch.zeros((n_iters, B, _lib.NMSE_FIELDS), dtype=torch.float64, device=plan.device)
             if gt is not None else None)
     snaps = {k: plan.empty_coeffs() for k in keep_r_iters if 0 <= k < n_iters} or None
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
+    plan.set_iteration_timing(True)
     x = plan.run(n_iters, trace=trace, nmse=nmse, snapshots=snaps)
-    e1.record()
-    e1.synchronize()
-    wall = e0.elapsed_time(e1) / 1e3 / n_iters
+    ms, images = plan.iteration_times(n_iters)
+    plan.set_iteration_timing(False)
+    # each iteration's own device time (src/vdamp.py:176-179), per image of its stream
+    wall = ms / 1e3 / max(images, 1)
     trace_np = trace.cpu().numpy()
     nmse_np = nmse.cpu().numpy() if nmse is not None else None
     traces = []

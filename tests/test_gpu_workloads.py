@@ -418,3 +418,19 @@ def test_fp32_threshold_is_exact_argmin_of_its_data(oracle, name, steps):
             # only an exact near-tie of the risk may pick another candidate
             assert exact_or_tie(oracle, m, tau, float(g.thresholds[j])), (k, j)
         rt = st.r_tilde
+
+
+def test_iteration_wall_times():
+    """Each IterationRecord carries its own iteration's device time (src/vdamp.py:176-179),
+    not a mean: positive, not all equal, and summing to about the loop's time."""
+    import time
+    from paper_1911_01234_b200 import vdamp, workload
+    w = workload.make_workload("cfg1", batch=1)
+    vdamp.run(w.ys[0], w.masks[0], w.pmap, w.noise_vars[0], 4, 10, precision="fp32")   # warm
+    t0 = time.perf_counter()
+    _, tr = vdamp.run(w.ys[0], w.masks[0], w.pmap, w.noise_vars[0], 4, 10, precision="fp32")
+    wall = time.perf_counter() - t0
+    wt = np.array([r.wall_time for r in tr.records])
+    assert wt.shape == (10,) and np.all(wt > 0)
+    assert len(np.unique(wt)) > 1
+    assert wt.sum() < wall

@@ -16,4 +16,4 @@ for k in a.files:
         print('$c', k, 'x_hat bitwise', np.array_equal(x, y), 'rel', np.linalg.norm(x - y) / np.linalg.norm(x))
 PY
 done
-for v in 2 3; do VDAMP_PRUNE=$v python bench.py --no-extras --no-cpu-baseline --steps 10 --quick; done
+for v in 0 1; do VDAMP_PRUNE=$v python bench.py --no-extras --no-cpu-baseline --steps 10 --quick; done
