@@ -432,8 +432,10 @@ template <typename R, int NT, int EF, typename SS, bool GLOBAL = false>
 __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, unsigned short* bid, R* list,
                               int lmax, double* sh, typename PrT<R>::U kmn, typename PrT<R>::U kmx, SS& S_,
                               PrOut& out, long long* dbg = nullptr) {
-    static_assert(PR_NC % NT == 0 && PR_NF % NT == 0, "whole buckets per thread");
-    constexpr int KC = PR_NC / NT, KF = PR_NF / NT;
+    // four fine buckets per thread (a 512-thread CTA uses 2,048: eight would spill)
+    constexpr int NF = 4 * NT;
+    static_assert(PR_NC % NT == 0 && NF <= PR_NF, "whole buckets per thread");
+    constexpr int KC = PR_NC / NT, KF = NF / NT;
     const int ef = GLOBAL ? n / NT : EF;
     auto key = [&](int e) -> R { if constexpr (GLOBAL) return __ldcg(keys + e); else return keys[KI(e)]; };
     typedef typename PrT<R>::U U;
@@ -459,7 +461,7 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
     U* ur = reinterpret_cast<U*>(sh);
     __syncthreads();
     if ((tid & 31) == 0) { ur[tid >> 5] = kmn; ur[NW + (tid >> 5)] = kmx; }
-    for (int i = tid; i < PR_NC + PR_NF; i += NT) cnt[i] = 0u;
+    for (int i = tid; i < PR_NC + NF; i += NT) cnt[i] = 0u;
     if (tid == 0) *lc = 1u;                      // list slot 0: the largest key below the window
     __syncthreads();
     U mn, mx;
@@ -488,7 +490,7 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
         C.ls = ls;
         C.top = PR_NC;
     }
-#pragma unroll (GLOBAL ? 4 : EF)
+#pragma unroll (GLOBAL ? 4 : (EF > 16 ? 8 : EF))
     for (int q = 0; q < ef; ++q) {
         const int e = tid + q * NT;
         const int b = C.bucket(PrT<R>::bits(key(e)));
@@ -513,13 +515,13 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
         const U fe = C.lo + ((U)(g1 >= 2 ? g1 - 1 : 0) << C.ls);   // one past the span's top bit
         int ls = 0;
         if (fe > F.base)
-            while (((fe - 1 - F.base) >> ls) > (U)(PR_NF - 3)) ++ls;
+            while (((fe - 1 - F.base) >> ls) > (U)(NF - 3)) ++ls;
         F.ls = ls;
         F.top = fe > F.base ? 3 + (int)((fe - 1 - F.base) >> ls) : 2;
     }
     const int flo = g0 >= 2 ? 2 : g0;            // first fine bucket that belongs to the span
     float pbf = 0.0f, iaf = 0.0f, cblf = 0.0f, zz = INFINITY;
-#pragma unroll (GLOBAL ? 4 : EF)
+#pragma unroll (GLOBAL ? 4 : (EF > 16 ? 8 : EF))
     for (int q = 0; q < ef; ++q) {
         const int e = tid + q * NT;
         const R m = key(e);
@@ -541,7 +543,7 @@ __device__ bool select_pruned(int n, double tau, const R* keys, unsigned* cnt, u
 
     // ---- 5. exact float64 offsets (all keys), list gather, sort, scan ---------
     double pre = 0.0, suf = 0.0, nbl = 0.0, nxt = INFINITY, mprev = -INFINITY;
-#pragma unroll (GLOBAL ? 4 : EF)
+#pragma unroll (GLOBAL ? 4 : (EF > 16 ? 8 : EF))
     for (int q = 0; q < ef; ++q) {
         const int e = tid + q * NT;
         const R m = key(e);

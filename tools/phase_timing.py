@@ -9,7 +9,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg1"
 nb = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 w = workload.make_workload(cfg, batch=nb)
 NIT = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, w.config.scales, NIT, precision="fp32")
+vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, w.config.scales, NIT, precision=os.environ.get("PREC", "fp32"))
 buf = (ctypes.c_longlong * (64 * 64 * 4))()
 lib = _lib.load()
 lib.vdamp_debug_phase_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
