@@ -1,22 +1,28 @@
 #!/usr/bin/env python
 """VDAMP image-iterations/s on B200 (BASELINE.json metric), one process per GPU.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1] [--precision fp32|fp64]
+                    [--impl ours|reference] [--no-extras] [--with-trace]
 
 A step = one VDAMP reconstruction (setup scatter, 30 iterations, finalize)
 of one batch of synthetic slices of ``--config`` (default cfg1: 64 x 256^2
 complex64, Haar s=4, R=4, 40 dB).  Each rank reconstructs its own batch of
 distinct slices (weak scaling, no collective in the data path).
 
-value    device-resident: inputs already in HBM, CUDA events per step, L2
-         flushed (256 MiB write) between steps, max over ranks.
-e2e      the public BatchReconstructor call with pinned host inputs; H2D of
-         y / indices / density and D2H of x_hat inside the timed region.
-roofline dominant kernel class: algorithmic bytes / its
-         CUDA-event time inside the timed region, vs MEASURED_PEAKS hbm_gbs.
-cpu_baseline  the numpy oracle port (oracle/vdamp_oracle.py) on a bounded
-         sample of the same slices, one slice per process, all host cores.
---impl reference  times that oracle port alone (rank 0; other ranks exit 0).
+value        device-resident: inputs already in HBM, CUDA events per step, L2
+             flushed (256 MiB write) between steps, max over ranks.
+e2e          the public StreamingReconstructor with pinned host inputs; H2D of
+             y / indices / density and D2H of x_hat inside the timed region.
+fixed_batch  BASELINE's "64 slices sharded across 1/2/4/8 GPUs": the config's
+             batch split over the ranks, dist.gather of x_hat to rank 0 timed.
+configs      (1 GPU) the other BASELINE configs and the fp64 parity mode, each
+             device-resident with its own B_iter roofline.
+roofline     dominant kernel class: algorithmic bytes / its
+             CUDA-event time inside the timed region, vs MEASURED_PEAKS hbm_gbs.
+cpu_baseline the numpy oracle port (oracle/vdamp_oracle.py) on a bounded
+             sample of the same slices, all host cores and one core.
+--impl reference  times that oracle port alone on the same slices (rank 0;
+             other ranks exit 0).
 """
 
 from __future__ import annotations
