@@ -120,6 +120,7 @@ struct Plan {
     // their own streams, so one lane's latency-bound SURE tail overlaps the FFT
     // kernels of the others; diagnostics ride on the lanes when interleaved
     int lanes = 1;
+    int Ball = 0;                    // images of the whole plan (a lane view's B is its own range)
     struct Lane { cudaStream_t st = nullptr, side = nullptr; cudaEvent_t fork = nullptr, join = nullptr, done = nullptr; };
     std::vector<Lane> lane;
     cudaEvent_t lane_start = nullptr;
@@ -466,6 +467,7 @@ struct Seq {
         // the small-subband kernel runs on a side stream, concurrently with the
         // big one (its CTAs fill the SMs the big kernel's tail leaves idle)
         bool forked = false;
+        std::vector<int> win_items;     // subbands taken by sure_win32 (fp32)
         if constexpr (std::is_same<R, float>::value) {
             if (p->bigpath) {
                 // subbands > SCAP: keys + histogram, then value ranges over several CTAs
@@ -524,61 +526,98 @@ struct Seq {
             const int cap = Scap<R>::v;
             const size_t slot16 = ((size_t)cap + cap / 32 + 2 + 3) & ~(size_t)3;   // kernel's SLOT
             int pm = p->prune;
-            // fp32 subbands of 4,096..SCAP keys (multiples of 2,048): the two-CTA-per-SM pruned
-            // kernel, then the full sort for the subbands it flagged
+            auto launch_big = [&](const std::vector<int>& items) {
+                set_items(items);
+                Launch L(p, 3, ls);
+                const size_t slots = (size_t)(cap + cap / 32 + 1) + 1;
+                size_t sm = sizeof(R) == 4 ? 2 * slot16 * sizeof(R) + CS_WORDS * sizeof(unsigned) : slots * sizeof(R);
+                // large subbands: global counting sort counters + ranking tile
+                const size_t gcs = sizeof(R) == 4 ? 32768 * 4 + 16384 * sizeof(R) : 8192 * 4 + 8192 * sizeof(R);
+                if (sm < gcs) sm = gcs;
+                // fp64 pruned path: keys | counters | bucket ids | reduction scratch + list (vdamp_prune.cuh)
+                const size_t smp = slot16 * sizeof(R) + (PR_NC + PR_NF + 32) * 4 + (size_t)PR_BIDN * 2 +
+                                   (5 * 32 + 8) * 8 + ((size_t)pr_lmax<R>() + pr_lmax<R>() / 32 + 8) * sizeof(R);
+                if (sizeof(R) == 8 && pm && sm < smp) sm = smp;
+                constexpr int BNT = sizeof(R) == 4 ? BNT32 : BNT64;
+                auto k = pm == 0 ? sure_select<R, BNT, 0>
+                       : pm == 1 ? sure_select<R, BNT, 1>
+                       : pm == 2 ? sure_select<R, BNT, 2> : sure_select<R, BNT, 3>;
+                set_smem(k, sm);
+                launch(k, dim3(p->B, (unsigned)items.size()), BNT, sm, ls, p->geo, a);
+            };
+            // fp32 subbands of 4,096 / 8,192 / 16,384 keys: sure_win32 (vdamp_win.cuh), one subband
+            // per CTA of 32 keys per thread (16 / 8 for the CTA shapes of small batches)
             if constexpr (std::is_same<R, float>::value) {
-                if ((pm & 1) && p->ntiles <= PR_MAXT) {
+                if ((pm & 1) && p->ntiles <= WN_MAXT) {
                     std::vector<int> lp, lr;
                     for (int j : li) {
                         const int n = p->geo.len[j];
-                        (n >= 4096 && n <= cap && n % 2048 == 0 ? lp : lr).push_back(j);
+                        (n == 16384 || n == 8192 || n == 4096 ? lp : lr).push_back(j);
                     }
-                    if (!lp.empty()) {
-                        set_items(lp);
-                        {
-                            Launch L(p, 3, ls);
-                            const size_t sm = slot16 * 4 + (PR_NC + PR_NF + 32) * 4 + (5 * 16 + 8) * 8 +
-                                              ((size_t)PR_LMAX / 2 + PR_LMAX / 64 + 8) * 4;
-                            auto k = sure_prune32<PR_NT32>;
-                            set_smem(k, sm);
-                            launch(k, dim3(p->B, (unsigned)lp.size()), PR_NT32, sm, ls, p->geo, a);
+                    static const int nt4 = [] { const char* e = getenv("VDAMP_WIN4"); return e ? atoi(e) : 256; }();
+                    static const int wside = [] { const char* e = getenv("VDAMP_WINSIDE"); return e ? atoi(e) : 1; }();
+                    const bool can_fork = wside && p->side && !p->timing && !lp.empty();
+                    auto fork = [&] {
+                        if (!forked) {
+                            CK(cudaEventRecord(p->ev_fork, st_));
+                            CK(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+                            forked = true;
                         }
-                        a.only = p->pflag;
-                        {
-                            Launch L(p, 3, ls);
-                            const size_t sm = 2 * slot16 * sizeof(R) + CS_WORDS * sizeof(unsigned);
-                            auto k = sure_select<R, BNT32, 0>;
-                            set_smem(k, sm);
-                            launch(k, dim3(p->B, (unsigned)lp.size()), BNT32, sm, ls, p->geo, a);
-                        }
-                        a.only = nullptr;
+                    };
+                    // larger subbands first (one long-running 1024-thread CTA each): the sure_win32
+                    // launches then run beside them on the side stream
+                    if (!lr.empty()) {
+                        if (can_fork) fork();
+                        pm &= 2;
+                        launch_big(lr);
                     }
-                    li = lr;
-                    pm &= 2;
-                    if (li.empty()) continue;
+                    // few CTAs (small batches): wider CTAs, half the keys per thread
+                    const bool few = (long long)p->Ball * 3 < (long long)p->nsm;
+                    for (int n : {16384, 8192, 4096}) {
+                        std::vector<int> ln;
+                        for (int j : lp) if (p->geo.len[j] == n) ln.push_back(j);
+                        if (ln.empty()) continue;
+                        set_items(ln);
+                        // the smaller subbands run beside the 16,384-key launch on the side stream
+                        cudaStream_t lw = ls;
+                        if (can_fork && (n != 16384 || !lr.empty())) { fork(); lw = p->side; }
+                        Launch L(p, 3, lw);
+                        const dim3 grid(p->B, (unsigned)ln.size());
+#define WN_LAUNCH(NT_, EF_) { auto k = sure_win32<NT_, EF_>; set_smem(k, wn_smem_bytes<NT_, EF_>()); \
+                              launch(k, grid, NT_, wn_smem_bytes<NT_, EF_>(), lw, p->geo, a); }
+                        if (n == 16384) { if (few) WN_LAUNCH(1024, 16) else WN_LAUNCH(512, 32) }
+                        else if (n == 8192) { if (few) WN_LAUNCH(512, 16) else WN_LAUNCH(256, 32) }
+                        else if (few || nt4 == 512) WN_LAUNCH(512, 8)
+                        else if (nt4 == 128) WN_LAUNCH(128, 32)
+                        else WN_LAUNCH(256, 16)
+#undef WN_LAUNCH
+                    }
+                    win_items = lp;
+                    continue;
                 }
             }
-            set_items(li);
-            Launch L(p, 3, ls);
-            const size_t slots = (size_t)(cap + cap / 32 + 1) + 1;
-            size_t sm = sizeof(R) == 4 ? 2 * slot16 * sizeof(R) + CS_WORDS * sizeof(unsigned) : slots * sizeof(R);
-            // large subbands: global counting sort counters + ranking tile
-            const size_t gcs = sizeof(R) == 4 ? 32768 * 4 + 16384 * sizeof(R) : 8192 * 4 + 8192 * sizeof(R);
-            if (sm < gcs) sm = gcs;
-            // fp64 pruned path: keys | counters | bucket ids | reduction scratch + list (vdamp_prune.cuh)
-            const size_t smp = slot16 * sizeof(R) + (PR_NC + PR_NF + 32) * 4 + (size_t)PR_BIDN * 2 +
-                               (5 * 32 + 8) * 8 + ((size_t)pr_lmax<R>() + pr_lmax<R>() / 32 + 8) * sizeof(R);
-            if (sizeof(R) == 8 && pm && sm < smp) sm = smp;
-            constexpr int BNT = sizeof(R) == 4 ? BNT32 : BNT64;
-            auto k = pm == 0 ? sure_select<R, BNT, 0>
-                   : pm == 1 ? sure_select<R, BNT, 1>
-                   : pm == 2 ? sure_select<R, BNT, 2> : sure_select<R, BNT, 3>;
-            set_smem(k, sm);
-            launch(k, dim3(p->B, (unsigned)li.size()), BNT, sm, ls, p->geo, a);
+            launch_big(li);
         }
         if (forked) {
             CK(cudaEventRecord(p->ev_join, p->side));
             CK(cudaStreamWaitEvent(st_, p->ev_join, 0));
+        }
+        if constexpr (std::is_same<R, float>::value) {
+            static const int wfull = [] { const char* e = getenv("VDAMP_WINFULL"); return e ? atoi(e) : 1; }();   // 0: timing experiments only
+            if (!win_items.empty() && wfull) {
+                // the full sort for the subbands sure_win32 flagged (normally none): a few CTAs
+                set_items(win_items);
+                a.only = p->pflag;
+                Launch L(p, 3, st_);
+                // (sure_win32<512, 32>'s shared-memory size: no carve-out change between the two)
+                const size_t sm = wn_smem_bytes<512, 32>();
+                auto k = sure_win_full;
+                set_smem(k, sm);
+                const int pairs = p->B * (int)win_items.size();
+                launch(k, dim3((unsigned)std::max(1, std::min(16, pairs / 8))), 512, sm, st_, p->geo, a, p->B,
+                       (int)win_items.size());
+                a.only = nullptr;
+            }
         }
     }
 
@@ -850,7 +889,7 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         if (precision != VDAMP_FP32 && precision != VDAMP_FP64) throw Err{VDAMP_ERR_ARG, "precision must be 0 (fp32) or 1 (fp64)"};
         if (1 + 3 * scales > MAXS || scales > 12) throw Err{VDAMP_ERR_UNSUPPORTED, "too many scales (max 12)"};
         p = new Plan();
-        p->H = height; p->W = width; p->s = scales; p->B = batch; p->prec = precision; p->dev = device;
+        p->H = height; p->W = width; p->s = scales; p->B = batch; p->Ball = batch; p->prec = precision; p->dev = device;
         p->S = 1 + 3 * scales;
         p->N = (long long)height * width;
         CK(cudaSetDevice(device));
@@ -974,7 +1013,7 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         // GPU-bound and measured slightly faster with direct launches (round 1, cfg1)
         p->graphs = (long long)batch * p->N <= 8LL * 65536;
         if (const char* pe = getenv("VDAMP_PARSEVAL")) p->parseval = atoi(pe) != 0;
-        p->prune = precision == VDAMP_FP64 ? 3 : 2;
+        p->prune = 3;
         {
             // one CTA per large subband: with few of them (cfg3: 1 image x 6) the pruned
             // single-CTA passes measured slower than the fp64 global sort (120 vs 165

@@ -2963,6 +2963,8 @@ __device__ __noinline__ void select_band_call(const Geo& g, const SelArgs<R>& a,
     select_band<R, NT>(g, a, j, bi, keys, S_);
 }
 
+#include "vdamp_win.cuh"
+
 // Shared state of sure_prune32 (the fields prune_band / select_finish / scan_tile use)
 template <int NT>
 struct PrShared {

@@ -1,0 +1,741 @@
+// Lean bound-pruned exact SURE selection for fp32 subbands of 4,096..16,384 keys
+// (src/denoise.py:62-118): the bounds of vdamp_prune.cuh, restated for 512-thread CTAs
+// that fit two to an SM (about 90 KB of shared memory, 64 registers, no spills), so one
+// CTA's block-wide scans and barriers overlap the other's key passes.
+//
+//  - every block-wide reduction / scan costs one barrier: warp shuffle tree, one
+//    partial per warp into a double-buffered scratch, barrier, then every warp combines
+//    the 16 partials itself (same fixed tree in every warp: deterministic);
+//  - bucket membership is tested on the key bits against precomputed bit thresholds
+//    (the bucket maps are monotone in the bits), the key passes are branch-free apart
+//    from the rare list append, and the float64 reciprocals of the exact pass run as
+//    independent chains (no per-key branch);
+//  - reciprocal bounds use the hardware approximation (1 ulp) widened by 3 ulp instead
+//    of the directed-rounding software reciprocals.
+//
+// Included inside namespace vdamp by vdamp_kernels.cuh (after vdamp_prune.cuh).
+#pragma once
+#ifndef WN_CUT
+#define WN_CUT 99
+#endif
+
+// A CTA of NT threads (NT = 128 / 256 / 512) takes a subband of EF * NT keys (4,096 /
+// 8,192 / 16,384): every thread owns 32 keys, so the per-CTA block-wide work (scans over
+// 2 NT coarse and 4 NT fine buckets, reductions over NT / 32 warps) shrinks with the
+// subband, and 1024 / NT CTAs share an SM.
+constexpr int WN_MAXT = 256;           // tau column-tile partials held
+template <int NT, int EF_ = 32> struct Wn {
+    static constexpr int EF = EF_;             // keys per thread
+    static constexpr int LE = NT >= 512 ? 4 : 8;   // list keys per thread of the exact scan
+    static constexpr int NW = NT / 32;
+    static constexpr int NC = 2 * NT;          // coarse buckets (two per thread)
+    static constexpr int NF = 4 * NT;          // fine buckets over the coarse span (four per thread)
+    static constexpr int LMAX = LE * NT;       // keys evaluated exactly at most (else the full sort)
+    static constexpr int LIST = LMAX + LMAX / 32 + 8;                 // padded list slots (KI layout)
+    static constexpr int SLOT = (EF * NT + EF * NT / 32 + 2 + 3) & ~3;       // padded key slots (KI layout)
+    static constexpr int LOGNC = NT == 1024 ? 11 : NT == 512 ? 10 : NT == 256 ? 9 : 8;
+};
+
+template <int NW>
+struct WnScratch {                     // per-warp partials, double-buffered
+    float f[2][5 * NW];
+    double d[2][2 * NW];
+    unsigned u[2][2 * NW];
+    int i[2][2 * NW];
+    int amin[2], wlo[2], whi[2];       // block min (ordered-int floats) / window bounds by shared atomics
+    float scale[2];
+};
+
+template <int NT, int EF>
+__host__ __device__ constexpr size_t wn_smem_bytes() {
+    return (size_t)Wn<NT, EF>::SLOT * 4 + (size_t)(Wn<NT>::NC + Wn<NT>::NF + 32) * 4 + sizeof(WnScratch<NT / 32>) +
+           (size_t)2 * Wn<NT>::LIST * 4;
+}
+
+__device__ __forceinline__ float wn_rcp(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+constexpr float WN_UP = 1.0000004f, WN_DN = 0.9999996f;   // 3 ulp around the 1-ulp approximation
+
+// float <-> int with the same order (an involution), for shared-memory atomicMin
+__device__ __forceinline__ int wn_ord(float x) { const int i = __float_as_int(x); return i ^ ((i >> 31) & 0x7fffffff); }
+__device__ __forceinline__ float wn_unord(int i) { return __int_as_float(i ^ ((i >> 31) & 0x7fffffff)); }
+
+// pr_lbf with the stationary point from the approximate reciprocal: the quadratic is
+// evaluated at a t within 1e-6 of its minimiser, i.e. within 1e-12 (relative) of its minimum
+__device__ __forceinline__ float wn_lbf(float pl, float c, float A, float B, float cu, float iu, float tau) {
+    float q = 0.0f;
+    if (cu > 0.0f) {
+        float t = tau * iu * (0.5f * wn_rcp(cu));
+        t = fminf(fmaxf(t, A), B);
+        q = t * fmaf(cu, t, -tau * iu);
+    }
+    return pl + c * A * A + 2.0f * tau * cu + q;
+}
+
+// Bucket map as PrMap<float>: 0 = zeros, 1 = nonzero keys below `lo`, b >= 2 linear in
+// the bits from `base` with width 2^ls.
+struct WnMap {
+    unsigned mn, lo, base;
+    int ls, top;
+    __device__ __forceinline__ int bucket(unsigned k) const {
+        if (!k) return 0;
+        if (k < lo) return 1;
+        return 2 + (int)((k - base) >> ls);
+    }
+    // smallest key bits that map to bucket b (b <= one past the last bucket of the map: with the
+    // largest key <= 2^40, select_win's guard, the sum neither wraps nor reaches +inf)
+    __device__ __forceinline__ unsigned lowbits(int b) const {
+        if (b <= 0) return 0u;
+        if (b == 1) return 1u;
+        return base + ((unsigned)(b - 2) << ls);
+    }
+    // lower value edge of bucket b; edge(b + 1) is its upper edge
+    __device__ __forceinline__ float edge(int b) const {
+        if (b <= 0) return 0.0f;
+        if (b == 1) return __uint_as_float(mn);
+        return __uint_as_float(lowbits(b));
+    }
+};
+
+// exclusive scans in thread order: f0..f2 forward (sum over lower threads), r0, r1
+// reverse (sum over higher threads); one barrier
+template <int NW>
+__device__ __forceinline__ void wn_scan5(float& f0, float& f1, float& f2, float& r0, float& r1, float* sh) {
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5, q = l & (NW - 1);
+    float t0, t1, t2, t3, t4;
+    f0 = warp_excl_scanf<false>(f0, t0);
+    f1 = warp_excl_scanf<false>(f1, t1);
+    f2 = warp_excl_scanf<false>(f2, t2);
+    r0 = warp_excl_scanf<true>(r0, t3);
+    r1 = warp_excl_scanf<true>(r1, t4);
+    if (l == 0) { sh[w] = t0; sh[NW + w] = t1; sh[2 * NW + w] = t2; sh[3 * NW + w] = t3; sh[4 * NW + w] = t4; }
+    __syncthreads();
+    t0 = q < w ? sh[q] : 0.0f; t1 = q < w ? sh[NW + q] : 0.0f; t2 = q < w ? sh[2 * NW + q] : 0.0f;
+    t3 = q > w ? sh[3 * NW + q] : 0.0f; t4 = q > w ? sh[4 * NW + q] : 0.0f;
+#pragma unroll
+    for (int o = NW / 2; o > 0; o >>= 1) {
+        t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+        t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+        t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+        t3 += __shfl_xor_sync(0xffffffffu, t3, o);
+        t4 += __shfl_xor_sync(0xffffffffu, t4, o);
+    }
+    f0 += t0; f1 += t1; f2 += t2; r0 += t3; r1 += t4;
+}
+
+// block sums of a, b, c (floats); one barrier
+template <int NW>
+__device__ __forceinline__ void wn_sum3(float& a, float& b, float& c, float* sh) {
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5, q = l & (NW - 1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    if (l == 0) { sh[w] = a; sh[NW + w] = b; sh[2 * NW + w] = c; }
+    __syncthreads();
+    a = sh[q]; b = sh[NW + q]; c = sh[2 * NW + q];
+#pragma unroll
+    for (int o = NW / 2; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+}
+
+// One bounds level (pr_stage of vdamp_prune.cuh): K buckets per thread of map M with
+// counts in cnt; only buckets [flo, ftop) belong to the range.  Upper bounds of the risk
+// at every lower edge (t = 0 exact when flo == 0, beyond the largest key when `top`), U =
+// their minimum (never above Uprev), then the buckets whose lower bound is <= U + margin
+// -> [w0, w1].  pbf / iaf / cblf: squares below the range, inverses above it, keys below
+// it.  Returns the margin-widened U.  Three barriers; the block minimum and the window bounds go
+// through shared-memory integer atomics (deterministic).
+template <int NT, int K>
+__device__ __forceinline__ float wn_stage(const unsigned* cnt, const WnMap& M, int flo, int ftop, bool top, float pbf,
+                                          float iaf, float cblf, int n, float tauf, float ntauf, float Uprev,
+                                          WnScratch<NT / 32>& sc, int& ph, int& w0, int& w1) {
+    const int tid = threadIdx.x;
+    const int b0 = K * tid;
+    float cv[K], A[K + 1], ivs[K], ibs[K];
+#pragma unroll
+    for (int i = 0; i <= K; ++i) A[i] = M.edge(b0 + i);
+    float f0 = 0.0f, f1 = 0.0f, f2 = 0.0f, r0 = 0.0f, r1 = 0.0f;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        const int b = b0 + i;
+        const float c = (b >= flo && b < ftop) ? (float)cnt[b] : 0.0f;
+        cv[i] = c;
+        f0 = fmaf(c * A[i], A[i], f0);
+        f1 = fmaf(c * A[i + 1], A[i + 1], f1);
+        ivs[i] = (b >= 1 && c > 0.0f) ? c * (wn_rcp(A[i]) * WN_UP) : 0.0f;
+        ibs[i] = (b >= 1 && c > 0.0f) ? c * (wn_rcp(A[i + 1]) * WN_DN) : 0.0f;
+        r0 += ivs[i];
+        r1 += ibs[i];
+        f2 += c;
+    }
+    const float own_b2 = f1;
+    if (tid == 0) { sc.amin[ph] = 0x7fffffff; sc.wlo[ph] = 0x7fffffff; sc.whi[ph] = -1; }
+    wn_scan5<NT / 32>(f0, f1, f2, r0, r1, sc.f[ph]);
+    // upper bounds at the lower edges (forward), with the inverse suffixes rebuilt on the way
+    float ub = INFINITY;
+    {
+        float s3 = iaf + r1;
+#pragma unroll
+        for (int i = K - 1; i >= 0; --i) s3 += ibs[i];              // inverses at or above edge b0 (lower bounds)
+        float p = pbf + f1, cbelow = cblf + f2;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const int b = b0 + i;
+            if (b >= flo && b < ftop && b >= 1)
+                ub = fminf(ub, pr_ubf(p, (float)n - cbelow, A[i], s3, tauf) - ntauf);
+            s3 -= ibs[i];
+            p = fmaf(cv[i] * A[i + 1], A[i + 1], p);
+            cbelow += cv[i];
+        }
+    }
+    if (flo == 0 && tid == 0) ub = fminf(ub, 2.0f * tauf * ((float)n - cv[0]) - ntauf);   // t = 0, exact
+    if (tid == NT - 1) {
+        const float scale = pbf + f1 + own_b2;           // all squares below the range top, upper edges
+        if (top) ub = fminf(ub, scale - ntauf);          // t beyond the largest key
+        sc.scale[ph] = scale;
+    }
+    {
+        const int um = __reduce_min_sync(0xffffffffu, wn_ord(ub));      // one REDUX per warp
+        if ((tid & 31) == 0) atomicMin(&sc.amin[ph], um);
+    }
+    __syncthreads();
+    ub = wn_unord(sc.amin[ph]);
+    const float scale = sc.scale[ph];
+    const float Ulim = fminf(Uprev, ub + 1e-5f * (fabsf(ub) + 2.0f * ntauf + scale));
+    w0 = 0x7fffffff;
+    w1 = -1;
+    {
+        float s2 = iaf + r0;
+#pragma unroll
+        for (int i = K - 1; i >= 1; --i) s2 += ivs[i];              // inverses above bucket b0 (upper bounds)
+        float p = pbf + f0, cbelow = cblf + f2;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            const int b = b0 + i;
+            const float cu = (float)n - cbelow - cv[i];
+            const float lb = wn_lbf(p, cv[i], A[i], A[i + 1], cu, s2, tauf) - ntauf;
+            if (b >= flo && b < ftop && lb <= Ulim) { w0 = min(w0, b); w1 = max(w1, b); }
+            if (i + 1 < K) s2 -= ivs[i + 1];
+            p = fmaf(cv[i] * A[i], A[i], p);
+            cbelow += cv[i];
+        }
+    }
+    w0 = __reduce_min_sync(0xffffffffu, w0);
+    w1 = __reduce_max_sync(0xffffffffu, w1);
+    if ((tid & 31) == 0 && w1 >= 0) { atomicMin(&sc.wlo[ph], w0); atomicMax(&sc.whi[ph], w1); }
+    __syncthreads();
+    w0 = sc.wlo[ph];
+    w1 = sc.whi[ph];
+    ph ^= 1;
+    return Ulim;
+}
+
+// Exact scan of Lr <= LE * NT sorted keys (KI layout) that follow nb smaller keys of the
+// subband: LE consecutive keys per thread, scan_tile's arithmetic (squares summed upwards,
+// inverses downwards: no cancellation) with one-barrier block scans; the argmin (ties ->
+// smaller t) is merged into S_.run by thread 0.  pre_list: squares below the list; suf:
+// inverses above it; nxt: first key above it.  Two barriers.
+template <int NT, typename SS>
+__device__ __forceinline__ void wn_scan_list(const float* list, int Lr, int nb, int n, double tau, double pre_list,
+                                             double suf, double nxt, WnScratch<NT / 32>& sc, int& ph, SS& S_) {
+    constexpr int LE = Wn<NT>::LE, WN_NW = Wn<NT>::NW;
+    const int tid = threadIdx.x, l = tid & 31, w = tid >> 5, q16 = l & (WN_NW - 1);
+    const int b0 = LE * tid;
+    const bool act = b0 < Lr;
+    double ssq = 0.0, sinv = 0.0, sreg[LE];
+    if (act) {
+#pragma unroll
+        for (int e = LE - 1; e >= 0; --e) {
+            if (b0 + e < Lr) {
+                sreg[e] = sinv;
+                const double m = (double)list[KI(b0 + e)];
+                ssq = fma(m, m, ssq);
+                if (m > 0) sinv += rcp_posf(m);
+            }
+        }
+    }
+    const bool wact = w * 32 * LE < Lr;          // warps past the list only publish identities
+    double ta = 0.0, tb = 0.0, pe = 0.0, se = 0.0;
+    if (wact) {
+        pe = warp_excl_scan<false>(ssq, ta);
+        se = warp_excl_scan<true>(sinv, tb);
+    }
+    if (l == 0) { sc.d[ph][w] = ta; sc.d[ph][WN_NW + w] = tb; }
+    __syncthreads();
+    Best best{INFINITY, INFINITY, 0.0, 0.0};
+    if (wact) {
+        ta = q16 < w ? sc.d[ph][q16] : 0.0;
+        tb = q16 > w ? sc.d[ph][WN_NW + q16] : 0.0;
+#pragma unroll
+        for (int o = WN_NW / 2; o > 0; o >>= 1) {
+            ta += __shfl_xor_sync(0xffffffffu, ta, o);
+            tb += __shfl_xor_sync(0xffffffffu, tb, o);
+        }
+        pe += ta + pre_list;
+        se += tb + suf;
+        if (tid == 0 && nb == 0) S_.totinv = se + sinv;       // sum of all inverses
+        if (act) scan_keys<float, NT, LE, false, LE, true>(list, Lr, nb, n, tau, b0, LE, pe, se, nxt, best, sreg, nullptr, nullptr);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            Best c;
+            c.risk = __shfl_xor_sync(0xffffffffu, best.risk, o);
+            c.t = __shfl_xor_sync(0xffffffffu, best.t, o);
+            c.cnt = __shfl_xor_sync(0xffffffffu, best.cnt, o);
+            c.inv = __shfl_xor_sync(0xffffffffu, best.inv, o);
+            if (better(c, best)) best = c;
+        }
+    }
+    ph ^= 1;
+    if (l == 0) S_.best[w] = best;
+    __syncthreads();
+    if (tid < 32) {                              // warp 0: argmin over the warp winners
+        Best c = S_.best[q16];
+#pragma unroll
+        for (int o = WN_NW / 2; o > 0; o >>= 1) {
+            Best d;
+            d.risk = __shfl_xor_sync(0xffffffffu, c.risk, o);
+            d.t = __shfl_xor_sync(0xffffffffu, c.t, o);
+            d.cnt = __shfl_xor_sync(0xffffffffu, c.cnt, o);
+            d.inv = __shfl_xor_sync(0xffffffffu, c.inv, o);
+            if (better(d, c)) c = d;
+        }
+        if (tid == 0 && better(c, S_.run)) S_.run = c;
+    }
+}
+
+// keys: n = EF * NT float keys at keys[KI(tid + q * NT)].  cnt: NC + NF + 32 words.
+// grp, list: Wn<NT>::LIST keys each.  Leaves the window argmin in S_.run (and
+// S_.totinv).  Returns false (scratch clobbered, keys intact) when the caller must sort
+// all keys.
+template <int NT, int EF, typename SS>
+__device__ __forceinline__ bool select_win(int n, double tau, const float* keys, unsigned* cnt, float* grp, float* list,
+                                           WnScratch<NT / 32>& sc, unsigned kmn, unsigned kmx, SS& S_, PrOut& out,
+                                           long long* dbg = nullptr) {
+    constexpr int LE = Wn<NT>::LE, WN_NW = Wn<NT>::NW, NW = WN_NW, WN_NC = Wn<NT>::NC, WN_NF = Wn<NT>::NF, WN_LMAX = Wn<NT>::LMAX;
+    const unsigned* kb = reinterpret_cast<const unsigned*>(keys);
+#ifdef VDAMP_PHASE_TIMING
+    long long pc0_ = clock64();
+    PR_NOTE(8, -1);
+#endif
+    const int tid = threadIdx.x, l = tid & 31, w = tid >> 5, q16 = l & (WN_NW - 1);
+    const float tauf = (float)tau, ntauf = (float)((double)n * tau);
+    unsigned* cc = cnt;                    // coarse counts
+    unsigned* cf = cnt + WN_NC;            // fine counts
+    int ph = 0;
+
+    // ---- 1. key range, coarse map, coarse histogram ---------------------------
+    kmn = __reduce_min_sync(0xffffffffu, kmn);
+    kmx = __reduce_max_sync(0xffffffffu, kmx);
+    if (l == 0) { sc.u[ph][w] = kmn; sc.u[ph][WN_NW + w] = kmx; }
+    {
+        uint4* cz = reinterpret_cast<uint4*>(cnt);                 // cnt is 16-byte aligned
+        for (int i = tid; i < (WN_NC + WN_NF) / 4; i += NT) cz[i] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    __syncthreads();
+    const unsigned mn = __reduce_min_sync(0xffffffffu, sc.u[ph][q16]);
+    const unsigned mx = __reduce_max_sync(0xffffffffu, sc.u[ph][WN_NW + q16]);
+    ph ^= 1;
+    if (mn > mx) return false;                     // all keys zero: the full path handles it
+    // the float bounds need squares and reciprocal sums well inside the float range:
+    // 2^-40 <= largest key <= 2^40, smallest nonzero key >= 2^-100 (else the full path)
+    if (mn < ((127u - 100u) << 23) || mx < ((127u - 40u) << 23) || mx > ((127u + 40u) << 23)) return false;
+    WnMap C;
+    C.mn = mn;
+    {
+        const unsigned span = (unsigned)PR_OCT << 23;
+        C.lo = C.base = (mx - mn > span) ? mx - span : mn;
+        const unsigned d = mx - C.lo;              // smallest ls with (d >> ls) <= WN_NC - 3
+        int ls = 0;
+        if (d > (unsigned)(WN_NC - 3)) {
+            ls = 32 - __clz(d) - Wn<NT>::LOGNC;
+            if (ls < 0) ls = 0;
+            while ((d >> ls) > (unsigned)(WN_NC - 3)) ++ls;
+        }
+        C.ls = ls;
+        C.top = WN_NC;
+    }
+#pragma unroll 8
+    for (int q = 0; q < EF; ++q) atomicAdd(&cc[C.bucket(kb[KI(tid + q * NT)])], 1u);
+    __syncthreads();
+    PR_MARK(0);
+    if (WN_CUT == 0) return false;
+
+    // ---- 2. coarse bounds -> span [g0, g1] -------------------------------------
+    int g0, g1;
+    const float Ulim = wn_stage<NT, WN_NC / NT>(cc, C, 0, WN_NC, true, 0.0f, 0.0f, 0.0f, n, tauf, ntauf, INFINITY, sc, ph, g0, g1);
+    if (g1 < 0) return false;
+    PR_MARK(1);
+    if (WN_CUT == 1) return false;
+
+    // ---- 3. float sums outside the span, fine histogram inside ----------------
+    WnMap F;
+    F.mn = mn;
+    F.lo = C.lo;
+    F.base = C.lo + ((unsigned)(g0 >= 2 ? g0 - 2 : 0) << C.ls);
+    const unsigned fe = C.lo + ((unsigned)(g1 >= 2 ? g1 - 1 : 0) << C.ls);   // one past the span's top bit
+    {
+        int ls = 0;
+        if (fe > F.base) {
+            const unsigned x = fe - 1u - F.base;
+            ls = x ? 32 - __clz(x) - (Wn<NT>::LOGNC + 1) : 0;
+            if (ls < 0) ls = 0;
+            while ((x >> ls) > (unsigned)(WN_NF - 3)) ++ls;
+        }
+        F.ls = ls;
+        F.top = fe > F.base ? 3 + (int)((fe - 1u - F.base) >> ls) : 2;
+    }
+    const int flo = g0 >= 2 ? 2 : g0;              // first fine bucket that belongs to the span
+    const unsigned klo = C.lowbits(g0);            // key bits below klo: below the span
+    const unsigned khi = g1 >= WN_NC - 1 ? 0xffffffffu : C.lowbits(g1 + 1);   // at or above khi: above it
+    float pbf = 0.0f, iaf = 0.0f, cblf = 0.0f;
+#pragma unroll 8
+    for (int q = 0; q < EF; ++q) {
+        const unsigned k = kb[KI(tid + q * NT)];
+        const float mf = __uint_as_float(k);
+        const bool below = k < klo, above = k >= khi;
+        pbf = fmaf(below ? mf : 0.0f, mf, pbf);
+        cblf += below ? 1.0f : 0.0f;
+        iaf += above ? wn_rcp(mf) * WN_UP : 0.0f;
+        if (!below && !above) atomicAdd(&cf[F.bucket(k)], 1u);
+    }
+    wn_sum3<NW>(pbf, iaf, cblf, sc.f[ph]);
+    ph ^= 1;
+    PR_MARK(2);
+    if (WN_CUT == 2) return false;
+
+    // ---- 4. fine bounds -> window [f0, f1] ---------------------------------------
+    int f0, f1;
+    wn_stage<NT, WN_NF / NT>(cf, F, flo, F.top, false, pbf, iaf, cblf, n, tauf, ntauf, Ulim, sc, ph, f0, f1);
+    if (f1 < 0) return false;
+    PR_MARK(3);
+    if (WN_CUT == 3) return false;
+
+    // ---- 5. window offsets: fine-bucket cursors (exclusive scan of the window counts) ----
+    const unsigned wlo = F.lowbits(f0);
+    const unsigned whi = f1 + 1 >= F.top ? khi : F.lowbits(f1 + 1);
+    int Lw, nbw, base;
+    {
+        constexpr int KF = WN_NF / NT;
+        int c[KF], own = 0, bel = 0;
+#pragma unroll
+        for (int i = 0; i < KF; ++i) {
+            const int b = KF * tid + i;
+            const int v = (b >= flo && b < F.top) ? (int)cf[b] : 0;
+            c[i] = (b >= f0 && b <= f1) ? v : 0;
+            own += c[i];
+            bel += b < f0 ? v : 0;
+        }
+        int inc = own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) { const int u = __shfl_up_sync(0xffffffffu, inc, o); if (l >= o) inc += u; }
+        bel = __reduce_add_sync(0xffffffffu, bel);
+        if (l == 31) sc.i[ph][w] = inc;
+        if (l == 0) sc.i[ph][WN_NW + w] = bel;
+        __syncthreads();
+        int tw = sc.i[ph][q16], tb = sc.i[ph][WN_NW + q16];
+        ph ^= 1;
+        // every lane q16 holds warp q16's totals, 32 / NW copies of each
+        const int pw = __reduce_add_sync(0xffffffffu, q16 < w ? tw : 0) / (32 / WN_NW);
+        tw = __reduce_add_sync(0xffffffffu, tw) / (32 / WN_NW);
+        tb = __reduce_add_sync(0xffffffffu, tb) / (32 / WN_NW);
+        Lw = tw;                                   // window keys
+        nbw = (int)cblf + tb;                      // keys below the window
+        base = nbw > 0 ? 1 : 0;                    // slot 0: the largest key below the window
+        PR_NOTE(7, Lw);
+        if (Lw + base > WN_LMAX || Lw + base < 1) return false;
+        int run = base + pw + (inc - own);
+#pragma unroll
+        for (int i = 0; i < KF; ++i) {
+            const int b = KF * tid + i;
+            if (b >= f0 && b <= f1) cf[b] = (unsigned)run;
+            run += c[i];
+        }
+    }
+    __syncthreads();
+
+    // ---- 6. exact float64 offsets (all keys), window keys grouped by fine bucket ----------
+    double pre = 0.0, suf = 0.0;
+    unsigned nxb = 0xffffffffu, pvb = 0u;
+#pragma unroll 4
+    for (int q = 0; q < EF; ++q) {
+        const unsigned k = kb[KI(tid + q * NT)];
+        const bool below = k < wlo, above = k >= whi;
+        const double md = (double)__uint_as_float(k);
+        pre = fma(below ? md : 0.0, md, pre);
+        pvb = below ? max(pvb, k) : pvb;
+        const double rr = rcp_posf(above ? md : 1.0);
+        suf += above ? rr : 0.0;
+        nxb = above ? min(nxb, k) : nxb;
+        if (!below && !above) {
+            const unsigned pos = atomicAdd(&cf[F.bucket(k)], 1u);
+            grp[KI(pos)] = __uint_as_float(k);
+        }
+    }
+    {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            pre += __shfl_xor_sync(0xffffffffu, pre, o);
+            suf += __shfl_xor_sync(0xffffffffu, suf, o);
+        }
+        nxb = __reduce_min_sync(0xffffffffu, nxb);
+        pvb = __reduce_max_sync(0xffffffffu, pvb);
+        if (l == 0) { sc.d[ph][w] = pre; sc.d[ph][WN_NW + w] = suf; sc.u[ph][w] = nxb; sc.u[ph][WN_NW + w] = pvb; }
+        __syncthreads();
+        pre = sc.d[ph][q16]; suf = sc.d[ph][WN_NW + q16];
+        nxb = __reduce_min_sync(0xffffffffu, sc.u[ph][q16]);
+        pvb = __reduce_max_sync(0xffffffffu, sc.u[ph][WN_NW + q16]);
+        ph ^= 1;
+#pragma unroll
+        for (int o = WN_NW / 2; o > 0; o >>= 1) {
+            pre += __shfl_xor_sync(0xffffffffu, pre, o);
+            suf += __shfl_xor_sync(0xffffffffu, suf, o);
+        }
+    }
+    const double mprev = (double)__uint_as_float(pvb);
+    const double nxt = nxb == 0xffffffffu ? (double)INFINITY : (double)__uint_as_float(nxb);
+    PR_MARK(4);
+    if (WN_CUT == 4) return false;
+    // offsets: squares below the list (all keys below but one instance of mprev, the
+    // list's first element; its ties stay below), inverses above it
+    const double pre_list = base ? pre - mprev * mprev : 0.0;
+    const int nb = nbw - base;
+    const int Lr = Lw + base;                      // keys of the list
+
+    // ---- 7. rank every window key inside its fine bucket -> sorted list ---------------
+    // (every cursor now holds its bucket's end = the next bucket's start; ties by position)
+    if (tid == 0 && base) list[KI(0)] = __uint_as_float(pvb);
+    for (int p = base + tid; p < Lr; p += NT) {
+        const float x = grp[KI(p)];
+        const int fb = F.bucket(__float_as_uint(x));
+        const int e1 = (int)cf[fb];
+        const int s0 = fb == f0 ? base : (int)cf[fb - 1];
+        int rank = 0;
+        for (int q = s0; q < e1; ++q) {
+            const float y = grp[KI(q)];
+            rank += (y < x) || (y == x && q < p);
+        }
+        list[KI(s0 + rank)] = x;
+    }
+    __syncthreads();
+    PR_MARK(5);
+    if (WN_CUT == 5) return false;
+
+    // ---- 8. exact scan of the list ------------------------------------------------------
+    if (tid == 0) S_.run = Best{INFINITY, INFINITY, 0.0, 0.0};
+    wn_scan_list<NT>(list, Lr, nb, n, tau, pre_list, suf, nxt, sc, ph, S_);
+    PR_MARK(6);
+    PR_NOTE(8, 1);
+    out.nbelow = nb;
+    out.m0 = (double)list[KI(0)];
+    return true;
+}
+
+// Shared state of sure_win32 (the fields select_win / select_finish use)
+template <int NT>
+struct WnShared {
+    double sh[66 + NT / 32 + 2];
+    double tpart[WN_MAXT];
+    double tau, totinv;
+    Best best[NT / 32];
+    Best run;
+    double err, ref;
+};
+
+// One subband of n = EF * NT keys: load, |r| keys (+ trace error sums), tau,
+// select_win, outputs.  Returns false when the bounds leave too many keys.
+// Shared memory: keys (KI layout) | counters | scratch | grouped list | sorted list.
+template <int NT, int EF>
+__device__ __forceinline__ bool win_band(const Geo& g, const SelArgs<float>& a, int j, int bi, float* keys,
+                                         WnShared<NT>& S_) {
+    typedef float2 C;
+    const int tid = threadIdx.x;
+    const int n = g.len[j];                                    // == EF * NT
+    const long long base = (long long)bi * g.N + g.off[j];
+    if (a.tau_in) {
+        if (tid == 0) S_.tau = a.tau_in[(long long)bi * g.S + j];
+    } else {
+        for (int i = tid; i < a.ntiles; i += NT) S_.tpart[i] = a.taupart[((long long)bi * a.ntiles + i) * g.S + j];
+    }
+    const C* rs = a.r + base;
+    const C* w0 = a.w0 ? a.w0 + base : nullptr;
+    double err = 0.0, ref = 0.0;
+    unsigned kmn = 0xffffffffu, kmx = 0u;
+    unsigned* cnt = reinterpret_cast<unsigned*>(keys + Wn<NT, EF>::SLOT);
+    WnScratch<NT / 32>& sc = *reinterpret_cast<WnScratch<NT / 32>*>(cnt + Wn<NT>::NC + Wn<NT>::NF + 32);
+    float* grp = reinterpret_cast<float*>(&sc + 1);          // window keys grouped by fine bucket
+    float* list = grp + Wn<NT>::LIST;                        // ... sorted
+    constexpr int LB = 8;                                      // loads in flight per thread
+#pragma unroll 1
+    for (int e0 = tid; e0 < EF * NT; e0 += LB * NT) {
+        C v[LB];
+#pragma unroll
+        for (int u = 0; u < LB; ++u) v[u] = rs[e0 + u * NT];
+#pragma unroll
+        for (int u = 0; u < LB; ++u) {
+            const int e = e0 + u * NT;
+            const float m = cmag(v[u]);
+            keys[KI(e)] = m;
+            const unsigned k = __float_as_uint(m);
+            if (k) kmn = min(kmn, k);
+            kmx = max(kmx, k);
+        }
+        if (w0) {
+#pragma unroll
+            for (int u = 0; u < LB; ++u) {
+                const C wv = w0[e0 + u * NT];
+                const double dx = (double)v[u].x - (double)wv.x, dy = (double)v[u].y - (double)wv.y;
+                err += dx * dx + dy * dy;
+                ref += (double)wv.x * (double)wv.x + (double)wv.y * (double)wv.y;
+            }
+        }
+    }
+    __syncthreads();
+    if (!a.tau_in && tid == 0) {
+        double t = 0.0;
+        for (int i = 0; i < a.ntiles; ++i) t += S_.tpart[i];
+        S_.tau = t;
+    }
+    if (w0) {
+        const double e2 = block_sum<NT>(err, S_.sh), r2 = block_sum<NT>(ref, S_.sh);
+        if (tid == 0) { S_.err = e2; S_.ref = r2; }
+    }
+    __syncthreads();
+    const double tau = fmax(S_.tau, TAU_FLOOR);
+#ifdef VDAMP_PHASE_TIMING
+    long long* pdbg = bi < 4096 ? &g_prune[bi][j][0] : nullptr;
+#else
+    long long* pdbg = nullptr;
+#endif
+    PrOut po{0, 0.0};
+    if (!select_win<NT, EF>(n, tau, keys, cnt, grp, list, sc, kmn, kmx, S_, po, pdbg)) return false;
+    select_finish<float, NT, WnShared<NT>>(g, a, j, bi, n, tau, po.nbelow == 0 ? po.m0 : 0.0, w0 != nullptr, S_);
+    return true;
+}
+
+// fp32 subbands of EF * NT keys (NT = 128 / 256 / 512: 4,096 / 8,192 / 16,384 keys), one
+// per CTA, 1024 / NT CTAs per SM.  A subband the bounds cannot settle (heavy ties, diverged or
+// degenerate magnitudes) is flagged in a.pflag and sorted fully by the sure_select_flagged
+// launch that follows.
+template <int NT, int EF>
+__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 1024 / NT) sure_win32(const __grid_constant__ Geo g,
+                                                            const __grid_constant__ SelArgs<float> a) {
+    pdl_enter();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* keys = reinterpret_cast<float*>(smem_raw);
+    __shared__ WnShared<NT> S_;
+    const int bi = blockIdx.x, it = blockIdx.y;
+    for (int q = a.item_start[it]; q < a.item_start[it + 1]; ++q) {
+        const int j = a.item_list[q];
+        const bool ok = win_band<NT, EF>(g, a, j, bi, keys, S_);
+        if (threadIdx.x == 0) a.pflag[(long long)bi * g.S + j] = ok ? 0u : 1u;
+        __syncthreads();
+    }
+}
+
+// The full sort for the (rare) subbands sure_win32 flagged in a.only (heavy ties, diverged
+// or degenerate magnitudes): a few 512-thread CTAs with sure_win32's shared-memory shape
+// scan the flags of all B x nitems (image, single-subband item) pairs; a flagged subband of
+// n = 4,096 / 8,192 / 16,384 keys is loaded, bitonic-sorted in place and scanned exactly in
+// tiles of 2,048 keys (wn_scan_list).  With nothing flagged the launch costs one pass over
+// the flags.
+__global__ void __launch_bounds__(512, 1) sure_win_full(const __grid_constant__ Geo g,
+                                                        const __grid_constant__ SelArgs<float> a, int B, int nitems) {
+    constexpr int NT = 512, LE = Wn<NT>::LE, T = LE * NT;
+    typedef float2 C;
+    pdl_enter();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* keys = reinterpret_cast<float*>(smem_raw);
+    WnScratch<NT / 32>& sc = *reinterpret_cast<WnScratch<NT / 32>*>(keys + Wn<NT, 32>::SLOT);
+    __shared__ WnShared<NT> S_;
+    __shared__ unsigned wmask[NT / 32];
+    const int tid = threadIdx.x;
+    const int pairs = B * nitems;
+    for (int r0 = 0; blockIdx.x + (long long)r0 * gridDim.x < pairs; r0 += NT) {
+        const long long p = blockIdx.x + (long long)(r0 + tid) * gridDim.x;
+        bool f = false;
+        if (p < pairs) {
+            const int bi = (int)(p % B), it = (int)(p / B);
+            f = a.only[(long long)bi * g.S + a.item_list[a.item_start[it]]] != 0u;
+        }
+        const unsigned bm = __ballot_sync(0xffffffffu, f);
+        if ((tid & 31) == 0) wmask[tid >> 5] = bm;
+        __syncthreads();
+        for (int ww = 0; ww < NT / 32; ++ww) {
+            unsigned m = wmask[ww];
+            while (m) {
+                const int ln = __ffs(m) - 1;
+                m &= m - 1u;
+                const long long pp = blockIdx.x + (long long)(r0 + ww * 32 + ln) * gridDim.x;
+                const int bi = (int)(pp % B), j = a.item_list[a.item_start[(int)(pp / B)]];
+                const int n = g.len[j];
+                const long long base = (long long)bi * g.N + g.off[j];
+                const C* rs = a.r + base;
+                const C* w0 = a.w0 ? a.w0 + base : nullptr;
+                double err = 0.0, ref = 0.0;
+                if (a.tau_in) {
+                    if (tid == 0) S_.tau = a.tau_in[(long long)bi * g.S + j];
+                } else if (tid == 0) {
+                    double t = 0.0;
+                    for (int i = 0; i < a.ntiles; ++i) t += a.taupart[((long long)bi * a.ntiles + i) * g.S + j];
+                    S_.tau = t;
+                }
+                for (int e = tid; e < n; e += NT) {
+                    const C v = rs[e];
+                    keys[KI(e)] = cmag(v);
+                    if (w0) {
+                        const C wv = w0[e];
+                        const double dx = (double)v.x - (double)wv.x, dy = (double)v.y - (double)wv.y;
+                        err += dx * dx + dy * dy;
+                        ref += (double)wv.x * (double)wv.x + (double)wv.y * (double)wv.y;
+                    }
+                }
+                __syncthreads();
+                if (w0) {
+                    const double e2 = block_sum<NT>(err, S_.sh), r2 = block_sum<NT>(ref, S_.sh);
+                    if (tid == 0) { S_.err = e2; S_.ref = r2; }
+                }
+                const double tau = fmax(S_.tau, TAU_FLOOR);
+                block_sort<float, NT>(keys, n);
+                const int ntl = n / T;                         // 2, 4 or 8 tiles
+                double* tot = S_.sh;                           // [2][8] tile totals -> offsets
+                for (int t = 0; t < ntl; ++t) {
+                    double q = 0.0, v = 0.0;
+#pragma unroll
+                    for (int e = 0; e < LE; ++e) {
+                        const double mm = (double)keys[KI(t * T + LE * tid + e)];
+                        q = fma(mm, mm, q);
+                        if (mm > 0) v += rcp_posf(mm);
+                    }
+                    q = block_sum<NT>(q, S_.sh + 16);
+                    v = block_sum<NT>(v, S_.sh + 16);
+                    if (tid == 0) { tot[t] = q; tot[8 + t] = v; }
+                }
+                if (tid == 0) {
+                    double acc = 0.0;
+                    for (int t = 0; t < ntl; ++t) { const double q = tot[t]; tot[t] = acc; acc += q; }
+                    acc = 0.0;
+                    for (int t = ntl - 1; t >= 0; --t) { const double v = tot[8 + t]; tot[8 + t] = acc; acc += v; }
+                    S_.run = Best{INFINITY, INFINITY, 0.0, 0.0};
+                }
+                __syncthreads();
+                int ph = 0;
+                for (int t = 0; t < ntl; ++t) {
+                    const double nf = t + 1 < ntl ? (double)keys[KI((t + 1) * T)] : (double)INFINITY;
+                    wn_scan_list<NT>(keys + KI(t * T), T, t * T, n, tau, tot[t], tot[8 + t], nf, sc, ph, S_);
+                }
+                select_finish<float, NT, WnShared<NT>>(g, a, j, bi, n, tau, (double)keys[0], w0 != nullptr, S_);
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+    }
+}
