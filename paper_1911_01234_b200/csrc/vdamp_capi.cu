@@ -467,7 +467,7 @@ struct Seq {
         // the small-subband kernel runs on a side stream, concurrently with the
         // big one (its CTAs fill the SMs the big kernel's tail leaves idle)
         bool forked = false;
-        std::vector<int> win_items;     // subbands taken by sure_win32 (fp32)
+        std::vector<int> win_items, win_large;     // subbands taken by sure_win32 (fp32): shared / global keys
         if constexpr (std::is_same<R, float>::value) {
             if (p->bigpath) {
                 // subbands > SCAP: keys + histogram, then value ranges over several CTAs
@@ -549,10 +549,14 @@ struct Seq {
             // per CTA of 32 keys per thread (16 / 8 for the CTA shapes of small batches)
             if constexpr (std::is_same<R, float>::value) {
                 if ((pm & 1) && p->ntiles <= WN_MAXT) {
-                    std::vector<int> lp, lr;
+                    // lp: keys in shared memory; lg: 32,768 .. 131,072 keys in L2-resident global
+                    // scratch (1024-thread CTAs); lr: the rest (sure_select)
+                    std::vector<int> lp, lg, lr;
                     for (int j : li) {
                         const int n = p->geo.len[j];
-                        (n == 16384 || n == 8192 || n == 4096 ? lp : lr).push_back(j);
+                        if (n == 16384 || n == 8192 || n == 4096) lp.push_back(j);
+                        else if ((pm & 2) && p->kA && (n == 32768 || n == 65536 || n == 131072)) lg.push_back(j);
+                        else lr.push_back(j);
                     }
                     static const int nt4 = [] { const char* e = getenv("VDAMP_WIN4"); return e ? atoi(e) : 256; }();
                     static const int wside = [] { const char* e = getenv("VDAMP_WINSIDE"); return e ? atoi(e) : 1; }();
@@ -564,13 +568,27 @@ struct Seq {
                             forked = true;
                         }
                     };
-                    // larger subbands first (one long-running 1024-thread CTA each): the sure_win32
-                    // launches then run beside them on the side stream
+                    // larger subbands first (one long-running 1024-thread CTA each): the other
+                    // sure_win32 launches then run beside them on the side stream
+                    const bool has_large = !lr.empty() || !lg.empty();
+                    if (has_large && can_fork) fork();
                     if (!lr.empty()) {
-                        if (can_fork) fork();
                         pm &= 2;
                         launch_big(lr);
                     }
+                    for (int n : {131072, 65536, 32768}) {
+                        std::vector<int> ln;
+                        for (int j : lg) if (p->geo.len[j] == n) ln.push_back(j);
+                        if (ln.empty()) continue;
+                        set_items(ln);
+                        Launch L(p, 3, ls);
+                        const dim3 grid(p->B, (unsigned)ln.size());
+#define WN_LAUNCH_G(EF_) { auto k = sure_win32<1024, EF_, true>; set_smem(k, wn_smem_bytes<1024, EF_, true>()); \
+                           launch(k, grid, 1024, wn_smem_bytes<1024, EF_, true>(), ls, p->geo, a); }
+                        if (n == 131072) WN_LAUNCH_G(128) else if (n == 65536) WN_LAUNCH_G(64) else WN_LAUNCH_G(32)
+#undef WN_LAUNCH_G
+                    }
+                    win_large = lg;
                     // few CTAs (small batches): wider CTAs, half the keys per thread
                     const bool few = (long long)p->Ball * 3 < (long long)p->nsm;
                     for (int n : {16384, 8192, 4096}) {
@@ -580,7 +598,7 @@ struct Seq {
                         set_items(ln);
                         // the smaller subbands run beside the 16,384-key launch on the side stream
                         cudaStream_t lw = ls;
-                        if (can_fork && (n != 16384 || !lr.empty())) { fork(); lw = p->side; }
+                        if (can_fork && (n != 16384 || has_large)) { fork(); lw = p->side; }
                         Launch L(p, 3, lw);
                         const dim3 grid(p->B, (unsigned)ln.size());
 #define WN_LAUNCH(NT_, EF_) { auto k = sure_win32<NT_, EF_>; set_smem(k, wn_smem_bytes<NT_, EF_>()); \
@@ -614,8 +632,22 @@ struct Seq {
                 auto k = sure_win_full;
                 set_smem(k, sm);
                 const int pairs = p->B * (int)win_items.size();
-                launch(k, dim3((unsigned)std::max(1, std::min(16, pairs / 8))), 512, sm, st_, p->geo, a, p->B,
+                launch(k, dim3((unsigned)std::max(1, std::min(p->nsm, pairs))), 512, sm, st_, p->geo, a, p->B,
                        (int)win_items.size());
+                a.only = nullptr;
+            }
+            if (!win_large.empty() && wfull) {
+                set_items(win_large);
+                a.only = p->pflag;
+                Launch L(p, 3, st_);
+                const size_t slot16 = ((size_t)SCAP + SCAP / 32 + 2 + 3) & ~(size_t)3;
+                size_t sm = 2 * slot16 * sizeof(R) + CS_WORDS * sizeof(unsigned);
+                if (sm < 32768 * 4 + 16384 * sizeof(R)) sm = 32768 * 4 + 16384 * sizeof(R);
+                auto k = sure_select_flagged<R, BNT32>;
+                set_smem(k, sm);
+                const int pairs = p->B * (int)win_large.size();
+                launch(k, dim3((unsigned)std::max(1, std::min(p->nsm, pairs))), BNT32, sm, st_, p->geo, a, p->B,
+                       (int)win_large.size());
                 a.only = nullptr;
             }
         }

@@ -3034,6 +3034,47 @@ __global__ void __launch_bounds__(NT, NT >= BNT32 ? 1 : 4) sure_select(const __g
     }
 }
 
+// The full path for the (rare) large subbands sure_win32<.., GLOBAL> flagged in a.only: a
+// few CTAs scan the flags of all B x nitems (image, single-subband item) pairs and run
+// select_band on the flagged ones.  With nothing flagged the launch costs one pass over
+// the flags.
+template <typename R, int NT>
+__global__ void __launch_bounds__(NT, 1) sure_select_flagged(const __grid_constant__ Geo g,
+                                                             const __grid_constant__ SelArgs<R> a, int B, int nitems) {
+    pdl_enter();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    R* keys = reinterpret_cast<R*>(smem_raw);
+    __shared__ SelShared<NT> S_;
+    __shared__ unsigned wmask[NT / 32];
+    const int tid = threadIdx.x;
+    if (tid == 0) { mbar_init(&S_.mbar, 1); S_.mphase = 0; }
+    __syncthreads();
+    const int pairs = B * nitems;
+    for (int r0 = 0; blockIdx.x + (long long)r0 * gridDim.x < pairs; r0 += NT) {
+        const long long p = blockIdx.x + (long long)(r0 + tid) * gridDim.x;
+        bool f = false;
+        if (p < pairs) {
+            const int bi = (int)(p % B), it = (int)(p / B);
+            f = a.only[(long long)bi * g.S + a.item_list[a.item_start[it]]] != 0u;
+        }
+        const unsigned bm = __ballot_sync(0xffffffffu, f);
+        if ((tid & 31) == 0) wmask[tid >> 5] = bm;
+        __syncthreads();
+        for (int ww = 0; ww < NT / 32; ++ww) {
+            unsigned m = wmask[ww];
+            while (m) {
+                const int ln = __ffs(m) - 1;
+                m &= m - 1u;
+                const long long pp = blockIdx.x + (long long)(r0 + ww * 32 + ln) * gridDim.x;
+                const int bi = (int)(pp % B), it = (int)(pp / B);
+                select_band<R, NT>(g, a, a.item_list[a.item_start[it]], bi, keys, S_);
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // -------------------------------------------- K4, subbands > SCAP (fp32) ----
 // A subband of n > SCAP keys is split by value over several CTAs:
 //  big_keys:  |r| -> kA and a histogram of the float bits >> 17 (1/64 octave,

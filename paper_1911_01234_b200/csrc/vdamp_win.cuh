@@ -24,12 +24,14 @@
 // 2 NT coarse and 4 NT fine buckets, reductions over NT / 32 warps) shrinks with the
 // subband, and 1024 / NT CTAs share an SM.
 constexpr int WN_MAXT = 256;           // tau column-tile partials held
-template <int NT, int EF_ = 32> struct Wn {
+template <int NT, int EF_ = 32, bool GL = false> struct Wn {
     static constexpr int EF = EF_;             // keys per thread
-    static constexpr int LE = NT >= 512 ? 4 : 8;   // list keys per thread of the exact scan
+    static constexpr int LE = (NT >= 512 && !GL) ? 4 : 8;   // list keys per thread of the exact scan
     static constexpr int NW = NT / 32;
     static constexpr int NC = 2 * NT;          // coarse buckets (two per thread)
-    static constexpr int NF = 4 * NT;          // fine buckets over the coarse span (four per thread)
+    static constexpr int KF = GL ? 8 : 4;      // fine buckets per thread (large subbands: as many keys per bucket)
+    static constexpr int NF = KF * NT;         // fine buckets over the coarse span
+    static constexpr int LOGNF = (NT == 1024 ? 10 : NT == 512 ? 9 : NT == 256 ? 8 : 7) + (GL ? 3 : 2);
     static constexpr int LMAX = LE * NT;       // keys evaluated exactly at most (else the full sort)
     static constexpr int LIST = LMAX + LMAX / 32 + 8;                 // padded list slots (KI layout)
     static constexpr int SLOT = (EF * NT + EF * NT / 32 + 2 + 3) & ~3;       // padded key slots (KI layout)
@@ -46,10 +48,12 @@ struct WnScratch {                     // per-warp partials, double-buffered
     float scale[2];
 };
 
-template <int NT, int EF>
+// GLOBAL: the keys stay in L2-resident global scratch (subbands beyond the shared capacity)
+template <int NT, int EF, bool GLOBAL = false>
 __host__ __device__ constexpr size_t wn_smem_bytes() {
-    return (size_t)Wn<NT, EF>::SLOT * 4 + (size_t)(Wn<NT>::NC + Wn<NT>::NF + 32) * 4 + sizeof(WnScratch<NT / 32>) +
-           (size_t)2 * Wn<NT>::LIST * 4;
+    typedef Wn<NT, EF, GLOBAL> W;
+    return (GLOBAL ? 0 : (size_t)W::SLOT * 4) + (size_t)(W::NC + W::NF + 32) * 4 + sizeof(WnScratch<NT / 32>) +
+           (size_t)2 * W::LIST * 4;
 }
 
 __device__ __forceinline__ float wn_rcp(float x) {
@@ -86,7 +90,7 @@ struct WnMap {
         return 2 + (int)((k - base) >> ls);
     }
     // smallest key bits that map to bucket b (b <= one past the last bucket of the map: with the
-    // largest key <= 2^40, select_win's guard, the sum neither wraps nor reaches +inf)
+    // largest key < 2^100, select_win's guard, the sum neither wraps nor reaches +inf)
     __device__ __forceinline__ unsigned lowbits(int b) const {
         if (b <= 0) return 0u;
         if (b == 1) return 1u;
@@ -152,17 +156,22 @@ __device__ __forceinline__ void wn_sum3(float& a, float& b, float& c, float* sh)
 // at every lower edge (t = 0 exact when flo == 0, beyond the largest key when `top`), U =
 // their minimum (never above Uprev), then the buckets whose lower bound is <= U + margin
 // -> [w0, w1].  pbf / iaf / cblf: squares below the range, inverses above it, keys below
-// it.  Returns the margin-widened U.  Three barriers; the block minimum and the window bounds go
+// it (all in the scaled units: edges times ksc, tau times ksc^2).  Returns the margin-widened U.
+// Three barriers; the block minimum and the window bounds go
 // through shared-memory integer atomics (deterministic).
 template <int NT, int K>
-__device__ __forceinline__ float wn_stage(const unsigned* cnt, const WnMap& M, int flo, int ftop, bool top, float pbf,
+__device__ __forceinline__ float wn_stage(const unsigned* cnt, const WnMap& M, float ksc, int flo, int ftop, bool top, float pbf,
                                           float iaf, float cblf, int n, float tauf, float ntauf, float Uprev,
                                           WnScratch<NT / 32>& sc, int& ph, int& w0, int& w1) {
     const int tid = threadIdx.x;
     const int b0 = K * tid;
-    float cv[K], A[K + 1], ivs[K], ibs[K];
+    float cv[K], A[K + 1];
 #pragma unroll
-    for (int i = 0; i <= K; ++i) A[i] = M.edge(b0 + i);
+    for (int i = 0; i <= K; ++i) A[i] = M.edge(b0 + i) * ksc;     // edges in units of 2^e(largest key)
+    // inverse-sum terms of bucket i: c / A_i rounded up (ivs), c / A_{i+1} rounded down (ibs);
+    // recomputed where needed rather than held (registers)
+    auto ivs = [&](int i) { return (b0 + i >= 1 && cv[i] > 0.0f) ? cv[i] * (wn_rcp(A[i]) * WN_UP) : 0.0f; };
+    auto ibs = [&](int i) { return (b0 + i >= 1 && cv[i] > 0.0f) ? cv[i] * (wn_rcp(A[i + 1]) * WN_DN) : 0.0f; };
     float f0 = 0.0f, f1 = 0.0f, f2 = 0.0f, r0 = 0.0f, r1 = 0.0f;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
@@ -171,10 +180,8 @@ __device__ __forceinline__ float wn_stage(const unsigned* cnt, const WnMap& M, i
         cv[i] = c;
         f0 = fmaf(c * A[i], A[i], f0);
         f1 = fmaf(c * A[i + 1], A[i + 1], f1);
-        ivs[i] = (b >= 1 && c > 0.0f) ? c * (wn_rcp(A[i]) * WN_UP) : 0.0f;
-        ibs[i] = (b >= 1 && c > 0.0f) ? c * (wn_rcp(A[i + 1]) * WN_DN) : 0.0f;
-        r0 += ivs[i];
-        r1 += ibs[i];
+        r0 += ivs(i);
+        r1 += ibs(i);
         f2 += c;
     }
     const float own_b2 = f1;
@@ -185,14 +192,14 @@ __device__ __forceinline__ float wn_stage(const unsigned* cnt, const WnMap& M, i
     {
         float s3 = iaf + r1;
 #pragma unroll
-        for (int i = K - 1; i >= 0; --i) s3 += ibs[i];              // inverses at or above edge b0 (lower bounds)
+        for (int i = K - 1; i >= 0; --i) s3 += ibs(i);              // inverses at or above edge b0 (lower bounds)
         float p = pbf + f1, cbelow = cblf + f2;
 #pragma unroll
         for (int i = 0; i < K; ++i) {
             const int b = b0 + i;
             if (b >= flo && b < ftop && b >= 1)
                 ub = fminf(ub, pr_ubf(p, (float)n - cbelow, A[i], s3, tauf) - ntauf);
-            s3 -= ibs[i];
+            s3 -= ibs(i);
             p = fmaf(cv[i] * A[i + 1], A[i + 1], p);
             cbelow += cv[i];
         }
@@ -216,7 +223,7 @@ __device__ __forceinline__ float wn_stage(const unsigned* cnt, const WnMap& M, i
     {
         float s2 = iaf + r0;
 #pragma unroll
-        for (int i = K - 1; i >= 1; --i) s2 += ivs[i];              // inverses above bucket b0 (upper bounds)
+        for (int i = K - 1; i >= 1; --i) s2 += ivs(i);              // inverses above bucket b0 (upper bounds)
         float p = pbf + f0, cbelow = cblf + f2;
 #pragma unroll
         for (int i = 0; i < K; ++i) {
@@ -224,7 +231,7 @@ __device__ __forceinline__ float wn_stage(const unsigned* cnt, const WnMap& M, i
             const float cu = (float)n - cbelow - cv[i];
             const float lb = wn_lbf(p, cv[i], A[i], A[i + 1], cu, s2, tauf) - ntauf;
             if (b >= flo && b < ftop && lb <= Ulim) { w0 = min(w0, b); w1 = max(w1, b); }
-            if (i + 1 < K) s2 -= ivs[i + 1];
+            if (i + 1 < K) s2 -= ivs(i + 1);
             p = fmaf(cv[i] * A[i], A[i], p);
             cbelow += cv[i];
         }
@@ -244,10 +251,10 @@ __device__ __forceinline__ float wn_stage(const unsigned* cnt, const WnMap& M, i
 // inverses downwards: no cancellation) with one-barrier block scans; the argmin (ties ->
 // smaller t) is merged into S_.run by thread 0.  pre_list: squares below the list; suf:
 // inverses above it; nxt: first key above it.  Two barriers.
-template <int NT, typename SS>
+template <int NT, int LE, typename SS>
 __device__ __forceinline__ void wn_scan_list(const float* list, int Lr, int nb, int n, double tau, double pre_list,
                                              double suf, double nxt, WnScratch<NT / 32>& sc, int& ph, SS& S_) {
-    constexpr int LE = Wn<NT>::LE, WN_NW = Wn<NT>::NW;
+    constexpr int WN_NW = NT / 32;
     const int tid = threadIdx.x, l = tid & 31, w = tid >> 5, q16 = l & (WN_NW - 1);
     const int b0 = LE * tid;
     const bool act = b0 < Lr;
@@ -313,21 +320,26 @@ __device__ __forceinline__ void wn_scan_list(const float* list, int Lr, int nb, 
 }
 
 // keys: n = EF * NT float keys at keys[KI(tid + q * NT)].  cnt: NC + NF + 32 words.
-// grp, list: Wn<NT>::LIST keys each.  Leaves the window argmin in S_.run (and
+// grp, list: Wn<NT, EF, GLOBAL>::LIST keys each.  Leaves the window argmin in S_.run (and
 // S_.totinv).  Returns false (scratch clobbered, keys intact) when the caller must sort
 // all keys.
-template <int NT, int EF, typename SS>
+template <int NT, int EF, bool GLOBAL, typename SS>
 __device__ __forceinline__ bool select_win(int n, double tau, const float* keys, unsigned* cnt, float* grp, float* list,
                                            WnScratch<NT / 32>& sc, unsigned kmn, unsigned kmx, SS& S_, PrOut& out,
                                            long long* dbg = nullptr) {
-    constexpr int LE = Wn<NT>::LE, WN_NW = Wn<NT>::NW, NW = WN_NW, WN_NC = Wn<NT>::NC, WN_NF = Wn<NT>::NF, WN_LMAX = Wn<NT>::LMAX;
+    typedef Wn<NT, EF, GLOBAL> W;
+    constexpr int LE = W::LE, WN_NW = W::NW, NW = WN_NW, WN_NC = W::NC, WN_NF = W::NF, WN_LMAX = W::LMAX;
     const unsigned* kb = reinterpret_cast<const unsigned*>(keys);
+    // key q of this thread: shared memory (KI layout), or global scratch through L2
+    auto key = [&](int q) -> unsigned {
+        if constexpr (GLOBAL) return __ldcg(kb + threadIdx.x + q * NT);
+        else return kb[KI((int)threadIdx.x + q * NT)];
+    };
 #ifdef VDAMP_PHASE_TIMING
     long long pc0_ = clock64();
     PR_NOTE(8, -1);
 #endif
     const int tid = threadIdx.x, l = tid & 31, w = tid >> 5, q16 = l & (WN_NW - 1);
-    const float tauf = (float)tau, ntauf = (float)((double)n * tau);
     unsigned* cc = cnt;                    // coarse counts
     unsigned* cf = cnt + WN_NC;            // fine counts
     int ph = 0;
@@ -345,9 +357,14 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
     const unsigned mx = __reduce_max_sync(0xffffffffu, sc.u[ph][WN_NW + q16]);
     ph ^= 1;
     if (mn > mx) return false;                     // all keys zero: the full path handles it
-    // the float bounds need squares and reciprocal sums well inside the float range:
-    // 2^-40 <= largest key <= 2^40, smallest nonzero key >= 2^-100 (else the full path)
-    if (mn < ((127u - 100u) << 23) || mx < ((127u - 40u) << 23) || mx > ((127u + 40u) << 23)) return false;
+    // The float bounds work on keys scaled by ksc = 2^-e (e: exponent of the largest key; exact)
+    // and tau scaled by ksc^2: comparing bounds is invariant under it, and squares and
+    // reciprocal sums stay well inside the float range for data of any magnitude (diverged
+    // runs).  Normal keys below 2^100 (bucket edges past the largest key stay finite) spanning at
+    // most 100 octaves; else the full path.
+    if (mn < 0x00800000u || mx >= ((127u + 100u) << 23) || (mx >> 23) - (mn >> 23) > 100u) return false;
+    const float ksc = __uint_as_float((254u - (mx >> 23)) << 23);
+    const float tauf = (float)(tau * (double)ksc * (double)ksc), ntauf = (float)((double)n * tau * (double)ksc * (double)ksc);
     WnMap C;
     C.mn = mn;
     {
@@ -356,7 +373,7 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
         const unsigned d = mx - C.lo;              // smallest ls with (d >> ls) <= WN_NC - 3
         int ls = 0;
         if (d > (unsigned)(WN_NC - 3)) {
-            ls = 32 - __clz(d) - Wn<NT>::LOGNC;
+            ls = 32 - __clz(d) - W::LOGNC;
             if (ls < 0) ls = 0;
             while ((d >> ls) > (unsigned)(WN_NC - 3)) ++ls;
         }
@@ -364,14 +381,14 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
         C.top = WN_NC;
     }
 #pragma unroll 8
-    for (int q = 0; q < EF; ++q) atomicAdd(&cc[C.bucket(kb[KI(tid + q * NT)])], 1u);
+    for (int q = 0; q < EF; ++q) atomicAdd(&cc[C.bucket(key(q))], 1u);
     __syncthreads();
     PR_MARK(0);
     if (WN_CUT == 0) return false;
 
     // ---- 2. coarse bounds -> span [g0, g1] -------------------------------------
     int g0, g1;
-    const float Ulim = wn_stage<NT, WN_NC / NT>(cc, C, 0, WN_NC, true, 0.0f, 0.0f, 0.0f, n, tauf, ntauf, INFINITY, sc, ph, g0, g1);
+    const float Ulim = wn_stage<NT, WN_NC / NT>(cc, C, ksc, 0, WN_NC, true, 0.0f, 0.0f, 0.0f, n, tauf, ntauf, INFINITY, sc, ph, g0, g1);
     if (g1 < 0) return false;
     PR_MARK(1);
     if (WN_CUT == 1) return false;
@@ -386,7 +403,7 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
         int ls = 0;
         if (fe > F.base) {
             const unsigned x = fe - 1u - F.base;
-            ls = x ? 32 - __clz(x) - (Wn<NT>::LOGNC + 1) : 0;
+            ls = x ? 32 - __clz(x) - W::LOGNF : 0;
             if (ls < 0) ls = 0;
             while ((x >> ls) > (unsigned)(WN_NF - 3)) ++ls;
         }
@@ -399,8 +416,8 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
     float pbf = 0.0f, iaf = 0.0f, cblf = 0.0f;
 #pragma unroll 8
     for (int q = 0; q < EF; ++q) {
-        const unsigned k = kb[KI(tid + q * NT)];
-        const float mf = __uint_as_float(k);
+        const unsigned k = key(q);
+        const float mf = __uint_as_float(k) * ksc;
         const bool below = k < klo, above = k >= khi;
         pbf = fmaf(below ? mf : 0.0f, mf, pbf);
         cblf += below ? 1.0f : 0.0f;
@@ -414,7 +431,7 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
 
     // ---- 4. fine bounds -> window [f0, f1] ---------------------------------------
     int f0, f1;
-    wn_stage<NT, WN_NF / NT>(cf, F, flo, F.top, false, pbf, iaf, cblf, n, tauf, ntauf, Ulim, sc, ph, f0, f1);
+    wn_stage<NT, WN_NF / NT>(cf, F, ksc, flo, F.top, false, pbf, iaf, cblf, n, tauf, ntauf, Ulim, sc, ph, f0, f1);
     if (f1 < 0) return false;
     PR_MARK(3);
     if (WN_CUT == 3) return false;
@@ -424,7 +441,7 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
     const unsigned whi = f1 + 1 >= F.top ? khi : F.lowbits(f1 + 1);
     int Lw, nbw, base;
     {
-        constexpr int KF = WN_NF / NT;
+        constexpr int KF = W::KF;
         int c[KF], own = 0, bel = 0;
 #pragma unroll
         for (int i = 0; i < KF; ++i) {
@@ -467,7 +484,7 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
     unsigned nxb = 0xffffffffu, pvb = 0u;
 #pragma unroll 4
     for (int q = 0; q < EF; ++q) {
-        const unsigned k = kb[KI(tid + q * NT)];
+        const unsigned k = key(q);
         const bool below = k < wlo, above = k >= whi;
         const double md = (double)__uint_as_float(k);
         pre = fma(below ? md : 0.0, md, pre);
@@ -531,7 +548,7 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
 
     // ---- 8. exact scan of the list ------------------------------------------------------
     if (tid == 0) S_.run = Best{INFINITY, INFINITY, 0.0, 0.0};
-    wn_scan_list<NT>(list, Lr, nb, n, tau, pre_list, suf, nxt, sc, ph, S_);
+    wn_scan_list<NT, LE>(list, Lr, nb, n, tau, pre_list, suf, nxt, sc, ph, S_);
     PR_MARK(6);
     PR_NOTE(8, 1);
     out.nbelow = nb;
@@ -553,7 +570,7 @@ struct WnShared {
 // One subband of n = EF * NT keys: load, |r| keys (+ trace error sums), tau,
 // select_win, outputs.  Returns false when the bounds leave too many keys.
 // Shared memory: keys (KI layout) | counters | scratch | grouped list | sorted list.
-template <int NT, int EF>
+template <int NT, int EF, bool GLOBAL>
 __device__ __forceinline__ bool win_band(const Geo& g, const SelArgs<float>& a, int j, int bi, float* keys,
                                          WnShared<NT>& S_) {
     typedef float2 C;
@@ -569,10 +586,12 @@ __device__ __forceinline__ bool win_band(const Geo& g, const SelArgs<float>& a, 
     const C* w0 = a.w0 ? a.w0 + base : nullptr;
     double err = 0.0, ref = 0.0;
     unsigned kmn = 0xffffffffu, kmx = 0u;
-    unsigned* cnt = reinterpret_cast<unsigned*>(keys + Wn<NT, EF>::SLOT);
-    WnScratch<NT / 32>& sc = *reinterpret_cast<WnScratch<NT / 32>*>(cnt + Wn<NT>::NC + Wn<NT>::NF + 32);
+    typedef Wn<NT, EF, GLOBAL> W;
+    unsigned* cnt = reinterpret_cast<unsigned*>(GLOBAL ? keys : keys + W::SLOT);
+    WnScratch<NT / 32>& sc = *reinterpret_cast<WnScratch<NT / 32>*>(cnt + W::NC + W::NF + 32);
     float* grp = reinterpret_cast<float*>(&sc + 1);          // window keys grouped by fine bucket
-    float* list = grp + Wn<NT>::LIST;                        // ... sorted
+    float* list = grp + W::LIST;                             // ... sorted
+    float* kst = GLOBAL ? a.kA + base : keys;                // where the keys go
     constexpr int LB = 8;                                      // loads in flight per thread
 #pragma unroll 1
     for (int e0 = tid; e0 < EF * NT; e0 += LB * NT) {
@@ -583,7 +602,8 @@ __device__ __forceinline__ bool win_band(const Geo& g, const SelArgs<float>& a, 
         for (int u = 0; u < LB; ++u) {
             const int e = e0 + u * NT;
             const float m = cmag(v[u]);
-            keys[KI(e)] = m;
+            if constexpr (GLOBAL) __stcg(kst + e, m);
+            else kst[KI(e)] = m;
             const unsigned k = __float_as_uint(m);
             if (k) kmn = min(kmn, k);
             kmx = max(kmx, k);
@@ -616,7 +636,7 @@ __device__ __forceinline__ bool win_band(const Geo& g, const SelArgs<float>& a, 
     long long* pdbg = nullptr;
 #endif
     PrOut po{0, 0.0};
-    if (!select_win<NT, EF>(n, tau, keys, cnt, grp, list, sc, kmn, kmx, S_, po, pdbg)) return false;
+    if (!select_win<NT, EF, GLOBAL>(n, tau, kst, cnt, grp, list, sc, kmn, kmx, S_, po, pdbg)) return false;
     select_finish<float, NT, WnShared<NT>>(g, a, j, bi, n, tau, po.nbelow == 0 ? po.m0 : 0.0, w0 != nullptr, S_);
     return true;
 }
@@ -625,7 +645,7 @@ __device__ __forceinline__ bool win_band(const Geo& g, const SelArgs<float>& a, 
 // per CTA, 1024 / NT CTAs per SM.  A subband the bounds cannot settle (heavy ties, diverged or
 // degenerate magnitudes) is flagged in a.pflag and sorted fully by the sure_select_flagged
 // launch that follows.
-template <int NT, int EF>
+template <int NT, int EF, bool GLOBAL = false>
 __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 1024 / NT) sure_win32(const __grid_constant__ Geo g,
                                                             const __grid_constant__ SelArgs<float> a) {
     pdl_enter();
@@ -635,7 +655,7 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 1024 / NT) sure_win32(con
     const int bi = blockIdx.x, it = blockIdx.y;
     for (int q = a.item_start[it]; q < a.item_start[it + 1]; ++q) {
         const int j = a.item_list[q];
-        const bool ok = win_band<NT, EF>(g, a, j, bi, keys, S_);
+        const bool ok = win_band<NT, EF, GLOBAL>(g, a, j, bi, keys, S_);
         if (threadIdx.x == 0) a.pflag[(long long)bi * g.S + j] = ok ? 0u : 1u;
         __syncthreads();
     }
@@ -730,7 +750,7 @@ __global__ void __launch_bounds__(512, 1) sure_win_full(const __grid_constant__ 
                 int ph = 0;
                 for (int t = 0; t < ntl; ++t) {
                     const double nf = t + 1 < ntl ? (double)keys[KI((t + 1) * T)] : (double)INFINITY;
-                    wn_scan_list<NT>(keys + KI(t * T), T, t * T, n, tau, tot[t], tot[8 + t], nf, sc, ph, S_);
+                    wn_scan_list<NT, LE>(keys + KI(t * T), T, t * T, n, tau, tot[t], tot[8 + t], nf, sc, ph, S_);
                 }
                 select_finish<float, NT, WnShared<NT>>(g, a, j, bi, n, tau, (double)keys[0], w0 != nullptr, S_);
                 __syncthreads();
