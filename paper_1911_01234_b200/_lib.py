@@ -11,6 +11,12 @@ from __future__ import annotations
 import ctypes
 import os
 
+# The image lanes and their side streams (up to 8 compute streams plus the copy streams of the
+# streaming API) should each get their own hardware work queue; the CUDA default of 8 lets two
+# of them share one, which serialises their kernels.  Read by the CUDA driver at context
+# creation, so it only takes effect when this package is imported before CUDA is initialised.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("VDAMP_LIB") or os.path.join(_HERE, "libvdamp_b200.so")
 

@@ -482,6 +482,7 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
     // ---- 6. exact float64 offsets (all keys), window keys grouped by fine bucket ----------
     double pre = 0.0, suf = 0.0;
     unsigned nxb = 0xffffffffu, pvb = 0u;
+    // branch-free arithmetic first (independent reciprocal chains of the unrolled keys) ...
 #pragma unroll 4
     for (int q = 0; q < EF; ++q) {
         const unsigned k = key(q);
@@ -492,7 +493,12 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
         const double rr = rcp_posf(above ? md : 1.0);
         suf += above ? rr : 0.0;
         nxb = above ? min(nxb, k) : nxb;
-        if (!below && !above) {
+    }
+    // ... then the (few) window keys into their fine buckets
+#pragma unroll 8
+    for (int q = 0; q < EF; ++q) {
+        const unsigned k = key(q);
+        if (k >= wlo && k < whi) {
             const unsigned pos = atomicAdd(&cf[F.bucket(k)], 1u);
             grp[KI(pos)] = __uint_as_float(k);
         }

@@ -10,7 +10,8 @@ import collections, csv, json, os, sys
 
 CLASS = {"synth_pass": "synth_rowfft", "synth256": "synth_rowfft", "col_pass": "col_residual",
          "col_pass256": "col_residual", "analysis_pass": "rowifft_analysis", "analysis256": "rowifft_analysis",
-         "sure_select": "sure_select", "big_keys": "sure_select", "big_range": "sure_select", "row_pass": "finalize"}
+         "sure_select": "sure_select", "sure_win32": "sure_select", "sure_win_full": "sure_select",
+         "sure_select_flagged": "sure_select", "big_keys": "sure_select", "big_range": "sure_select", "row_pass": "finalize"}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
          "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
 
