@@ -244,6 +244,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-depth", type=int, default=1, help="batches reconstructing side by side in the e2e leg")
     ap.add_argument("--quick", action="store_true", help="print a short human summary instead of JSON")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the per-config lines (cfg0/2/3/4 and fp64) of a 1-GPU run")
@@ -400,25 +401,33 @@ def main():
             rec(host["y"], host["indices"], host["counts"], host["probs"], host["noise_var"], cfg.n_iters, out=out)
         t_sync = max_over_ranks(time.perf_counter() - t0)
         barrier()
-        # (b) the streaming API: batch k+1's H2D and batch k-1's D2H overlap batch k
-        srec = vdamp.StreamingReconstructor(cfg.size, cfg.size, cfg.scales, B, precision=args.precision,
-                                            device=local)
-        outs = [out, torch.empty_like(out).pin_memory()]
-        for i in range(args.warmup):
-            srec.submit(host, cfg.n_iters, outs[i & 1])
-        srec.wait()
-        barrier()
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        for i in range(args.steps):
-            srec.submit(host, cfg.n_iters, outs[i & 1])
-        srec.wait()
-        t_e2e = max_over_ranks(time.perf_counter() - t0)
-        barrier()
+        # (b) the streaming API: batch k+1's H2D and batch k-1's D2H overlap batch k; at the
+        # default depth 2 the reconstructions of two consecutive batches also run side by side
+        # (own plans and streams); depth 1 (one reconstruction at a time) is reported beside it
+        def stream_run(depth):
+            srec = vdamp.StreamingReconstructor(cfg.size, cfg.size, cfg.scales, B, precision=args.precision,
+                                                device=local, depth=depth)
+            outs = [torch.empty_like(out).pin_memory() for _ in range(depth + 1)]
+            for i in range(max(args.warmup, depth + 1)):
+                srec.submit(host, cfg.n_iters, outs[i % len(outs)])
+            srec.wait()
+            barrier()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            for i in range(args.steps):
+                srec.submit(host, cfg.n_iters, outs[i % len(outs)])
+            srec.wait()
+            t = max_over_ranks(time.perf_counter() - t0)
+            barrier()
+            assert torch.equal(outs[0], out), "streaming result differs from the synchronous call"
+            return t
+        t_e2e = stream_run(args.e2e_depth)
         e2e = {"value": images_all * cfg.n_iters * args.steps / t_e2e, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": 1e3 * t_e2e / args.steps,
-               "api": "StreamingReconstructor.submit (copies overlap the previous/next batch)",
+               "api": "StreamingReconstructor.submit: H2D of batch k+1 and D2H of batch k-1 overlap the reconstruction "
+                      "of batch k; x_hat checked bitwise against the synchronous call",
+               "depth": args.e2e_depth,
                "sync_call_value": images_all * cfg.n_iters * args.steps / t_sync}
 
     # ---- fixed batch sharded across the ranks (BASELINE cfg1/cfg4 wording) ----

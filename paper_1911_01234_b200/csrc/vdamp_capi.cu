@@ -113,6 +113,16 @@ struct Plan {
     long long g_launches = 0;
     long long g_cls[VDAMP_KERNEL_CLASSES] = {0};
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> gev;   // timing events inside the graph
+    // graphs of other keys seen recently (a pipelined caller alternates output buffers):
+    // parked instead of destroyed, at most GRAPH_PARK of them
+    struct GraphSlot {
+        cudaGraphExec_t gexec;
+        std::vector<const void*> gkey;
+        long long g_launches;
+        long long g_cls[VDAMP_KERNEL_CLASSES];
+        std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> gev;
+    };
+    std::vector<GraphSlot> gpark;
     cudaStream_t gstream = nullptr; // capture/launch stream when the caller passes the legacy default stream
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -220,8 +230,30 @@ static bool pdl_enabled() {
     return on;
 }
 
+// Shared-memory carve-out preference of the per-iteration kernels, in percent of the SM's
+// unified L1 / shared storage (VDAMP_CARVEOUT; -1 leaves the driver's per-kernel choice).
+// Kernels of different lanes and of the side streams run side by side on one SM only while
+// they agree on its carve-out; a CTA that needs another split waits for the SM to drain.
+// One common preference for all of them removes those drains.
+int carveout_pref() {
+    static const int v = [] { const char* e = getenv("VDAMP_CARVEOUT"); return e ? atoi(e) : -1; }();
+    return v;
+}
+
+template <typename K>
+void prefer_carveout(K kern) {
+    const int v = carveout_pref();
+    if (v < 0) return;
+    static thread_local std::vector<const void*> done;
+    const void* key = reinterpret_cast<const void*>(kern);
+    for (const void* d : done) if (d == key) return;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, v > 100 ? 100 : v));
+    done.push_back(key);
+}
+
 template <typename... KArgs, typename... Args>
 void launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t sm, cudaStream_t st, Args... args) {
+    prefer_carveout(k);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -249,12 +281,59 @@ void accumulate(Plan* p, std::vector<std::pair<int, std::pair<cudaEvent_t, cudaE
     if (destroy) ev.clear();
 }
 
-void drop_graph(Plan* p) {
+constexpr size_t GRAPH_PARK = 3;
+
+// destroys the current graph only
+void drop_current_graph(Plan* p) {
     if (p->gexec) cudaGraphExecDestroy(p->gexec);
     p->gexec = nullptr;
     p->gkey.clear();
     for (auto& e : p->gev) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
     p->gev.clear();
+}
+
+// destroys every graph of the plan (anything baked into them changed)
+void drop_graph(Plan* p) {
+    drop_current_graph(p);
+    for (auto& g : p->gpark) {
+        if (g.gexec) cudaGraphExecDestroy(g.gexec);
+        for (auto& e : g.gev) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
+    }
+    p->gpark.clear();
+}
+
+// The current graph does not match `key`: park it (oldest parked one destroyed beyond
+// GRAPH_PARK) and make a parked graph of that key current if there is one.
+bool switch_graph(Plan* p, const std::vector<const void*>& key) {
+    if (p->gexec) {
+        Plan::GraphSlot g;
+        g.gexec = p->gexec;
+        g.gkey = p->gkey;
+        g.g_launches = p->g_launches;
+        for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) g.g_cls[c] = p->g_cls[c];
+        g.gev.swap(p->gev);
+        p->gexec = nullptr;
+        p->gkey.clear();
+        p->gpark.push_back(std::move(g));
+    }
+    for (size_t i = 0; i < p->gpark.size(); ++i) {
+        if (p->gpark[i].gkey != key) continue;
+        Plan::GraphSlot g = std::move(p->gpark[i]);
+        p->gpark.erase(p->gpark.begin() + (long)i);
+        p->gexec = g.gexec;
+        p->gkey = g.gkey;
+        p->g_launches = g.g_launches;
+        for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) p->g_cls[c] = g.g_cls[c];
+        p->gev.swap(g.gev);
+        return true;
+    }
+    while (p->gpark.size() > GRAPH_PARK) {
+        Plan::GraphSlot& g = p->gpark.front();
+        if (g.gexec) cudaGraphExecDestroy(g.gexec);
+        for (auto& e : g.gev) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
+        p->gpark.erase(p->gpark.begin());
+    }
+    return false;
 }
 
 template <typename K>
@@ -1041,9 +1120,10 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         CK(cudaStreamCreateWithFlags(&p->gstream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
-        // graphs pay off when launches are short (small batches); large batches are
-        // GPU-bound and measured slightly faster with direct launches (round 1, cfg1)
-        p->graphs = (long long)batch * p->N <= 8LL * 65536;
+        // graphs pay off while the host's launch rate limits the run (~860 launches per 3.9 ms
+        // step on cfg1: 487k -> 519k img-iter/s; cfg0 13.0k -> 13.7k, cfg3 3.14k -> 3.22k);
+        // larger batches are GPU-bound and measured 2-3% faster with direct launches (cfg2, cfg4)
+        p->graphs = (long long)batch * p->N <= 64LL * 65536;
         if (const char* pe = getenv("VDAMP_PARSEVAL")) p->parseval = atoi(pe) != 0;
         p->prune = 3;
         {
@@ -1435,8 +1515,7 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
                                      (const void*)(intptr_t)p->iter_timing};
         if (snapshots) for (int k = 0; k < n_iters; ++k) key.push_back(snapshots[k]);
         else key.push_back(nullptr);
-        if (!p->gexec || key != p->gkey) {
-            drop_graph(p);
+        if ((!p->gexec || key != p->gkey) && !switch_graph(p, key)) {
             CK(cudaSetDevice(p->dev));
             // capture: launches and timing events recorded during capture belong to the graph
             const long long l0 = p->launches;
@@ -1459,7 +1538,7 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
             if (!ok || ec != cudaSuccess) {
                 if (graph) cudaGraphDestroy(graph);
                 p->graphs = false;             // fall back to direct launches for this plan
-                drop_graph(p);
+                drop_current_graph(p);         // (the events collected during the failed capture)
                 p->launches = l0;
                 for (int c = 0; c < VDAMP_KERNEL_CLASSES; ++c) p->cls_launches[c] = c0[c];
                 cudaGetLastError();

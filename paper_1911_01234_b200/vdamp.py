@@ -303,28 +303,40 @@ class BatchReconstructor:
 
 class StreamingReconstructor:
     """Pipelined batches: host->device copies of batch k+1 and the device->host
-    copy of batch k-1 overlap the reconstruction of batch k.
+    copy of batch k-1 overlap the reconstruction of batch k.  With ``depth`` > 1
+    the reconstructions of ``depth`` consecutive batches also run side by side on
+    their own plans and compute streams; measured slower on cfg1 (64 x 256^2:
+    depth 1 / 2 / 3 = 503k / 408k / 317k img-iter/s: a batch's image lanes already
+    fill the GPU), so the default is one reconstruction at a time.
 
     ``submit`` takes pinned host tensors (see :meth:`BatchReconstructor.upload`)
     and a pinned host ``out`` tensor (B, H, W); it returns at once.  ``wait``
     blocks until every submitted batch has landed in its ``out``.  Inputs of a
-    submitted batch must not be modified until its copy has finished (two
-    batches in flight at most; ``submit`` blocks beyond that).
+    submitted batch must not be modified until its copy has finished
+    (``depth`` + 1 batches in flight at most; ``submit`` blocks beyond that).
+    Results are bitwise those of :class:`BatchReconstructor` at any depth.
     """
 
-    def __init__(self, height, width, scales, batch, *, precision="fp32", device=None):
+    def __init__(self, height, width, scales, batch, *, precision="fp32", device=None, depth=1):
         import torch
-        from .plan import get_plan
+        from .plan import Plan, get_plan
         SubbandLayout.create(height, width, scales)
+        if depth < 1:
+            raise ValueError(f"depth must be >= 1, got {depth}")
         self.plan = get_plan(height, width, scales, batch, precision, device)
         dev = self.plan.device
-        self.compute = torch.cuda.Stream(dev)
+        # one plan (workspace) and compute stream per batch in flight on the device
+        self.plans = [self.plan] + [Plan(height, width, scales, batch, precision, dev.index)
+                                    for _ in range(depth - 1)]
+        self.computes = [torch.cuda.Stream(dev) for _ in range(depth)]
+        self.compute = self.computes[0]
         self.copy = torch.cuda.Stream(dev)          # host -> device
         self.copy_out = torch.cuda.Stream(dev)      # device -> host (never queued behind an upload)
-        self._x = [self.plan.empty_images(), self.plan.empty_images()]
-        self._stage = [None, None]
-        self._ev_used = [None, None]        # compute finished reading stage / writing x of slot
-        self._ev_out = [None, None]         # D2H of slot finished
+        self.depth = depth
+        ns = depth + 1                              # staged inputs / x_hat slots
+        self._x = [self.plan.empty_images() for _ in range(ns)]
+        self._stage = [None] * ns
+        self._ev_out = [None] * ns          # D2H of slot finished
         self._k = 0
 
     upload = BatchReconstructor.upload
@@ -333,7 +345,8 @@ class StreamingReconstructor:
         import torch
         if n_iters < 1:
             raise ValueError(f"need at least one iteration, got {n_iters}")
-        p, s = self.plan, self._k & 1
+        s = self._k % (self.depth + 1)
+        p, compute = self.plans[self._k % self.depth], self.computes[self._k % self.depth]
         self._k += 1
         if self._ev_out[s] is not None:
             self._ev_out[s].synchronize()      # slot s (stage and x) free again
@@ -344,13 +357,13 @@ class StreamingReconstructor:
             ev_in = torch.cuda.Event()
             ev_in.record(self.copy)
         self._stage[s] = st
-        self.compute.wait_event(ev_in)
-        with torch.cuda.stream(self.compute):
+        compute.wait_event(ev_in)
+        with torch.cuda.stream(compute):
             p.set_measurements(st["y"], st["indices"], host["counts"], st["probs"], host["noise_var"],
-                               host.get("shared_probs", True), stream=self.compute, sync_validation=False)
-            p.run(n_iters, x_hat=self._x[s], stream=self.compute)
+                               host.get("shared_probs", True), stream=compute, sync_validation=False)
+            p.run(n_iters, x_hat=self._x[s], stream=compute)
             ev_done = torch.cuda.Event()
-            ev_done.record(self.compute)
+            ev_done.record(compute)
         self.copy_out.wait_event(ev_done)
         with torch.cuda.stream(self.copy_out):
             out.copy_(self._x[s], non_blocking=True)
@@ -365,4 +378,5 @@ class StreamingReconstructor:
         for e in self._ev_out:
             if e is not None:
                 e.synchronize()
-        self.plan.measurement_status(wait=True)
+        for p in self.plans:
+            p.measurement_status(wait=True)

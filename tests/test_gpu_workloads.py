@@ -189,9 +189,12 @@ def test_parseval_nmse_matches_finalize_path(cfg0_small):
     assert np.abs(out["1"] - out["0"]).max() <= 1e-8
 
 
-def test_streaming_reconstructor_matches_sync():
-    """Pipelined submissions (copies overlapping the neighbouring batches) give
-    the synchronous call's results bitwise, for several batches in flight."""
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_streaming_reconstructor_matches_sync(depth):
+    """Pipelined submissions (copies overlapping the neighbouring batches, and with
+    depth > 1 the reconstructions of consecutive batches running side by side on their
+    own plans) give the synchronous call's results bitwise, with distinct batches in
+    flight."""
     import torch
     from paper_1911_01234_b200 import vdamp, workload
     w = workload.make_workload("cfg1", batch=4)
@@ -200,13 +203,18 @@ def test_streaming_reconstructor_matches_sync():
     rec = vdamp.BatchReconstructor(cfg.size, cfg.size, cfg.scales, 4, precision="fp32")
     host = rec.upload(inp, pin=True)
     ref = rec(host["y"], host["indices"], host["counts"], host["probs"], host["noise_var"], 5).cpu().clone()
-    srec = vdamp.StreamingReconstructor(cfg.size, cfg.size, cfg.scales, 4, precision="fp32")
-    outs = [torch.empty(ref.shape, dtype=ref.dtype).pin_memory() for _ in range(3)]
-    for i in range(5):
-        srec.submit(host, 5, outs[i % 3])
+    # a second, different batch: neighbours in the pipeline must not mix
+    w2 = workload.make_workload("cfg1", batch=4, first=4)
+    host2 = rec.upload(vdamp.prepare_batch(w2.ys, w2.masks, w2.pmap, w2.noise_vars), pin=True)
+    ref2 = rec(host2["y"], host2["indices"], host2["counts"], host2["probs"], host2["noise_var"], 5).cpu().clone()
+    assert not torch.equal(ref, ref2)
+    srec = vdamp.StreamingReconstructor(cfg.size, cfg.size, cfg.scales, 4, precision="fp32", depth=depth)
+    outs = [torch.empty(ref.shape, dtype=ref.dtype).pin_memory() for _ in range(7)]
+    for i in range(7):
+        srec.submit(host2 if i % 2 else host, 5, outs[i])
     srec.wait()
-    for o in outs:
-        assert torch.equal(o, ref)
+    for i, o in enumerate(outs):
+        assert torch.equal(o, ref2 if i % 2 else ref), i
 
 
 def test_lanes_bitwise_equal():
