@@ -73,6 +73,10 @@ struct Plan {
     void* twW = nullptr;
     // fp32 subbands > SCAP: value-range split over several CTAs (big_keys / big_range)
     bool bigpath = false;
+    bool cluster = false;           // few subbands of >= 16,384 keys: one thread-block cluster per subband (sure_winc)
+    bool cluster16 = false;         // ... of 16 CTAs for subbands of >= 131,072 keys (non-portable size, if schedulable)
+    cudaStream_t side2 = nullptr;   // second fork/join stream (cluster mode: mid-size subbands)
+    cudaEvent_t ev_join2 = nullptr;
     std::vector<int> large;         // subband ids
     int big_ranges = 0, big_chunks = 0;
     unsigned* bhist = nullptr;      // [B][nlarge][BIGB]
@@ -264,6 +268,27 @@ void launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t sm, cudaStream_t 
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+}
+
+// The same with a thread-block cluster of `cs` CTAs along x (cs > 8: the kernel must have been
+// opted into non-portable cluster sizes)
+template <typename... KArgs, typename... Args>
+void launch_cluster(void (*k)(KArgs...), int cs, dim3 grid, dim3 block, size_t sm, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     CK(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
 }
 
@@ -545,7 +570,7 @@ struct Seq {
         // 128-thread CTAs with little shared memory, many per SM
         // the small-subband kernel runs on a side stream, concurrently with the
         // big one (its CTAs fill the SMs the big kernel's tail leaves idle)
-        bool forked = false;
+        bool forked = false, forked2 = false;
         std::vector<int> win_items, win_large;     // subbands taken by sure_win32 (fp32): shared / global keys
         if constexpr (std::is_same<R, float>::value) {
             if (p->bigpath) {
@@ -630,10 +655,11 @@ struct Seq {
                 if ((pm & 1) && p->ntiles <= WN_MAXT) {
                     // lp: keys in shared memory; lg: 32,768 .. 131,072 keys in L2-resident global
                     // scratch (1024-thread CTAs); lr: the rest (sure_select)
-                    std::vector<int> lp, lg, lr;
+                    std::vector<int> lp, lg, lr, lc;
                     for (int j : li) {
                         const int n = p->geo.len[j];
-                        if (n == 16384 || n == 8192 || n == 4096) lp.push_back(j);
+                        if (p->cluster && p->kA && n >= 16384 && n <= (1 << 20) && (n & (n - 1)) == 0) lc.push_back(j);
+                        else if (n == 16384 || n == 8192 || n == 4096) lp.push_back(j);
                         else if ((pm & 2) && p->kA && (n == 32768 || n == 65536 || n == 131072)) lg.push_back(j);
                         else lr.push_back(j);
                     }
@@ -649,8 +675,63 @@ struct Seq {
                     };
                     // larger subbands first (one long-running 1024-thread CTA each): the other
                     // sure_win32 launches then run beside them on the side stream
-                    const bool has_large = !lr.empty() || !lg.empty();
+                    const bool has_large = !lr.empty() || !lg.empty() || !lc.empty();
                     if (has_large && can_fork) fork();
+                    // clusters: subbands of >= 131,072 keys on 16 CTAs each (this stream), the others
+                    // on 8 CTAs each (second side stream), one launch per cluster size
+                    int lcmax = 0;
+                    for (int j : lc) lcmax = std::max(lcmax, p->geo.len[j]);
+                    if (!lc.empty() && lcmax <= 32768) {
+                        // only 16,384 / 32,768-key subbands (cfg0): 512-thread CTAs with the smaller
+                        // histograms (28 vs 53 us per launch for 16,384 keys)
+                        for (int n : {32768, 16384}) {
+                            std::vector<int> ln;
+                            for (int j : lc) if (p->geo.len[j] == n) ln.push_back(j);
+                            if (ln.empty()) continue;
+                            set_items(ln);
+                            Launch L(p, 3, ls);
+                            const dim3 grid(8u * (unsigned)p->B, (unsigned)ln.size());
+                            if (n == 32768) {
+                                auto k = sure_winc<512, 8, 8>;
+                                set_smem(k, wn_smem_bytes<512, 8, true, 8>());
+                                launch_cluster(k, 8, grid, 512, wn_smem_bytes<512, 8, true, 8>(), ls, p->geo, a);
+                            } else {
+                                auto k = sure_winc<512, 4, 8>;
+                                set_smem(k, wn_smem_bytes<512, 4, true, 8>());
+                                launch_cluster(k, 8, grid, 512, wn_smem_bytes<512, 4, true, 8>(), ls, p->geo, a);
+                            }
+                        }
+                        for (int j : lc) (p->geo.len[j] > 16384 ? win_large : win_items).push_back(j);
+                    } else if (!lc.empty()) {
+                        std::vector<int> l16, l8;
+                        for (int j : lc) (p->cluster16 && p->geo.len[j] >= 131072 ? l16 : l8).push_back(j);
+                        auto by_len = [&](int x, int y) { return p->geo.len[x] > p->geo.len[y]; };
+                        std::stable_sort(l16.begin(), l16.end(), by_len);
+                        std::stable_sort(l8.begin(), l8.end(), by_len);
+                        const size_t sm = wn_smem_bytes<1024, 0, true, 8>();
+                        if (!l16.empty()) {
+                            set_items(l16);
+                            Launch L(p, 3, ls);
+                            auto k = sure_winc<1024, 0, 16>;
+                            set_smem(k, sm);
+                            launch_cluster(k, 16, dim3(16u * (unsigned)p->B, (unsigned)l16.size()), 1024, sm, ls, p->geo, a);
+                        }
+                        if (!l8.empty()) {
+                            cudaStream_t l2 = ls;
+                            if (can_fork && p->side2 && !l16.empty()) {
+                                fork();
+                                CK(cudaStreamWaitEvent(p->side2, p->ev_fork, 0));
+                                l2 = p->side2;
+                                forked2 = true;
+                            }
+                            set_items(l8);
+                            Launch L(p, 3, l2);
+                            auto k = sure_winc<1024, 0, 8>;
+                            set_smem(k, sm);
+                            launch_cluster(k, 8, dim3(8u * (unsigned)p->B, (unsigned)l8.size()), 1024, sm, l2, p->geo, a);
+                        }
+                        for (int j : lc) (p->geo.len[j] > 16384 ? win_large : win_items).push_back(j);
+                    }
                     if (!lr.empty()) {
                         pm &= 2;
                         launch_big(lr);
@@ -667,7 +748,7 @@ struct Seq {
                         if (n == 131072) WN_LAUNCH_G(128) else if (n == 65536) WN_LAUNCH_G(64) else WN_LAUNCH_G(32)
 #undef WN_LAUNCH_G
                     }
-                    win_large = lg;
+                    win_large.insert(win_large.end(), lg.begin(), lg.end());
                     // few CTAs (small batches): wider CTAs, half the keys per thread
                     const bool few = (long long)p->Ball * 3 < (long long)p->nsm;
                     for (int n : {16384, 8192, 4096}) {
@@ -689,7 +770,7 @@ struct Seq {
                         else WN_LAUNCH(256, 16)
 #undef WN_LAUNCH
                     }
-                    win_items = lp;
+                    win_items.insert(win_items.end(), lp.begin(), lp.end());
                     continue;
                 }
             }
@@ -698,6 +779,10 @@ struct Seq {
         if (forked) {
             CK(cudaEventRecord(p->ev_join, p->side));
             CK(cudaStreamWaitEvent(st_, p->ev_join, 0));
+        }
+        if (forked2) {
+            CK(cudaEventRecord(p->ev_join2, p->side2));
+            CK(cudaStreamWaitEvent(st_, p->ev_join2, 0));
         }
         if constexpr (std::is_same<R, float>::value) {
             static const int wfull = [] { const char* e = getenv("VDAMP_WINFULL"); return e ? atoi(e) : 1; }();   // 0: timing experiments only
@@ -927,6 +1012,8 @@ void free_plan(Plan* p) {
     for (auto& e : p->ev) { cudaEventDestroy(e.second.first); cudaEventDestroy(e.second.second); }
     drop_graph(p);
     if (p->side) cudaStreamDestroy(p->side);
+    if (p->side2) cudaStreamDestroy(p->side2);
+    if (p->ev_join2) cudaEventDestroy(p->ev_join2);
     if (p->gstream) cudaStreamDestroy(p->gstream);
     if (p->ev_in) cudaEventDestroy(p->ev_in);
     if (p->ev_out) cudaEventDestroy(p->ev_out);
@@ -1087,13 +1174,53 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         p->pflag = (unsigned*)dalloc(p, (size_t)batch * p->S * sizeof(unsigned));
         const int maxlen = *std::max_element(g.len, g.len + p->S);
         const int capk = precision == VDAMP_FP32 ? Scap<float>::v : Scap<double>::v;
+        CK(cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, device));
+        {
+            // fp32, few subbands of >= 16,384 keys (cfg0: 1 image x 3, cfg3: 1 x 9): a cluster of
+            // 8 CTAs per subband (sure_winc) instead of one CTA, or of value ranges over CTAs
+            int nbig = 0;
+            for (int j = 0; j < p->S; ++j) nbig += g.len[j] >= 16384;
+            const char* ce = getenv("VDAMP_CLUSTER");
+            p->cluster = precision == VDAMP_FP32 && nbig > 0 && (long long)batch * nbig * 8 <= (long long)p->nsm &&
+                         !(ce && atoi(ce) == 0);
+            if (p->cluster && maxlen <= capk) p->kA = dalloc(p, img * rs);      // the clusters' key scratch
+            if (p->cluster) {
+                p->side2 = create_side_stream();
+                CK(cudaEventCreateWithFlags(&p->ev_join2, cudaEventDisableTiming));
+                // 16-CTA clusters (non-portable size) for the largest subbands, if the device can
+                // place one with this kernel's shared memory
+                // (measured slower: 104 vs 80 us for a 262,144-key subband, cfg3 5.3k vs 5.5k
+                // img-iter/s; off unless VDAMP_CLUSTER16=1)
+                const char* c16 = getenv("VDAMP_CLUSTER16");
+                if (maxlen >= 131072 && c16 && atoi(c16) == 1) {
+                    auto k = sure_winc<1024, 0, 16>;
+                    const size_t sm = wn_smem_bytes<1024, 0, true, 8>();
+                    bool ok = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+                              cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) == cudaSuccess;
+                    if (ok) {
+                        cudaLaunchConfig_t cfg = {};
+                        cfg.gridDim = dim3(16, 1, 1);
+                        cfg.blockDim = dim3(1024, 1, 1);
+                        cfg.dynamicSmemBytes = sm;
+                        cudaLaunchAttribute at[1];
+                        at[0].id = cudaLaunchAttributeClusterDimension;
+                        at[0].val.clusterDim.x = 16; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+                        cfg.attrs = at;
+                        cfg.numAttrs = 1;
+                        int nc = 0;
+                        ok = cudaOccupancyMaxActiveClusters(&nc, k, &cfg) == cudaSuccess && nc >= 1;
+                    }
+                    cudaGetLastError();
+                    p->cluster16 = ok;
+                }
+            }
+        }
         if (maxlen > capk) {
             if (maxlen / capk > MAXTILES) throw Err{VDAMP_ERR_UNSUPPORTED, "subband too large"};
             p->kA = dalloc(p, img * rs);
             p->kB = dalloc(p, img * rs);
-            CK(cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, device));
             const char* be = getenv("VDAMP_BIGRANGE");
-            if (precision == VDAMP_FP32 && !(be && atoi(be) == 0)) {
+            if (precision == VDAMP_FP32 && !p->cluster && !(be && atoi(be) == 0)) {
                 for (int j = 0; j < p->S; ++j) if (g.len[j] > capk) p->large.push_back(j);
                 // only when the single-CTA path would leave most SMs idle: with many large
                 // subbands per batch (cfg2: 32 x 3) it fills the GPU and is measured faster
@@ -1372,6 +1499,7 @@ Plan lane_view(const Plan* p, int b0, int nb, const Plan::Lane& l) {
     }
     v.B = nb;
     v.side = l.side; v.ev_fork = l.fork; v.ev_join = l.join;
+    v.side2 = nullptr;                 // (one per plan: lanes keep their clusters on their own stream)
     v.ev.clear();
     v.lane.clear(); v.lanes = 1;
     return v;

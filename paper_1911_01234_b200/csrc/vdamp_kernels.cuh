@@ -16,6 +16,7 @@
 // modulation; the output sign is folded into y at setup.
 #pragma once
 #include "vdamp_device.cuh"
+#include <cooperative_groups.h>
 #include <type_traits>
 
 namespace vdamp {

@@ -48,13 +48,26 @@ struct WnScratch {                     // per-warp partials, double-buffered
     float scale[2];
 };
 
-// GLOBAL: the keys stay in L2-resident global scratch (subbands beyond the shared capacity)
-template <int NT, int EF, bool GLOBAL = false>
+// GLOBAL: the keys stay in L2-resident global scratch (subbands beyond the shared capacity).
+// CS > 1 (cluster of CS CTAs per subband, GLOBAL keys): a second counter array holds the
+// histograms merged over the cluster.
+template <int NT, int EF, bool GLOBAL = false, int CS = 1>
 __host__ __device__ constexpr size_t wn_smem_bytes() {
     typedef Wn<NT, EF, GLOBAL> W;
-    return (GLOBAL ? 0 : (size_t)W::SLOT * 4) + (size_t)(W::NC + W::NF + 32) * 4 + sizeof(WnScratch<NT / 32>) +
-           (size_t)2 * W::LIST * 4;
+    return (GLOBAL ? 0 : (size_t)W::SLOT * 4) + (size_t)(W::NC + W::NF + 32) * 4 * (CS > 1 ? 2 : 1) +
+           sizeof(WnScratch<NT / 32>) + (size_t)2 * W::LIST * 4;
 }
+
+// Per-CTA partial results exchanged through distributed shared memory (cluster variant):
+// every CTA publishes its own and reads all of them in rank order (fixed order: deterministic,
+// and identical in every CTA of the cluster)
+struct WnX {
+    unsigned mn, mx;                   // key-bit range of the CTA's keys
+    float pbf, iaf, cblf;              // float sums outside the coarse span
+    unsigned nxb, pvb;                 // first key above / largest key below the window
+    double pre, suf;                   // exact sums outside the window
+    double err, ref;                   // trace error sums
+};
 
 __device__ __forceinline__ float wn_rcp(float x) {
     float r;
@@ -323,11 +336,24 @@ __device__ __forceinline__ void wn_scan_list(const float* list, int Lr, int nb, 
 // grp, list: Wn<NT, EF, GLOBAL>::LIST keys each.  Leaves the window argmin in S_.run (and
 // S_.totinv).  Returns false (scratch clobbered, keys intact) when the caller must sort
 // all keys.
-template <int NT, int EF, bool GLOBAL, typename SS>
+//
+// CS > 1: the subband's n = CS * EF * NT keys are spread over a cluster of CS CTAs (keys: this
+// CTA's EF * NT).  Every CTA histograms its own keys; after a cluster barrier each merges all
+// CS histograms into its own copy (cnt + NC + NF + 32) and runs the same bounds on it, so all
+// CTAs take the same decisions without a broadcast; per-CTA sums go through X (rank order).
+// Window keys are appended to rank 0's grouped list by distributed-shared-memory atomics;
+// rank 0 alone ranks and scans the list.  Returns true in every CTA; S_.run / out are rank 0's.
+template <int NT, int EF, bool GLOBAL, int CS = 1, typename SS>
 __device__ __forceinline__ bool select_win(int n, double tau, const float* keys, unsigned* cnt, float* grp, float* list,
                                            WnScratch<NT / 32>& sc, unsigned kmn, unsigned kmx, SS& S_, PrOut& out,
-                                           long long* dbg = nullptr) {
+                                           long long* dbg = nullptr, WnX* X = nullptr, int ef_rt = 0) {
     typedef Wn<NT, EF, GLOBAL> W;
+    const int ef = EF > 0 ? EF : ef_rt;            // keys per thread (EF == 0: a launch-time value)
+    namespace cg = ::cooperative_groups;
+    [[maybe_unused]] cg::cluster_group cluster = cg::this_cluster();
+    [[maybe_unused]] const unsigned crank = CS > 1 ? cluster.block_rank() : 0u;
+    // leave together: no CTA may exit while another still reads its shared memory
+    auto fail = [&]() { if constexpr (CS > 1) cluster.sync(); return false; };
     constexpr int LE = W::LE, WN_NW = W::NW, NW = WN_NW, WN_NC = W::NC, WN_NF = W::NF, WN_LMAX = W::LMAX;
     const unsigned* kb = reinterpret_cast<const unsigned*>(keys);
     // key q of this thread: shared memory (KI layout), or global scratch through L2
@@ -340,9 +366,27 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
     PR_NOTE(8, -1);
 #endif
     const int tid = threadIdx.x, l = tid & 31, w = tid >> 5, q16 = l & (WN_NW - 1);
-    unsigned* cc = cnt;                    // coarse counts
+    unsigned* cc = cnt;                    // coarse counts (this CTA's keys)
     unsigned* cf = cnt + WN_NC;            // fine counts
+    // the counts the bounds run on: merged over the cluster, or the CTA's own
+    unsigned* ccm = CS > 1 ? cnt + (WN_NC + WN_NF + 32) : cc;
+    unsigned* cfm = ccm + WN_NC;
     int ph = 0;
+    // ccm/cfm[b] = sum over the cluster's CTAs of their cc/cf[b] (after a cluster barrier)
+    auto merge_counts = [&](unsigned* dst, unsigned* src, int words) {
+        if constexpr (CS > 1) {
+            for (int i = tid; i < words / 4; i += NT) {
+                uint4 s4 = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll 8
+                for (int r = 0; r < CS; ++r) {
+                    const uint4 v = reinterpret_cast<const uint4*>(cluster.map_shared_rank(src, r))[i];
+                    s4.x += v.x; s4.y += v.y; s4.z += v.z; s4.w += v.w;
+                }
+                reinterpret_cast<uint4*>(dst)[i] = s4;
+            }
+            __syncthreads();
+        }
+    };
 
     // ---- 1. key range, coarse map, coarse histogram ---------------------------
     kmn = __reduce_min_sync(0xffffffffu, kmn);
@@ -353,16 +397,31 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
         for (int i = tid; i < (WN_NC + WN_NF) / 4; i += NT) cz[i] = make_uint4(0u, 0u, 0u, 0u);
     }
     __syncthreads();
-    const unsigned mn = __reduce_min_sync(0xffffffffu, sc.u[ph][q16]);
-    const unsigned mx = __reduce_max_sync(0xffffffffu, sc.u[ph][WN_NW + q16]);
+    unsigned mn = __reduce_min_sync(0xffffffffu, sc.u[ph][q16]);
+    unsigned mx = __reduce_max_sync(0xffffffffu, sc.u[ph][WN_NW + q16]);
     ph ^= 1;
-    if (mn > mx) return false;                     // all keys zero: the full path handles it
+    if constexpr (CS > 1) {
+        if (tid == 0) { X->mn = mn; X->mx = mx; }
+        cluster.sync();
+#pragma unroll
+        for (int r = 0; r < CS; ++r) {
+            const WnX* xr = cluster.map_shared_rank(X, r);
+            mn = min(mn, xr->mn);
+            mx = max(mx, xr->mx);
+        }
+        if (crank == 0 && tid == 0) {              // trace error sums of the whole subband (rank order)
+            double e2 = 0.0, r2 = 0.0;
+            for (int r = 0; r < CS; ++r) { const WnX* xr = cluster.map_shared_rank(X, r); e2 += xr->err; r2 += xr->ref; }
+            S_.err = e2; S_.ref = r2;
+        }
+    }
+    if (mn > mx) return fail();                    // all keys zero: the full path handles it
     // The float bounds work on keys scaled by ksc = 2^-e (e: exponent of the largest key; exact)
     // and tau scaled by ksc^2: comparing bounds is invariant under it, and squares and
     // reciprocal sums stay well inside the float range for data of any magnitude (diverged
     // runs).  Normal keys below 2^100 (bucket edges past the largest key stay finite) spanning at
     // most 100 octaves; else the full path.
-    if (mn < 0x00800000u || mx >= ((127u + 100u) << 23) || (mx >> 23) - (mn >> 23) > 100u) return false;
+    if (mn < 0x00800000u || mx >= ((127u + 100u) << 23) || (mx >> 23) - (mn >> 23) > 100u) return fail();
     const float ksc = __uint_as_float((254u - (mx >> 23)) << 23);
     const float tauf = (float)(tau * (double)ksc * (double)ksc), ntauf = (float)((double)n * tau * (double)ksc * (double)ksc);
     WnMap C;
@@ -381,17 +440,18 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
         C.top = WN_NC;
     }
 #pragma unroll 8
-    for (int q = 0; q < EF; ++q) atomicAdd(&cc[C.bucket(key(q))], 1u);
-    __syncthreads();
+    for (int q = 0; q < ef; ++q) atomicAdd(&cc[C.bucket(key(q))], 1u);
+    if constexpr (CS > 1) cluster.sync(); else __syncthreads();
+    merge_counts(ccm, cc, WN_NC);
     PR_MARK(0);
-    if (WN_CUT == 0) return false;
+    if (WN_CUT == 0) return fail();
 
     // ---- 2. coarse bounds -> span [g0, g1] -------------------------------------
     int g0, g1;
-    const float Ulim = wn_stage<NT, WN_NC / NT>(cc, C, ksc, 0, WN_NC, true, 0.0f, 0.0f, 0.0f, n, tauf, ntauf, INFINITY, sc, ph, g0, g1);
-    if (g1 < 0) return false;
+    const float Ulim = wn_stage<NT, WN_NC / NT>(ccm, C, ksc, 0, WN_NC, true, 0.0f, 0.0f, 0.0f, n, tauf, ntauf, INFINITY, sc, ph, g0, g1);
+    if (g1 < 0) return fail();
     PR_MARK(1);
-    if (WN_CUT == 1) return false;
+    if (WN_CUT == 1) return fail();
 
     // ---- 3. float sums outside the span, fine histogram inside ----------------
     WnMap F;
@@ -415,7 +475,7 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
     const unsigned khi = g1 >= WN_NC - 1 ? 0xffffffffu : C.lowbits(g1 + 1);   // at or above khi: above it
     float pbf = 0.0f, iaf = 0.0f, cblf = 0.0f;
 #pragma unroll 8
-    for (int q = 0; q < EF; ++q) {
+    for (int q = 0; q < ef; ++q) {
         const unsigned k = key(q);
         const float mf = __uint_as_float(k) * ksc;
         const bool below = k < klo, above = k >= khi;
@@ -426,15 +486,26 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
     }
     wn_sum3<NW>(pbf, iaf, cblf, sc.f[ph]);
     ph ^= 1;
+    if constexpr (CS > 1) {
+        if (tid == 0) { X->pbf = pbf; X->iaf = iaf; X->cblf = cblf; }
+        cluster.sync();
+        pbf = iaf = cblf = 0.0f;
+#pragma unroll
+        for (int r = 0; r < CS; ++r) {
+            const WnX* xr = cluster.map_shared_rank(X, r);
+            pbf += xr->pbf; iaf += xr->iaf; cblf += xr->cblf;
+        }
+        merge_counts(cfm, cf, WN_NF);
+    }
     PR_MARK(2);
-    if (WN_CUT == 2) return false;
+    if (WN_CUT == 2) return fail();
 
     // ---- 4. fine bounds -> window [f0, f1] ---------------------------------------
     int f0, f1;
-    wn_stage<NT, WN_NF / NT>(cf, F, ksc, flo, F.top, false, pbf, iaf, cblf, n, tauf, ntauf, Ulim, sc, ph, f0, f1);
-    if (f1 < 0) return false;
+    wn_stage<NT, WN_NF / NT>(cfm, F, ksc, flo, F.top, false, pbf, iaf, cblf, n, tauf, ntauf, Ulim, sc, ph, f0, f1);
+    if (f1 < 0) return fail();
     PR_MARK(3);
-    if (WN_CUT == 3) return false;
+    if (WN_CUT == 3) return fail();
 
     // ---- 5. window offsets: fine-bucket cursors (exclusive scan of the window counts) ----
     const unsigned wlo = F.lowbits(f0);
@@ -446,7 +517,7 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
 #pragma unroll
         for (int i = 0; i < KF; ++i) {
             const int b = KF * tid + i;
-            const int v = (b >= flo && b < F.top) ? (int)cf[b] : 0;
+            const int v = (b >= flo && b < F.top) ? (int)cfm[b] : 0;
             c[i] = (b >= f0 && b <= f1) ? v : 0;
             own += c[i];
             bel += b < f0 ? v : 0;
@@ -468,23 +539,25 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
         nbw = (int)cblf + tb;                      // keys below the window
         base = nbw > 0 ? 1 : 0;                    // slot 0: the largest key below the window
         PR_NOTE(7, Lw);
-        if (Lw + base > WN_LMAX || Lw + base < 1) return false;
+        if (Lw + base > WN_LMAX || Lw + base < 1) return fail();
         int run = base + pw + (inc - own);
 #pragma unroll
         for (int i = 0; i < KF; ++i) {
             const int b = KF * tid + i;
-            if (b >= f0 && b <= f1) cf[b] = (unsigned)run;
+            if (b >= f0 && b <= f1) cfm[b] = (unsigned)run;
             run += c[i];
         }
     }
-    __syncthreads();
+    if constexpr (CS > 1) cluster.sync(); else __syncthreads();      // (rank 0's cursors are the cluster's)
+    unsigned* cur = CS > 1 ? cluster.map_shared_rank(cfm, 0) : cfm;
+    float* grp0 = CS > 1 ? cluster.map_shared_rank(grp, 0) : grp;
 
     // ---- 6. exact float64 offsets (all keys), window keys grouped by fine bucket ----------
     double pre = 0.0, suf = 0.0;
     unsigned nxb = 0xffffffffu, pvb = 0u;
     // branch-free arithmetic first (independent reciprocal chains of the unrolled keys) ...
 #pragma unroll 4
-    for (int q = 0; q < EF; ++q) {
+    for (int q = 0; q < ef; ++q) {
         const unsigned k = key(q);
         const bool below = k < wlo, above = k >= whi;
         const double md = (double)__uint_as_float(k);
@@ -496,11 +569,11 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
     }
     // ... then the (few) window keys into their fine buckets
 #pragma unroll 8
-    for (int q = 0; q < EF; ++q) {
+    for (int q = 0; q < ef; ++q) {
         const unsigned k = key(q);
         if (k >= wlo && k < whi) {
-            const unsigned pos = atomicAdd(&cf[F.bucket(k)], 1u);
-            grp[KI(pos)] = __uint_as_float(k);
+            const unsigned pos = atomicAdd(&cur[F.bucket(k)], 1u);
+            grp0[KI(pos)] = __uint_as_float(k);
         }
     }
     {
@@ -523,6 +596,21 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
             suf += __shfl_xor_sync(0xffffffffu, suf, o);
         }
     }
+    if constexpr (CS > 1) {
+        if (tid == 0) { X->pre = pre; X->suf = suf; X->nxb = nxb; X->pvb = pvb; }
+        cluster.sync();                            // partials and every CTA's window keys have landed
+        if (crank == 0) {
+            pre = suf = 0.0;
+#pragma unroll
+            for (int r = 0; r < CS; ++r) {
+                const WnX* xr = cluster.map_shared_rank(X, r);
+                pre += xr->pre; suf += xr->suf;
+                nxb = min(nxb, xr->nxb); pvb = max(pvb, xr->pvb);
+            }
+        }
+        cluster.sync();                            // rank 0 has read them: the other CTAs are done
+        if (crank != 0) return true;
+    }
     const double mprev = (double)__uint_as_float(pvb);
     const double nxt = nxb == 0xffffffffu ? (double)INFINITY : (double)__uint_as_float(nxb);
     PR_MARK(4);
@@ -539,8 +627,8 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
     for (int p = base + tid; p < Lr; p += NT) {
         const float x = grp[KI(p)];
         const int fb = F.bucket(__float_as_uint(x));
-        const int e1 = (int)cf[fb];
-        const int s0 = fb == f0 ? base : (int)cf[fb - 1];
+        const int e1 = (int)cfm[fb];
+        const int s0 = fb == f0 ? base : (int)cfm[fb - 1];
         int rank = 0;
         for (int q = s0; q < e1; ++q) {
             const float y = grp[KI(q)];
@@ -576,15 +664,19 @@ struct WnShared {
 // One subband of n = EF * NT keys: load, |r| keys (+ trace error sums), tau,
 // select_win, outputs.  Returns false when the bounds leave too many keys.
 // Shared memory: keys (KI layout) | counters | scratch | grouped list | sorted list.
-template <int NT, int EF, bool GLOBAL>
+template <int NT, int EF, bool GLOBAL, int CS = 1>
 __device__ __forceinline__ bool win_band(const Geo& g, const SelArgs<float>& a, int j, int bi, float* keys,
-                                         WnShared<NT>& S_) {
+                                         WnShared<NT>& S_, WnX* X = nullptr) {
     typedef float2 C;
     const int tid = threadIdx.x;
-    const int n = g.len[j];                                    // == EF * NT
-    const long long base = (long long)bi * g.N + g.off[j];
+    const int n = g.len[j];                                    // == CS * ef * NT
+    const int ef = EF > 0 ? EF : n / (CS * NT);                // EF == 0: any subband of a multiple of CS * NT keys
+    [[maybe_unused]] const unsigned crank = CS > 1 ? ::cooperative_groups::this_cluster().block_rank() : 0u;
+    const long long slice = CS > 1 ? (long long)crank * (ef * NT) : 0;     // this CTA's keys of the subband
+    const long long base = (long long)bi * g.N + g.off[j] + slice;
+    const long long pj = (long long)bi * g.S + j;
     if (a.tau_in) {
-        if (tid == 0) S_.tau = a.tau_in[(long long)bi * g.S + j];
+        if (tid == 0) S_.tau = a.tau_in[pj];
     } else {
         for (int i = tid; i < a.ntiles; i += NT) S_.tpart[i] = a.taupart[((long long)bi * a.ntiles + i) * g.S + j];
     }
@@ -594,13 +686,12 @@ __device__ __forceinline__ bool win_band(const Geo& g, const SelArgs<float>& a, 
     unsigned kmn = 0xffffffffu, kmx = 0u;
     typedef Wn<NT, EF, GLOBAL> W;
     unsigned* cnt = reinterpret_cast<unsigned*>(GLOBAL ? keys : keys + W::SLOT);
-    WnScratch<NT / 32>& sc = *reinterpret_cast<WnScratch<NT / 32>*>(cnt + W::NC + W::NF + 32);
+    WnScratch<NT / 32>& sc = *reinterpret_cast<WnScratch<NT / 32>*>(cnt + (W::NC + W::NF + 32) * (CS > 1 ? 2 : 1));
     float* grp = reinterpret_cast<float*>(&sc + 1);          // window keys grouped by fine bucket
     float* list = grp + W::LIST;                             // ... sorted
     float* kst = GLOBAL ? a.kA + base : keys;                // where the keys go
-    constexpr int LB = 8;                                      // loads in flight per thread
-#pragma unroll 1
-    for (int e0 = tid; e0 < EF * NT; e0 += LB * NT) {
+    constexpr int LB = EF == 0 ? 2 : (EF < 8 ? EF : 8);       // loads in flight per thread (EF == 0: x 4 by unrolling)
+    auto load_keys = [&](int e0) {
         C v[LB];
 #pragma unroll
         for (int u = 0; u < LB; ++u) v[u] = rs[e0 + u * NT];
@@ -623,6 +714,13 @@ __device__ __forceinline__ bool win_band(const Geo& g, const SelArgs<float>& a, 
                 ref += (double)wv.x * (double)wv.x + (double)wv.y * (double)wv.y;
             }
         }
+    };
+    if constexpr (EF == 0) {
+#pragma unroll 4
+        for (int e0 = tid; e0 < ef * NT; e0 += LB * NT) load_keys(e0);
+    } else {
+#pragma unroll 1
+        for (int e0 = tid; e0 < EF * NT; e0 += LB * NT) load_keys(e0);
     }
     __syncthreads();
     if (!a.tau_in && tid == 0) {
@@ -632,17 +730,21 @@ __device__ __forceinline__ bool win_band(const Geo& g, const SelArgs<float>& a, 
     }
     if (w0) {
         const double e2 = block_sum<NT>(err, S_.sh), r2 = block_sum<NT>(ref, S_.sh);
-        if (tid == 0) { S_.err = e2; S_.ref = r2; }
+        if (tid == 0) {
+            if constexpr (CS > 1) { X->err = e2; X->ref = r2; }    // summed over the cluster by select_win
+            else { S_.err = e2; S_.ref = r2; }
+        }
     }
     __syncthreads();
     const double tau = fmax(S_.tau, TAU_FLOOR);
 #ifdef VDAMP_PHASE_TIMING
-    long long* pdbg = bi < 4096 ? &g_prune[bi][j][0] : nullptr;
+    long long* pdbg = (bi < 4096 && crank == 0) ? &g_prune[bi][j][0] : nullptr;
 #else
     long long* pdbg = nullptr;
 #endif
     PrOut po{0, 0.0};
-    if (!select_win<NT, EF, GLOBAL>(n, tau, kst, cnt, grp, list, sc, kmn, kmx, S_, po, pdbg)) return false;
+    if (!select_win<NT, EF, GLOBAL, CS>(n, tau, kst, cnt, grp, list, sc, kmn, kmx, S_, po, pdbg, X, ef)) return false;
+    if (CS > 1 && crank != 0) return true;                     // rank 0 holds the result
     select_finish<float, NT, WnShared<NT>>(g, a, j, bi, n, tau, po.nbelow == 0 ? po.m0 : 0.0, w0 != nullptr, S_);
     return true;
 }
@@ -663,6 +765,32 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 1024 / NT) sure_win32(con
         const int j = a.item_list[q];
         const bool ok = win_band<NT, EF, GLOBAL>(g, a, j, bi, keys, S_);
         if (threadIdx.x == 0) a.pflag[(long long)bi * g.S + j] = ok ? 0u : 1u;
+        __syncthreads();
+    }
+}
+
+// The same selection with one subband of CS * EF * NT keys spread over a thread-block cluster of
+// CS CTAs (keys in L2-resident global scratch, histograms merged and partial sums exchanged
+// through distributed shared memory; see select_win): for batches with so few subbands of
+// >= 16,384 keys that one CTA per subband would leave most SMs idle and put the whole
+// subband's latency on one SM (cfg0: 1 image x 3 subbands; cfg3: 1 x 9).  Grid: (CS * B, items),
+// cluster dimension (CS, 1, 1) set at launch.  EF == 0: keys per thread = len / (CS * NT) per
+// subband, so one launch takes subbands of different sizes.
+template <int NT, int EF, int CS>
+__global__ void __launch_bounds__(NT, 1) sure_winc(const __grid_constant__ Geo g,
+                                                                             const __grid_constant__ SelArgs<float> a) {
+    pdl_enter();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* keys = reinterpret_cast<float*>(smem_raw);
+    __shared__ WnShared<NT> S_;
+    __shared__ WnX X;
+    const int bi = blockIdx.x / CS, it = blockIdx.y;
+    const unsigned crank = ::cooperative_groups::this_cluster().block_rank();
+    for (int q = a.item_start[it]; q < a.item_start[it + 1]; ++q) {
+        const int j = a.item_list[q];
+        if (q > a.item_start[it]) ::cooperative_groups::this_cluster().sync();     // X and the lists are reused
+        const bool ok = win_band<NT, EF, true, CS>(g, a, j, bi, keys, S_, &X);
+        if (crank == 0 && threadIdx.x == 0) a.pflag[(long long)bi * g.S + j] = ok ? 0u : 1u;
         __syncthreads();
     }
 }

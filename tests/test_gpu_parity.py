@@ -212,9 +212,11 @@ def test_finalize_vs_reference(oracle):
 @pytest.mark.parametrize("shape", [(512, 512, 2), (1024, 1024, 1)])
 @pytest.mark.parametrize("kind", ["gauss", "ties", "zeros", "sparse", "diverged"])
 def test_sure_select_fp32_large_subbands(oracle, shape, kind, monkeypatch):
-    """fp32 subbands > 16,384 keys (value ranges over several CTAs, big_keys/big_range;
-    massive ties fall back to the single-CTA path).  Real float32 inputs make the GPU's
-    float keys and the oracle's float64 magnitudes identical, so the argmin must agree."""
+    """fp32 subbands > 16,384 keys on each of their paths: one thread-block cluster per subband
+    (sure_winc, the default for few large subbands), value ranges over several CTAs
+    (big_keys/big_range, VDAMP_CLUSTER=0) and one CTA per subband (VDAMP_BIGRANGE=0); massive
+    ties fall back to the full sort.  Real float32 inputs make the GPU's float keys and the
+    oracle's float64 magnitudes identical, so the argmin must agree."""
     from paper_1911_01234_b200 import denoise, wavelet
     from paper_1911_01234_b200.plan import clear_plans
     h, w, s = shape
@@ -227,8 +229,9 @@ def test_sure_select_fp32_large_subbands(oracle, shape, kind, monkeypatch):
         tau = tau * 1e24
     wh_o, al_o, lam_o, t_o = oracle.denoise_colored(r, tau, oracle.band_table(h, w, s))
     outs = {}
-    for env in ("1", "0"):
-        monkeypatch.setenv("VDAMP_BIGRANGE", env)
+    for env in ("cluster", "1", "0"):
+        monkeypatch.setenv("VDAMP_CLUSTER", "1" if env == "cluster" else "0")
+        monkeypatch.setenv("VDAMP_BIGRANGE", "1" if env == "cluster" else env)
         clear_plans()
         outs[env] = denoise.denoise_colored(wavelet.WaveletCoeffs(r, lay), denoise.SubbandVector(tau),
                                             precision="fp32")
