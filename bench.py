@@ -186,9 +186,11 @@ EXTRAS = [("cfg1", "fp64"), ("cfg0", "fp32"), ("cfg2", "fp32"), ("cfg2", "fp64")
           ("cfg4_r8", "fp32"), ("cfg4_r8", "fp64"), ("cfg4_r16", "fp32"), ("cfg4_r16", "fp64")]
 
 
-def measure_config(name, precision, steps, warmup, local, procs, peak):
+def measure_config(name, precision, steps, warmup, local, procs, peak, trace=False):
     """Device-resident img-iter/s of one BASELINE config on this GPU (same timing rules as
-    the headline: CUDA events per step, L2 flushed between steps, all images of the config)."""
+    the headline: CUDA events per step, L2 flushed between steps, all images of the config).
+    trace: with ground truth, i.e. per-iteration NMSE and trace records as the reference CLI
+    asks for (src/cli.py:51-55)."""
     import torch
     from paper_1911_01234_b200 import vdamp
     from paper_1911_01234_b200.plan import clear_plans
@@ -204,6 +206,16 @@ def measure_config(name, precision, steps, warmup, local, procs, peak):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     step = lambda: rec(y, idx, inp.counts, probs, inp.noise_var, cfg.n_iters, shared_probs=True, sync=False)
+    if trace:
+        plan = rec.plan
+        plan.set_measurements(y, idx, inp.counts, probs, inp.noise_var, True)
+        plan.set_ground_truth(torch.from_numpy(w.x0).to(dev, cd))
+        trace_buf = plan.new_trace(cfg.n_iters)
+        nmse_buf = torch.zeros((cfg.n_iters, cfg.batch, 2), dtype=torch.float64, device=dev)
+
+        def step():
+            plan.set_measurements(y, idx, inp.counts, probs, inp.noise_var, True, sync_validation=False)
+            return plan.run(cfg.n_iters, x_hat=rec._x, trace=trace_buf, nmse=nmse_buf)
     for _ in range(warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -222,6 +234,7 @@ def measure_config(name, precision, steps, warmup, local, procs, peak):
     b_iter = workload.algorithmic_bytes_per_image_iter(cfg.size * cfg.size, n_mean, b_c)
     out = {"value": value, "unit": UNIT, "precision": precision, "images": cfg.batch, "n_iters": cfg.n_iters,
            "steps": steps, "ms_per_step": float(np.mean(ms)),
+           "trace": "ground truth + per-iteration NMSE/trace records" if trace else "off",
            "workload": f"{cfg.batch} x {cfg.size}^2, Haar s={cfg.scales}, R={cfg.undersampling:g}, "
                        f"{cfg.snr_db:g} dB, {cfg.n_iters} iterations",
            "iteration_roofline": {"B_iter_bytes": b_iter, "achieved_GBps": value * b_iter / 1e9,
@@ -493,6 +506,11 @@ def main():
                 extras[f"{name}_{prec}"] = measure_config(name, prec, args.extras_steps, 3, local, cores, peak)
             except Exception as e:          # report, never hide a failure
                 extras[f"{name}_{prec}"] = {"error": f"{type(e).__name__}: {e}"}
+        try:                                # the production path: ground truth given, trace recorded
+            extras[f"{cfg.name}_{args.precision}_trace"] = measure_config(cfg.name, args.precision, args.extras_steps, 3,
+                                                                          local, cores, peak, trace=True)
+        except Exception as e:
+            extras[f"{cfg.name}_{args.precision}_trace"] = {"error": f"{type(e).__name__}: {e}"}
 
     # ---- roofline of the dominant kernel class -----------------------
     N = cfg.size * cfg.size

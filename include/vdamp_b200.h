@@ -173,10 +173,11 @@ VDAMP_API int vdamp_set_timing(vdamp_plan_t plan, int enable);
 /* Synchronises the recorded events; ms[c] = summed device time, launches[c] = count. */
 VDAMP_API int vdamp_kernel_times(vdamp_plan_t plan, double* ms, int64_t* launches);
 /* vdamp_run captures its whole launch sequence as a CUDA graph (default: on for
- * plans of at most 8 x 256^2 pixels, where launches are short; env VDAMP_GRAPHS=0/1
- * overrides) and replays it while the outputs, iteration count,
- * stream and flags are unchanged.  With timing enabled each graph run synchronises
- * once to accumulate the kernel times. */
+ * plans of at most 64 x 256^2 pixels, where the host's launch rate limits the run;
+ * env VDAMP_GRAPHS=0/1 overrides) and replays it while the outputs, iteration count,
+ * stream and flags are unchanged; the graphs of the last few other combinations are
+ * kept (a pipelined caller alternating output buffers never re-captures).  With
+ * timing enabled each graph run synchronises once to accumulate the kernel times. */
 VDAMP_API int vdamp_set_graphs(vdamp_plan_t plan, int enable);
 /* Image lanes of vdamp_run (with trace, NMSE or snapshots only when interleaved,
  * each lane writing its image range of every record): the batch runs as `lanes` contiguous image ranges on their own streams, forked from

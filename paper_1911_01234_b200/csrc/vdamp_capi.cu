@@ -750,7 +750,8 @@ struct Seq {
                     }
                     win_large.insert(win_large.end(), lg.begin(), lg.end());
                     // few CTAs (small batches): wider CTAs, half the keys per thread
-                    const bool few = (long long)p->Ball * 3 < (long long)p->nsm;
+                    static const int wfew = [] { const char* e = getenv("VDAMP_WINFEW"); return e ? atoi(e) : -1; }();
+                    const bool few = wfew >= 0 ? wfew != 0 : (long long)p->Ball * 3 < (long long)p->nsm;
                     for (int n : {16384, 8192, 4096}) {
                         std::vector<int> ln;
                         for (int j : lp) if (p->geo.len[j] == n) ln.push_back(j);
@@ -759,6 +760,12 @@ struct Seq {
                         // the smaller subbands run beside the 16,384-key launch on the side stream
                         cudaStream_t lw = ls;
                         if (can_fork && (n != 16384 || has_large)) { fork(); lw = p->side; }
+                        // cluster mode (few CTAs, latency-bound): beside the small-subband kernel too
+                        if (lw == p->side && p->cluster && p->side2 && !forked2) {
+                            CK(cudaStreamWaitEvent(p->side2, p->ev_fork, 0));
+                            lw = p->side2;
+                            forked2 = true;
+                        }
                         Launch L(p, 3, lw);
                         const dim3 grid(p->B, (unsigned)ln.size());
 #define WN_LAUNCH(NT_, EF_) { auto k = sure_win32<NT_, EF_>; set_smem(k, wn_smem_bytes<NT_, EF_>()); \
@@ -1181,8 +1188,13 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
             int nbig = 0;
             for (int j = 0; j < p->S; ++j) nbig += g.len[j] >= 16384;
             const char* ce = getenv("VDAMP_CLUSTER");
-            p->cluster = precision == VDAMP_FP32 && nbig > 0 && (long long)batch * nbig * 8 <= (long long)p->nsm &&
-                         !(ce && atoi(ce) == 0);
+            // measured crossovers: 256^2 (16,384-key subbands, 3 per image) 4 images 64.7k vs 56.0k
+            // img-iter/s without clusters, 6 images 70.8k vs 79.5k; 512^2 (65,536-key subbands) 4
+            // images 25.9k vs 17.8k, 8 images 32.3k vs 30.0k
+            const long long ctas = (long long)batch * nbig * 8;
+            p->cluster = precision == VDAMP_FP32 && nbig > 0 && !(ce && atoi(ce) == 0) &&
+                         (maxlen >= 65536 ? ctas <= 3LL * p->nsm : 3 * ctas <= 2LL * p->nsm);
+            if (precision == VDAMP_FP32 && nbig > 0 && ce && atoi(ce) == 1) p->cluster = true;    // forced (A/B runs)
             if (p->cluster && maxlen <= capk) p->kA = dalloc(p, img * rs);      // the clusters' key scratch
             if (p->cluster) {
                 p->side2 = create_side_stream();
