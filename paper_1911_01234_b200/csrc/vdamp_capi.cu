@@ -135,7 +135,16 @@ struct Plan {
     // kernels of the others; diagnostics ride on the lanes when interleaved
     int lanes = 1;
     int Ball = 0;                    // images of the whole plan (a lane view's B is its own range)
-    struct Lane { cudaStream_t st = nullptr, side = nullptr; cudaEvent_t fork = nullptr, join = nullptr, done = nullptr; };
+    struct Lane {
+        cudaStream_t st = nullptr, side = nullptr;
+        cudaEvent_t fork = nullptr, join = nullptr, done = nullptr;
+        cudaEvent_t nm0 = nullptr, nmr = nullptr, nmd = nullptr;
+    };
+    // per-iteration NMSE beside the next iteration (Seq::nmse_iter): events "thresholds ready",
+    // "r consumed", "record written"; nm_pending: an NMSE pass is in flight on the side stream
+    cudaEvent_t ev_nm0 = nullptr, ev_nmr = nullptr, ev_nmd = nullptr;
+    bool nm_pending = false;
+    bool nm_overlap = true;          // VDAMP_NMSE_OVERLAP=0: NMSE passes in line, on the iteration's stream
     std::vector<Lane> lane;
     cudaEvent_t lane_start = nullptr;
     bool have_meas = false;
@@ -398,7 +407,7 @@ struct Seq {
     // rowfft, else the image goes to `img`.
     // early: coef was written at least two kernels before this synthesis (not by
     // the immediately preceding kernel), so synth256 may read it before its PDL wait
-    void synth(const C* coef, const double* par, bool rowfft, C* img, int cls, bool early = false) {
+    void synth(const C* coef, const double* par, bool rowfft, C* img, int cls, bool early = false, C* t1 = nullptr) {
         const int P = (int)p->passes.size();
         for (int i = P - 1; i >= 0; --i) {
             const Pass& ps = p->passes[i];
@@ -409,7 +418,7 @@ struct Seq {
             a.a = ps.a; a.b = ps.b; a.k = ps.k; a.Wa = ps.Wa; a.logWa = ps.logWa;
             a.tw = (const C*)p->twW;
             const bool last = (i == 0);
-            a.dst = last ? (rowfft ? (C*)p->T1 : img) : (C*)p->scratch[i];
+            a.dst = last ? (rowfft ? (t1 ? t1 : (C*)p->T1) : img) : (C*)p->scratch[i];
             a.dst_bs = (long long)ps.Ha * ps.Wa;
             dim3 grid(ps.nstrips, p->B);
             const size_t sm = (size_t)SPN(ps.Wa << ps.k) * sizeof(C);
@@ -843,6 +852,8 @@ struct Seq {
         if (tm) CK(record(p->itev[2 * k], st));
         synth(r(), p->par, true, nullptr, 0, true);        // r: written by K3 two kernels back
         col(COL_VDAMP, (const C*)p->T1, (C*)p->T2, 1);
+        // the previous iteration's NMSE pass (side stream) must have read r before K3 rewrites it
+        if (p->nm_pending) CK(cudaStreamWaitEvent(st, p->ev_nmr, 0));
         analysis(nullptr, true, r(), p->par, true, 2);
         if (snapshot) CK(cudaMemcpyAsync(snapshot, p->r, (size_t)p->B * p->N * sizeof(C), cudaMemcpyDeviceToDevice, st));
         select(r(), nullptr, trace, p->have_gt);
@@ -918,7 +929,32 @@ struct Seq {
     }
 
     // NMSE record of this iteration's estimate into rec[b * VDAMP_NMSE_FIELDS]
+    // The NMSE pass only consumes (r_k, thresholds_k); nothing in the loop consumes its result.
+    // Single-pass geometries run it on the side stream with its own row-FFT buffer (xtmp), beside
+    // K1 / K2 of the next iteration: K3 of that iteration waits until it has read r (ev_nmr), and the
+    // next K4's fork queues behind it on the same side stream.
+    bool nmse_beside() const {
+        return p->parseval && p->nm_overlap && p->side && p->ev_nm0 && !p->timing && p->passes.size() == 1 && p->xtmp;
+    }
+    void nmse_join() {
+        if (!p->nm_pending) return;
+        CK(cudaEventRecord(p->ev_nmd, p->side));
+        CK(cudaStreamWaitEvent(st, p->ev_nmd, 0));
+        p->nm_pending = false;
+    }
     void nmse_iter(double* rec) {
+        if (nmse_beside()) {
+            CK(cudaEventRecord(p->ev_nm0, st));
+            CK(cudaStreamWaitEvent(p->side, p->ev_nm0, 0));
+            Seq<R> s2{p, p->side};
+            s2.synth(r(), p->parf, true, nullptr, 4, false, (C*)p->xtmp);
+            CK(cudaEventRecord(p->ev_nmr, p->side));
+            s2.col(COL_NMSE, (const C*)p->xtmp, nullptr, 4);
+            Launch L(p, 5, p->side);
+            nmse_finish<<<(p->B + 127) / 128, 128, 0, p->side>>>(p->nmpart, p->ntiles, p->nmconst, rec, p->B);
+            p->nm_pending = true;
+            return;
+        }
         if (p->parseval) {
             // x_hat_k = finalize(soft(r_k)): F x_hat is y on the mask and
             // F Psi^H w_hat elsewhere, so one forward FFT suffices
@@ -941,6 +977,7 @@ struct Seq {
             if (nmse_out) nmse_iter(nmse_out + (long long)it * p->B * VDAMP_NMSE_FIELDS);
         }
         finalize_from_r(p->parf, xhat);
+        nmse_join();
     }
 };
 
@@ -973,6 +1010,9 @@ void set_lanes(Plan* p, int nl) {
         CK(cudaEventCreateWithFlags(&l.fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&l.join, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&l.nm0, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&l.nmr, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&l.nmd, cudaEventDisableTiming));
         p->lane.push_back(l);
     }
     if (p->lanes > 1 && !p->lane_start) CK(cudaEventCreateWithFlags(&p->lane_start, cudaEventDisableTiming));
@@ -1020,6 +1060,7 @@ void free_plan(Plan* p) {
     drop_graph(p);
     if (p->side) cudaStreamDestroy(p->side);
     if (p->side2) cudaStreamDestroy(p->side2);
+    for (cudaEvent_t e : {p->ev_nm0, p->ev_nmr, p->ev_nmd}) if (e) cudaEventDestroy(e);
     if (p->ev_join2) cudaEventDestroy(p->ev_join2);
     if (p->gstream) cudaStreamDestroy(p->gstream);
     if (p->ev_in) cudaEventDestroy(p->ev_in);
@@ -1028,6 +1069,7 @@ void free_plan(Plan* p) {
     for (auto& l : p->lane) {
         cudaStreamDestroy(l.st); cudaStreamDestroy(l.side);
         cudaEventDestroy(l.fork); cudaEventDestroy(l.join); cudaEventDestroy(l.done);
+        cudaEventDestroy(l.nm0); cudaEventDestroy(l.nmr); cudaEventDestroy(l.nmd);
     }
     if (p->lane_start) cudaEventDestroy(p->lane_start);
     if (p->ev_join) cudaEventDestroy(p->ev_join);
@@ -1256,6 +1298,13 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
             }
         }
         p->side = create_side_stream();
+        CK(cudaEventCreateWithFlags(&p->ev_nm0, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&p->ev_nmr, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&p->ev_nmd, cudaEventDisableTiming));
+        // pays while the loop is latency-bound (cfg0 with trace 13.2k -> 15.6k img-iter/s, cfg1 fp64
+        // 82.5k -> 84.9k); a batch whose lanes fill the GPU gains nothing (cfg1 fp32 350k -> 343k)
+        p->nm_overlap = batch < 32 || precision == VDAMP_FP64;
+        if (const char* ne = getenv("VDAMP_NMSE_OVERLAP")) p->nm_overlap = atoi(ne) != 0;
         CK(cudaStreamCreateWithFlags(&p->gstream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
@@ -1511,6 +1560,7 @@ Plan lane_view(const Plan* p, int b0, int nb, const Plan::Lane& l) {
     }
     v.B = nb;
     v.side = l.side; v.ev_fork = l.fork; v.ev_join = l.join;
+    v.ev_nm0 = l.nm0; v.ev_nmr = l.nmr; v.ev_nmd = l.nmd; v.nm_pending = false;
     v.side2 = nullptr;                 // (one per plan: lanes keep their clusters on their own stream)
     v.ev.clear();
     v.lane.clear(); v.lanes = 1;
@@ -1593,6 +1643,7 @@ int vdamp_run(vdamp_plan_t plan, int n_iters, void* x_hat, double* trace, double
                         dispatch(&vs[li], (void*)p->lane[li].st, [&](auto& s) {
                             typedef typename std::remove_reference<decltype(s)>::type S_;
                             s.finalize_from_r(s.p->parf, (typename S_::C*)xo);
+                            s.nmse_join();
                         });
                     }
                 } catch (...) {

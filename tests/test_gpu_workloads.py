@@ -189,6 +189,29 @@ def test_parseval_nmse_matches_finalize_path(cfg0_small):
     assert np.abs(out["1"] - out["0"]).max() <= 1e-8
 
 
+@pytest.mark.parametrize("precision,graphs", [("fp32", "0"), ("fp32", "1"), ("fp64", "1")])
+def test_nmse_beside_next_iteration_is_bitwise(precision, graphs):
+    """The per-iteration NMSE pass run on the side stream beside K1 / K2 of the next iteration
+    (small batches; VDAMP_NMSE_OVERLAP) gives bitwise the records, thresholds and x_hat of the
+    in-line pass: the same kernels on the same data, only ordered by events."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); "
+            "from paper_1911_01234_b200 import vdamp, workload; w = workload.make_workload('cfg1', batch=3); "
+            "x, tr = vdamp.run_batch(w.ys, w.masks, w.pmap, w.noise_vars, 4, 9, ground_truths=w.x0, precision=%r); "
+            "print(repr([list(t.nmse_curve()) for t in tr] + [[float(np.abs(x).sum()), float(x.real.sum())]] + "
+            "[[float(r.thresholds.sum()) for r in t.records] for t in tr]))"
+            ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), precision)
+    out = {}
+    for v in ("1", "0"):
+        env = dict(os.environ, VDAMP_NMSE_OVERLAP=v, VDAMP_GRAPHS=graphs)
+        res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True)
+        out[v] = eval(res.stdout.strip().splitlines()[-1])
+    assert out["1"] == out["0"]
+    assert np.isfinite(np.array(out["1"][0])).all()
+
+
 @pytest.mark.parametrize("depth", [1, 2, 3])
 def test_streaming_reconstructor_matches_sync(depth):
     """Pipelined submissions (copies overlapping the neighbouring batches, and with
