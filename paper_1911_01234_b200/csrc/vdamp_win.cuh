@@ -332,7 +332,8 @@ __device__ __forceinline__ void wn_scan_list(const float* list, int Lr, int nb, 
     }
 }
 
-// keys: n = EF * NT float keys at keys[KI(tid + q * NT)].  cnt: NC + NF + 32 words.
+// keys: n = EF * NT float keys, stored linearly; thread tid owns keys KV * (tid + q * NT) + j,
+// j < KV = 4 (one 16-byte access each).  cnt: NC + NF + 32 words.
 // grp, list: Wn<NT, EF, GLOBAL>::LIST keys each.  Leaves the window argmin in S_.run (and
 // S_.totinv).  Returns false (scratch clobbered, keys intact) when the caller must sort
 // all keys.
@@ -355,11 +356,19 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
     // leave together: no CTA may exit while another still reads its shared memory
     auto fail = [&]() { if constexpr (CS > 1) cluster.sync(); return false; };
     constexpr int LE = W::LE, WN_NW = W::NW, NW = WN_NW, WN_NC = W::NC, WN_NF = W::NF, WN_LMAX = W::LMAX;
-    const unsigned* kb = reinterpret_cast<const unsigned*>(keys);
-    // key q of this thread: shared memory (KI layout), or global scratch through L2
-    auto key = [&](int q) -> unsigned {
-        if constexpr (GLOBAL) return __ldcg(kb + threadIdx.x + q * NT);
-        else return kb[KI((int)threadIdx.x + q * NT)];
+    // The thread's keys: KV consecutive keys per access (one 16-byte LDS / L2 load; 8 bytes when
+    // the key count per thread is only known to be even), accesses NT * KV keys apart; keys
+    // stored linearly in shared memory or in global scratch read through L2.
+    constexpr int KV = EF == 0 ? 2 : 4;
+    typedef typename std::conditional<KV == 4, uint4, uint2>::type KVt;
+    const KVt* kb = reinterpret_cast<const KVt*>(keys);
+    const int nacc = ef / KV;
+    auto keyv = [&](int q, unsigned (&kk)[KV]) {
+        KVt t;
+        if constexpr (GLOBAL) t = __ldcg(kb + threadIdx.x + q * NT);
+        else t = kb[threadIdx.x + q * NT];
+        kk[0] = t.x; kk[1] = t.y;
+        if constexpr (KV == 4) { kk[2] = t.z; kk[3] = t.w; }
     };
 #ifdef VDAMP_PHASE_TIMING
     long long pc0_ = clock64();
@@ -439,8 +448,13 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
         C.ls = ls;
         C.top = WN_NC;
     }
-#pragma unroll 8
-    for (int q = 0; q < ef; ++q) atomicAdd(&cc[C.bucket(key(q))], 1u);
+#pragma unroll 2
+    for (int q = 0; q < nacc; ++q) {
+        unsigned kk[KV];
+        keyv(q, kk);
+#pragma unroll
+        for (int j = 0; j < KV; ++j) atomicAdd(&cc[C.bucket(kk[j])], 1u);
+    }
     if constexpr (CS > 1) cluster.sync(); else __syncthreads();
     merge_counts(ccm, cc, WN_NC);
     PR_MARK(0);
@@ -474,15 +488,20 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
     const unsigned klo = C.lowbits(g0);            // key bits below klo: below the span
     const unsigned khi = g1 >= WN_NC - 1 ? 0xffffffffu : C.lowbits(g1 + 1);   // at or above khi: above it
     float pbf = 0.0f, iaf = 0.0f, cblf = 0.0f;
-#pragma unroll 8
-    for (int q = 0; q < ef; ++q) {
-        const unsigned k = key(q);
-        const float mf = __uint_as_float(k) * ksc;
-        const bool below = k < klo, above = k >= khi;
-        pbf = fmaf(below ? mf : 0.0f, mf, pbf);
-        cblf += below ? 1.0f : 0.0f;
-        iaf += above ? wn_rcp(mf) * WN_UP : 0.0f;
-        if (!below && !above) atomicAdd(&cf[F.bucket(k)], 1u);
+#pragma unroll 2
+    for (int q = 0; q < nacc; ++q) {
+        unsigned kk[KV];
+        keyv(q, kk);
+#pragma unroll
+        for (int j = 0; j < KV; ++j) {
+            const unsigned k = kk[j];
+            const float mf = __uint_as_float(k) * ksc;
+            const bool below = k < klo, above = k >= khi;
+            pbf = fmaf(below ? mf : 0.0f, mf, pbf);
+            cblf += below ? 1.0f : 0.0f;
+            iaf += above ? wn_rcp(mf) * WN_UP : 0.0f;
+            if (!below && !above) atomicAdd(&cf[F.bucket(k)], 1u);
+        }
     }
     wn_sum3<NW>(pbf, iaf, cblf, sc.f[ph]);
     ph ^= 1;
@@ -556,24 +575,34 @@ __device__ __forceinline__ bool select_win(int n, double tau, const float* keys,
     double pre = 0.0, suf = 0.0;
     unsigned nxb = 0xffffffffu, pvb = 0u;
     // branch-free arithmetic first (independent reciprocal chains of the unrolled keys) ...
-#pragma unroll 4
-    for (int q = 0; q < ef; ++q) {
-        const unsigned k = key(q);
-        const bool below = k < wlo, above = k >= whi;
-        const double md = (double)__uint_as_float(k);
-        pre = fma(below ? md : 0.0, md, pre);
-        pvb = below ? max(pvb, k) : pvb;
-        const double rr = rcp_posf(above ? md : 1.0);
-        suf += above ? rr : 0.0;
-        nxb = above ? min(nxb, k) : nxb;
+#pragma unroll 1
+    for (int q = 0; q < nacc; ++q) {
+        unsigned kk[KV];
+        keyv(q, kk);
+#pragma unroll
+        for (int j = 0; j < KV; ++j) {
+            const unsigned k = kk[j];
+            const bool below = k < wlo, above = k >= whi;
+            const double md = (double)__uint_as_float(k);
+            pre = fma(below ? md : 0.0, md, pre);
+            pvb = below ? max(pvb, k) : pvb;
+            const double rr = rcp_posf(above ? md : 1.0);
+            suf += above ? rr : 0.0;
+            nxb = above ? min(nxb, k) : nxb;
+        }
     }
     // ... then the (few) window keys into their fine buckets
-#pragma unroll 8
-    for (int q = 0; q < ef; ++q) {
-        const unsigned k = key(q);
-        if (k >= wlo && k < whi) {
-            const unsigned pos = atomicAdd(&cur[F.bucket(k)], 1u);
-            grp0[KI(pos)] = __uint_as_float(k);
+#pragma unroll 2
+    for (int q = 0; q < nacc; ++q) {
+        unsigned kk[KV];
+        keyv(q, kk);
+#pragma unroll
+        for (int j = 0; j < KV; ++j) {
+            const unsigned k = kk[j];
+            if (k >= wlo && k < whi) {
+                const unsigned pos = atomicAdd(&cur[F.bucket(k)], 1u);
+                grp0[KI(pos)] = __uint_as_float(k);
+            }
         }
     }
     {
@@ -690,37 +719,60 @@ __device__ __forceinline__ bool win_band(const Geo& g, const SelArgs<float>& a, 
     float* grp = reinterpret_cast<float*>(&sc + 1);          // window keys grouped by fine bucket
     float* list = grp + W::LIST;                             // ... sorted
     float* kst = GLOBAL ? a.kA + base : keys;                // where the keys go
-    constexpr int LB = EF == 0 ? 2 : (EF < 8 ? EF : 8);       // loads in flight per thread (EF == 0: x 4 by unrolling)
-    auto load_keys = [&](int e0) {
-        C v[LB];
+    // KV consecutive coefficients per access (KV / 2 16-byte loads), QB accesses in flight; the
+    // keys are stored as the matching vector (select_win's layout)
+    constexpr int KV = EF == 0 ? 2 : 4, QB = EF >= 8 ? 2 : 1, HV = KV / 2;
+    typedef typename std::conditional<KV == 4, float4, float2>::type KVf;
+    const float4* rs4 = reinterpret_cast<const float4*>(rs);
+    const float4* w04 = reinterpret_cast<const float4*>(w0);
+    KVf* kv = reinterpret_cast<KVf*>(kst);
+    auto load_keys = [&](int q0) {
+        float4 v[QB][HV];
 #pragma unroll
-        for (int u = 0; u < LB; ++u) v[u] = rs[e0 + u * NT];
+        for (int u = 0; u < QB; ++u)
 #pragma unroll
-        for (int u = 0; u < LB; ++u) {
-            const int e = e0 + u * NT;
-            const float m = cmag(v[u]);
-            if constexpr (GLOBAL) __stcg(kst + e, m);
-            else kst[KI(e)] = m;
-            const unsigned k = __float_as_uint(m);
-            if (k) kmn = min(kmn, k);
-            kmx = max(kmx, k);
+            for (int h = 0; h < HV; ++h) v[u][h] = rs4[HV * (tid + (q0 + u) * NT) + h];
+#pragma unroll
+        for (int u = 0; u < QB; ++u) {
+            float m[KV];
+#pragma unroll
+            for (int h = 0; h < HV; ++h) {
+                m[2 * h] = cmag(make_float2(v[u][h].x, v[u][h].y));
+                m[2 * h + 1] = cmag(make_float2(v[u][h].z, v[u][h].w));
+            }
+            KVf mv;
+            mv.x = m[0]; mv.y = m[1];
+            if constexpr (KV == 4) { mv.z = m[2]; mv.w = m[3]; }
+            if constexpr (GLOBAL) __stcg(kv + tid + (q0 + u) * NT, mv);
+            else kv[tid + (q0 + u) * NT] = mv;
+#pragma unroll
+            for (int j = 0; j < KV; ++j) {
+                const unsigned k = __float_as_uint(m[j]);
+                if (k) kmn = min(kmn, k);
+                kmx = max(kmx, k);
+            }
         }
         if (w0) {
 #pragma unroll
-            for (int u = 0; u < LB; ++u) {
-                const C wv = w0[e0 + u * NT];
-                const double dx = (double)v[u].x - (double)wv.x, dy = (double)v[u].y - (double)wv.y;
-                err += dx * dx + dy * dy;
-                ref += (double)wv.x * (double)wv.x + (double)wv.y * (double)wv.y;
-            }
+            for (int u = 0; u < QB; ++u)
+#pragma unroll
+                for (int h = 0; h < HV; ++h) {
+                    const float4 wv = w04[HV * (tid + (q0 + u) * NT) + h], rv = v[u][h];
+                    const double dx = (double)rv.x - (double)wv.x, dy = (double)rv.y - (double)wv.y;
+                    const double ex = (double)rv.z - (double)wv.z, ey = (double)rv.w - (double)wv.w;
+                    err += dx * dx + dy * dy;
+                    ref += (double)wv.x * (double)wv.x + (double)wv.y * (double)wv.y;
+                    err += ex * ex + ey * ey;
+                    ref += (double)wv.z * (double)wv.z + (double)wv.w * (double)wv.w;
+                }
         }
     };
     if constexpr (EF == 0) {
 #pragma unroll 4
-        for (int e0 = tid; e0 < ef * NT; e0 += LB * NT) load_keys(e0);
+        for (int q0 = 0; q0 < ef / KV; q0 += QB) load_keys(q0);
     } else {
 #pragma unroll 1
-        for (int e0 = tid; e0 < EF * NT; e0 += LB * NT) load_keys(e0);
+        for (int q0 = 0; q0 < EF / KV; q0 += QB) load_keys(q0);
     }
     __syncthreads();
     if (!a.tau_in && tid == 0) {
