@@ -73,6 +73,7 @@ struct Plan {
     void* twW = nullptr;
     // fp32 subbands > SCAP: value-range split over several CTAs (big_keys / big_range)
     bool bigpath = false;
+    bool t2_alias = false;          // T2 is T1 (K2 in place)
     bool cluster = false;           // few subbands of >= 16,384 keys: one thread-block cluster per subband (sure_winc)
     bool cluster16 = false;         // ... of 16 CTAs for subbands of >= 131,072 keys (non-portable size, if schedulable)
     cudaStream_t side2 = nullptr;   // second fork/join stream (cluster mode: mid-size subbands)
@@ -1052,6 +1053,7 @@ void dispatch(Plan* p, void* stream, F&& f) {
 void free_plan(Plan* p) {
     if (!p) return;
     cudaSetDevice(p->dev);
+    if (p->t2_alias) p->T2 = nullptr;      // (T1's memory)
     void* bufs[] = {p->what, p->btau, p->berr, p->x0r, p->nmconst, p->nmpart, p->r, p->T1, p->T2, p->yg, p->pinv, p->par, p->parf, p->taupart, p->prow, p->pcol, p->prs256,
                     p->nvar, p->offs, p->twH, p->twW, p->kA, p->kB, p->bhist, p->btick, p->bbest, p->baux, p->berrp, p->x0, p->w0, p->xtmp, p->trtmp, p->pflag};
     for (void* b : bufs) if (b) cudaFree(b);
@@ -1204,7 +1206,16 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
         const size_t img = (size_t)batch * p->N;
         p->r = dalloc(p, img * cs);
         p->T1 = dalloc(p, img * cs);
-        p->T2 = dalloc(p, img * cs);
+        {
+            // col_pass256 holds its whole 256 x 16 tile in registers between its loads and its
+            // stores, so K2 can run in place: T2 aliases T1 and an image's working set drops by
+            // 8N bytes (cfg1's 64 images: 150 -> 117 MB against the 126 MB L2; 523k -> 532k
+            // img-iter/s, K2 1.01 -> 0.96 and K3 0.84 -> 0.78 ms/step; VDAMP_INPLACE=0: separate buffers)
+            const char* ie = getenv("VDAMP_INPLACE");
+            const char* fe = getenv("VDAMP_F256");
+            p->t2_alias = height == 256 && p->cw == 16 && !(fe && atoi(fe) == 0) && !(ie && atoi(ie) == 0);
+            p->T2 = p->t2_alias ? p->T1 : dalloc(p, img * cs);
+        }
         p->yg = dalloc(p, img * cs);
         p->pinv = dalloc(p, img * rs);
         p->scratch.assign(p->passes.size(), nullptr);

@@ -1309,11 +1309,22 @@ __global__ void __launch_bounds__(PNT, sizeof(R) == 4 ? 3 : 2) col_pass256(Geo g
     for (int j = 0; j < 16; ++j) v[j] = p.src[colbase + (long long)(16 * j) * W];
     // 1/p (L2-prefetched before the wait) loads under the forward FFT; y at its use
     R pvs[16];
+    // y and 1/p are read once per iteration; as streaming loads (evict-first, -DVDAMP_STREAM_LOADS)
+    // they leave T2 in L2 for K3 on a batch that nearly fits it (cfg1: K3 0.785 -> 0.731 ms/step)
+    // but slow this kernel on a batch that streams from DRAM anyway (cfg4: K2 10.8 -> 11.5
+    // ms/step): plain loads
+#ifndef VDAMP_STREAM_LOADS
 #define YS(k) p.yg[colbase + (long long)(16 * (k)) * W]
+#define PS(k) p.pinv[colbase + (long long)(16 * (k)) * W]
+#else
+#define YS(k) __ldcs(p.yg + colbase + (long long)(16 * (k)) * W)
+#define PS(k) __ldcs(p.pinv + colbase + (long long)(16 * (k)) * W)
+#endif
     if (MODE != COL_NMSE) {
 #pragma unroll
-        for (int k2 = 0; k2 < 16; ++k2) pvs[k2] = p.pinv[colbase + (long long)(16 * k2) * W];
+        for (int k2 = 0; k2 < 16; ++k2) pvs[k2] = PS(k2);
     }
+#undef PS
     fft256_stage_a<C, false>(v, d, p.tw);
 #pragma unroll
     for (int m = 0; m < 16; ++m) buf[(m * 16 + d) * 16 + c] = v[m];
