@@ -813,7 +813,8 @@ struct Seq {
                 auto k = sure_win_full;
                 set_smem(k, sm);
                 const int pairs = p->B * (int)win_items.size();
-                launch(k, dim3((unsigned)std::max(1, std::min(p->nsm, pairs))), 512, sm, st_, p->geo, a, p->B,
+                static const int fctas = [] { const char* e = getenv("VDAMP_WINFULL_CTAS"); return e ? atoi(e) : 0; }();
+                launch(k, dim3((unsigned)std::max(1, std::min(fctas > 0 ? fctas : p->nsm, pairs))), 512, sm, st_, p->geo, a, p->B,
                        (int)win_items.size());
                 a.only = nullptr;
             }
