@@ -137,8 +137,8 @@ struct Plan {
     int lanes = 1;
     int Ball = 0;                    // images of the whole plan (a lane view's B is its own range)
     struct Lane {
-        cudaStream_t st = nullptr, side = nullptr;
-        cudaEvent_t fork = nullptr, join = nullptr, done = nullptr;
+        cudaStream_t st = nullptr, side = nullptr, side2 = nullptr;
+        cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr, done = nullptr;
         cudaEvent_t nm0 = nullptr, nmr = nullptr, nmd = nullptr;
     };
     // per-iteration NMSE beside the next iteration (Seq::nmse_iter): events "thresholds ready",
@@ -771,7 +771,11 @@ struct Seq {
                         cudaStream_t lw = ls;
                         if (can_fork && (n != 16384 || has_large)) { fork(); lw = p->side; }
                         // cluster mode (few CTAs, latency-bound): beside the small-subband kernel too
-                        if (lw == p->side && p->cluster && p->side2 && !forked2) {
+                        // the 4,096-key launch beside the small-subband kernel, not behind it (the side
+                        // chain small -> 4,096-key was as long as the 16,384-key launch on the main
+                        // stream: cfg1 530k -> 556k img-iter/s, cfg2 111.6k -> 115.0k; VDAMP_SIDE2=0: one side stream)
+                        static const int s2all = [] { const char* e = getenv("VDAMP_SIDE2"); return e ? atoi(e) : 1; }();
+                        if (lw == p->side && (p->cluster || s2all) && p->side2 && !forked2) {
                             CK(cudaStreamWaitEvent(p->side2, p->ev_fork, 0));
                             lw = p->side2;
                             forked2 = true;
@@ -1009,6 +1013,8 @@ void set_lanes(Plan* p, int nl) {
         Plan::Lane l;
         CK(cudaStreamCreateWithFlags(&l.st, cudaStreamNonBlocking));
         l.side = create_side_stream();
+        l.side2 = create_side_stream();
+        CK(cudaEventCreateWithFlags(&l.join2, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&l.fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&l.join, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming));
@@ -1070,7 +1076,7 @@ void free_plan(Plan* p) {
     if (p->ev_out) cudaEventDestroy(p->ev_out);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     for (auto& l : p->lane) {
-        cudaStreamDestroy(l.st); cudaStreamDestroy(l.side);
+        cudaStreamDestroy(l.st); cudaStreamDestroy(l.side); cudaStreamDestroy(l.side2); cudaEventDestroy(l.join2);
         cudaEventDestroy(l.fork); cudaEventDestroy(l.join); cudaEventDestroy(l.done);
         cudaEventDestroy(l.nm0); cudaEventDestroy(l.nmr); cudaEventDestroy(l.nmd);
     }
@@ -1250,9 +1256,9 @@ int vdamp_plan_create(int height, int width, int scales, int batch, int precisio
                          (maxlen >= 65536 ? ctas <= 3LL * p->nsm : 3 * ctas <= 2LL * p->nsm);
             if (precision == VDAMP_FP32 && nbig > 0 && ce && atoi(ce) == 1) p->cluster = true;    // forced (A/B runs)
             if (p->cluster && maxlen <= capk) p->kA = dalloc(p, img * rs);      // the clusters' key scratch
+            p->side2 = create_side_stream();
+            CK(cudaEventCreateWithFlags(&p->ev_join2, cudaEventDisableTiming));
             if (p->cluster) {
-                p->side2 = create_side_stream();
-                CK(cudaEventCreateWithFlags(&p->ev_join2, cudaEventDisableTiming));
                 // 16-CTA clusters (non-portable size) for the largest subbands, if the device can
                 // place one with this kernel's shared memory
                 // (measured slower: 104 vs 80 us for a 262,144-key subband, cfg3 5.3k vs 5.5k
@@ -1573,7 +1579,7 @@ Plan lane_view(const Plan* p, int b0, int nb, const Plan::Lane& l) {
     v.B = nb;
     v.side = l.side; v.ev_fork = l.fork; v.ev_join = l.join;
     v.ev_nm0 = l.nm0; v.ev_nmr = l.nmr; v.ev_nmd = l.nmd; v.nm_pending = false;
-    v.side2 = nullptr;                 // (one per plan: lanes keep their clusters on their own stream)
+    v.side2 = l.side2; v.ev_join2 = l.join2;
     v.ev.clear();
     v.lane.clear(); v.lanes = 1;
     return v;
