@@ -184,7 +184,7 @@ VDAMP_API int vdamp_set_graphs(vdamp_plan_t plan, int enable);
  * and joined back into the caller's stream, launched iteration-major (every lane
  * gets iteration k before any lane gets k+1; env VDAMP_INTERLEAVE=0: lane-major).
  * When graphs are on, the fork/join is captured into the graph.  Results are
- * identical for any lane count (images are independent).  Default min(4, batch / 16) (1 from 256 images), env VDAMP_LANES overrides;
+ * identical for any lane count (images are independent).  Default min(4, batch / 16) (2 from 128 images, 1 from 256), env VDAMP_LANES overrides;
  * lanes = 0 restores the default. */
 VDAMP_API int vdamp_set_lanes(vdamp_plan_t plan, int lanes);
 /* Per-iteration device time of vdamp_run (the reference records each iteration's own

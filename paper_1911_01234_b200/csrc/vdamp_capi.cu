@@ -992,7 +992,8 @@ struct Seq {
 // cfg4, 1024 x 256^2: 1 / 2 / 4 / 8 lanes 466k / 458k / 447k / 433k; cfg2, 32 x 512^2:
 // 1 / 2 / 4 lanes 41.1k / 43.8k / 41.6k img-iter/s); VDAMP_LANES overrides
 int default_lanes(int batch) {
-    int nl = batch >= 256 ? 1 : std::max(1, std::min(4, batch / 16));
+    // (session 5, 128 x 256^2: 1 / 2 / 4 lanes 538k / 565k / 523k; 256 images: 606k / 589k / 518k)
+    int nl = batch >= 256 ? 1 : batch >= 128 ? 2 : std::max(1, std::min(4, batch / 16));
     if (const char* le = getenv("VDAMP_LANES")) nl = atoi(le);
     return nl;
 }
