@@ -576,6 +576,29 @@ struct Seq {
         a.w0 = use_w0 ? (const C*)p->w0 : nullptr;
         a.kA = (R*)p->kA; a.kB = (R*)p->kB;
         a.prune = p->prune;
+        a.cond = 0;
+        // Captured run (CUDA graph), optional: the flag-scan launch after the sure_win32 kernels becomes
+        // the body of a conditional IF node whose handle the flagging kernels set, so a run in which
+        // nothing is flagged (the normal case) does not pay that launch between K4 and the next K1.
+        cudaGraph_t cgraph = nullptr;
+        if constexpr (std::is_same<R, float>::value) {
+            // Measured on cfg1: one batch at a time 557k -> 580k img-iter/s (device-resident) and 437k ->
+            // 451k (synchronous calls), but back-to-back graph launches of the streaming API 538k -> 531k
+            // (graphs with conditional nodes start later behind one another), 16 / 32 images 284k ->
+            // 275k / 425k -> 411k, one image 16.4k -> 15.3k.  Off unless VDAMP_CONDNODE=1.
+            static const int condenv = [] { const char* e = getenv("VDAMP_CONDNODE"); return e ? atoi(e) : 0; }();
+            const bool condon = condenv != 0;
+            cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+            if (condon && !p->timing && cudaStreamIsCapturing(st_, &cst) == cudaSuccess && cst == cudaStreamCaptureStatusActive) {
+                unsigned long long cid = 0;
+                const cudaGraphNode_t* deps = nullptr;
+                size_t nd = 0;
+                CK(cudaStreamGetCaptureInfo(st_, &cst, &cid, &cgraph, &deps, &nd));
+                cudaGraphConditionalHandle h;
+                CK(cudaGraphConditionalHandleCreate(&h, cgraph, 0, cudaGraphCondAssignDefault));
+                a.cond = (unsigned long long)h;
+            }
+        }
         // big subbands: 1024-thread CTAs with the full sort workspace; small ones:
         // 128-thread CTAs with little shared memory, many per SM
         // the small-subband kernel runs on a side stream, concurrently with the
@@ -818,8 +841,38 @@ struct Seq {
                 set_smem(k, sm);
                 const int pairs = p->B * (int)win_items.size();
                 static const int fctas = [] { const char* e = getenv("VDAMP_WINFULL_CTAS"); return e ? atoi(e) : 0; }();
-                launch(k, dim3((unsigned)std::max(1, std::min(fctas > 0 ? fctas : p->nsm, pairs))), 512, sm, st_, p->geo, a, p->B,
-                       (int)win_items.size());
+                const dim3 fgrid((unsigned)std::max(1, std::min(fctas > 0 ? fctas : p->nsm, pairs)));
+                if (a.cond && cgraph) {
+                    cudaStreamCaptureStatus cst;
+                    unsigned long long cid = 0;
+                    const cudaGraphNode_t* deps = nullptr;
+                    size_t nd = 0;
+                    CK(cudaStreamGetCaptureInfo(st_, &cst, &cid, &cgraph, &deps, &nd));
+                    cudaGraphNodeParams np = {};
+                    np.type = cudaGraphNodeTypeConditional;
+                    np.conditional.handle = (cudaGraphConditionalHandle)a.cond;
+                    np.conditional.type = cudaGraphCondTypeIf;
+                    np.conditional.size = 1;
+                    cudaGraphNode_t cnode;
+                    CK(cudaGraphAddNode(&cnode, cgraph, deps, nd, &np));
+                    cudaGraph_t body = np.conditional.phGraph_out[0];
+                    Geo garg = p->geo;
+                    SelArgs<R> aarg = a;
+                    int Barg = p->B, narg = (int)win_items.size();
+                    void* kargs[] = {&garg, &aarg, &Barg, &narg};
+                    cudaKernelNodeParams kp = {};
+                    kp.func = (void*)k;
+                    kp.gridDim = fgrid;
+                    kp.blockDim = dim3(512);
+                    kp.sharedMemBytes = (unsigned)sm;
+                    kp.kernelParams = kargs;
+                    kp.extra = nullptr;
+                    cudaGraphNode_t kn;
+                    CK(cudaGraphAddKernelNode(&kn, body, nullptr, 0, &kp));
+                    CK(cudaStreamUpdateCaptureDependencies(st_, &cnode, 1, cudaStreamSetCaptureDependencies));
+                } else {
+                    launch(k, fgrid, 512, sm, st_, p->geo, a, p->B, (int)win_items.size());
+                }
                 a.only = nullptr;
             }
             if (!win_large.empty() && wfull) {

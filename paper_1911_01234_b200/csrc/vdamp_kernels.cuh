@@ -1643,6 +1643,7 @@ struct SelArgs {
     int prune;                       // bound-pruned exact selection (vdamp_prune.cuh): bit 0 4096..SCAP keys, bit 1 larger
     unsigned* pflag;                 // [B][S] fallback flags of sure_prune32 (1 = sort fully)
     const unsigned* only;            // non-null: process only the items flagged here
+    unsigned long long cond;         // CUDA-graph conditional handle of the flag-scan launch (0: none): set to 1 by a kernel that flags
     int item_start[MAXS + 1];        // work items: subbands item_list[item_start[i] .. item_start[i+1])
     int item_list[MAXS];
 };

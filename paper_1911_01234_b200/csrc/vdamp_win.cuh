@@ -816,7 +816,11 @@ __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 1024 / NT) sure_win32(con
     for (int q = a.item_start[it]; q < a.item_start[it + 1]; ++q) {
         const int j = a.item_list[q];
         const bool ok = win_band<NT, EF, GLOBAL>(g, a, j, bi, keys, S_);
-        if (threadIdx.x == 0) a.pflag[(long long)bi * g.S + j] = ok ? 0u : 1u;
+        if (threadIdx.x == 0) {
+            a.pflag[(long long)bi * g.S + j] = ok ? 0u : 1u;
+            // captured run: the flag-scan launch is the body of a conditional node, run only if set
+            if (!ok && a.cond) cudaGraphSetConditional((cudaGraphConditionalHandle)a.cond, 1u);
+        }
         __syncthreads();
     }
 }
@@ -842,7 +846,10 @@ __global__ void __launch_bounds__(NT, 1) sure_winc(const __grid_constant__ Geo g
         const int j = a.item_list[q];
         if (q > a.item_start[it]) ::cooperative_groups::this_cluster().sync();     // X and the lists are reused
         const bool ok = win_band<NT, EF, true, CS>(g, a, j, bi, keys, S_, &X);
-        if (crank == 0 && threadIdx.x == 0) a.pflag[(long long)bi * g.S + j] = ok ? 0u : 1u;
+        if (crank == 0 && threadIdx.x == 0) {
+            a.pflag[(long long)bi * g.S + j] = ok ? 0u : 1u;
+            if (!ok && a.cond) cudaGraphSetConditional((cudaGraphConditionalHandle)a.cond, 1u);
+        }
         __syncthreads();
     }
 }

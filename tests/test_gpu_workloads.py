@@ -189,6 +189,33 @@ def test_parseval_nmse_matches_finalize_path(cfg0_small):
     assert np.abs(out["1"] - out["0"]).max() <= 1e-8
 
 
+@pytest.mark.parametrize("batch", [2, 8])
+def test_flagged_subbands_inside_a_captured_run(batch):
+    """A captured run (CUDA graph) makes the fallback-flag scan the body of a conditional node
+    that the flagging kernel sets.  Images with all-zero measurements (every key zero: every
+    large subband is flagged in every iteration) next to ordinary ones must give bitwise the
+    results of direct launches, with the conditional node, with the plain launch inside the
+    graph, and for the cluster kernels of small batches."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); "
+            "from paper_1911_01234_b200 import vdamp, workload; w = workload.make_workload('cfg1', batch=%d); "
+            "ys = [y if i %% 2 else np.zeros_like(y) for i, y in enumerate(w.ys)]; "
+            "x, tr = vdamp.run_batch(ys, w.masks, w.pmap, w.noise_vars, 4, 6, precision='fp32'); "
+            "assert np.isfinite(x).all() and np.abs(x[0]).max() == 0.0 and np.abs(x[1]).max() > 0.0; "
+            "print(repr([float(np.abs(x).sum()), float(x.real.sum()), float(x.imag.sum())] + "
+            "[float(r.thresholds.sum()) for t in tr for r in t.records]))"
+            ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), batch)
+    out = []
+    for graphs, cond in (("0", "0"), ("1", "0"), ("1", "1")):
+        env = dict(os.environ, VDAMP_GRAPHS=graphs, VDAMP_CONDNODE=cond)
+        res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+        assert res.returncode == 0, res.stderr[-2000:]
+        out.append(eval(res.stdout.strip().splitlines()[-1]))
+    assert out[0] == out[1] == out[2]
+
+
 @pytest.mark.parametrize("precision,graphs", [("fp32", "0"), ("fp32", "1"), ("fp64", "1")])
 def test_nmse_beside_next_iteration_is_bitwise(precision, graphs):
     """The per-iteration NMSE pass run on the side stream beside K1 / K2 of the next iteration
